@@ -1,0 +1,396 @@
+"""paper_2111_05426_b200 -- B200-native DistIR grid-search simulator pass.
+
+Thin Python binding over ``libdistir.so`` (C ABI in ``include/distir.h``).
+This module only marshals arguments: every step of the path (enumerate,
+expand, cost, timeline, memory, feasibility, top-k, merge) runs in the CUDA
+kernels of ``csrc/``.  PyTorch is used for device memory (the workspace and
+device output tensors), streams and process groups.  There is no CPU
+fallback: if the shared library is missing, importing the binding raises.
+
+The function names are the C names (``distir_sim_create`` ...); ``Simulator``
+is a convenience wrapper that owns a handle and a workspace.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(_HERE)
+SO_PATH = os.path.join(_HERE, "libdistir.so")
+SOURCES = [os.path.join(_HERE, "csrc", f)
+           for f in ("distir.cu", "kernels.cuh", "common.cuh")] + [
+    os.path.join(ROOT, "include", "distir.h")]
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
+              "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libdistir.so for sm_100a in-tree (nvcc cross-compiles here)."""
+    newest = max(os.path.getmtime(s) for s in SOURCES)
+    if force or not os.path.exists(SO_PATH) or os.path.getmtime(SO_PATH) < newest:
+        cmd = ["nvcc"] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + [
+            "-o", SO_PATH, os.path.join(_HERE, "csrc", "distir.cu"), "-ldl"]
+        subprocess.check_call(cmd)
+    return SO_PATH
+
+
+# ------------------------------------------------------------ C structs -----
+
+class distir_model(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
+        "n_ctx", "dtype_bytes", "id_bytes", "lm_head")]
+
+
+class distir_topology(ctypes.Structure):
+    _fields_ = [("world_max", ctypes.c_int32), ("node_size", ctypes.c_int32),
+                ("flops_per_s", ctypes.c_double),
+                ("op_overhead_s", ctypes.c_double),
+                ("alpha_intra_s", ctypes.c_double),
+                ("bw_intra_Bps", ctypes.c_double),
+                ("alpha_inter_s", ctypes.c_double),
+                ("bw_inter_Bps", ctypes.c_double),
+                ("capacity_bytes", ctypes.c_int64)]
+
+
+class distir_config(ctypes.Structure):
+    _fields_ = [("dp", ctypes.c_int32), ("tp", ctypes.c_int32),
+                ("pp", ctypes.c_int32), ("microbatches", ctypes.c_int32),
+                ("batch", ctypes.c_int64), ("model", ctypes.c_int32),
+                ("topo", ctypes.c_int32)]
+
+
+class distir_grid_spec(ctypes.Structure):
+    _fields_ = [("n_world", ctypes.c_int32), ("world", ctypes.c_int32 * 8),
+                ("k_mode", ctypes.c_int32), ("n_k", ctypes.c_int32),
+                ("k_set", ctypes.c_int32 * 16), ("n_batch", ctypes.c_int32),
+                ("batch", ctypes.c_int64 * 32), ("n_models", ctypes.c_int32),
+                ("models", ctypes.c_int32 * 8), ("n_topos", ctypes.c_int32),
+                ("topos", ctypes.c_int32 * 8), ("dp_mask", ctypes.c_uint32),
+                ("tp_mask", ctypes.c_uint32), ("pp_mask", ctypes.c_uint32),
+                ("synth_seed", ctypes.c_uint64),
+                ("synth_count", ctypes.c_int64)]
+
+
+class distir_topk_entry(ctypes.Structure):
+    _fields_ = [("index", ctypes.c_int64), ("makespan_s", ctypes.c_double),
+                ("throughput", ctypes.c_double),
+                ("peak_bytes", ctypes.c_int64)]
+
+
+class distir_profile_data(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("kernels", ctypes.c_int64),
+                ("ms_prepare", ctypes.c_double), ("ms_simulate", ctypes.c_double),
+                ("ms_topk", ctypes.c_double), ("ms_merge", ctypes.c_double)]
+
+
+class distir_stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "n_configs", "n_valid", "n_feasible", "op_events", "stage_steps",
+        "n_buckets", "n_items", "h2d_bytes", "d2h_bytes")]
+
+
+TOPK_DTYPE = np.dtype([("index", "<i8"), ("makespan_s", "<f8"),
+                       ("throughput", "<f8"), ("peak_bytes", "<i8")])
+
+STATUS = {0: "DISTIR_OK", 1: "DISTIR_E_INVALID_ARG", 2: "DISTIR_E_UNSUPPORTED",
+          3: "DISTIR_E_OUT_OF_MEMORY", 4: "DISTIR_E_CUDA", 5: "DISTIR_E_NCCL",
+          6: "DISTIR_E_WORKSPACE"}
+
+# Every symbol include/distir.h declares (checked by the CPU tests).
+EXPORTS = ("distir_sim_create", "distir_sim_destroy", "distir_grid_size",
+           "distir_workspace_size", "distir_grid_eval", "distir_grid_upload",
+           "distir_grid_launch", "distir_last_stats", "distir_profile",
+           "distir_grid_eval_sharded", "distir_nccl_unique_id",
+           "distir_nccl_comm_init", "distir_nccl_comm_destroy",
+           "distir_shard_indices", "distir_last_error", "distir_version")
+
+
+class DistirError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(SO_PATH):
+        raise ImportError(
+            "libdistir.so not built (%s); run __graft_entry__.build() -- the "
+            "DistIR path has no CPU fallback" % SO_PATH)
+    L = ctypes.CDLL(SO_PATH)
+    vp, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    P = ctypes.POINTER
+    L.distir_last_error.restype = ctypes.c_char_p
+    L.distir_version.restype = ctypes.c_char_p
+    L.distir_sim_create.argtypes = [P(distir_model), i32, P(distir_topology), i32,
+                                    i32, vp, P(vp)]
+    L.distir_sim_destroy.argtypes = [vp]
+    L.distir_sim_destroy.restype = None
+    L.distir_grid_size.argtypes = [vp, P(distir_grid_spec), P(i64)]
+    L.distir_workspace_size.argtypes = [vp, i64, P(ctypes.c_size_t)]
+    L.distir_grid_eval.argtypes = [vp, P(distir_grid_spec), P(distir_config), i64,
+                                   i32, vp, ctypes.c_size_t, vp, vp, vp, vp,
+                                   P(i32), P(distir_stats)]
+    L.distir_grid_upload.argtypes = [vp, P(distir_grid_spec), P(distir_config), i64,
+                                     i32, i32, vp, ctypes.c_size_t, P(i64)]
+    L.distir_grid_launch.argtypes = [vp, i32, vp, vp, ctypes.c_size_t, vp, vp, vp, vp, vp]
+    L.distir_profile.argtypes = [vp, i32, P(distir_profile_data)]
+    L.distir_last_stats.argtypes = [vp, vp, P(distir_stats)]
+    L.distir_grid_eval_sharded.argtypes = [vp, P(distir_grid_spec), P(distir_config),
+                                           i64, i32, i32, vp, i32, vp, ctypes.c_size_t,
+                                           vp, vp, vp, vp, P(i32), P(distir_stats)]
+    L.distir_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.distir_nccl_comm_init.argtypes = [ctypes.c_char_p, i32, i32, i32, P(vp)]
+    L.distir_nccl_comm_destroy.argtypes = [vp]
+    L.distir_shard_indices.argtypes = [i64, i32, i32, P(i64), i64]
+    L.distir_shard_indices.restype = i64
+    for f in EXPORTS:
+        if f not in ("distir_sim_destroy", "distir_last_error", "distir_version",
+                     "distir_shard_indices"):
+            getattr(L, f).restype = ctypes.c_int
+    return L
+
+
+lib = _load()
+
+
+def _check(status):
+    if status != 0:
+        raise DistirError(status, lib.distir_last_error().decode())
+
+
+# ------------------------------------------------------ marshalling ---------
+
+def model_struct(m) -> distir_model:
+    return distir_model(*[int(m[k]) for k in (
+        "kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
+        "n_ctx", "dtype_bytes", "id_bytes", "lm_head")])
+
+
+def topo_struct(t) -> distir_topology:
+    return distir_topology(int(t["world_max"]), int(t["node_size"]),
+                           float(t["flops_per_s"]), float(t["op_overhead_s"]),
+                           float(t["alpha_intra_s"]), float(t["bw_intra_Bps"]),
+                           float(t["alpha_inter_s"]), float(t["bw_inter_Bps"]),
+                           int(t["capacity_bytes"]))
+
+
+def spec_struct(grid, model_index, topo_index) -> distir_grid_spec:
+    """workloads grid dict -> distir_grid_spec; model/topo names are mapped
+    through the handle's index dicts."""
+    s = distir_grid_spec()
+    s.n_world = len(grid["world"])
+    for i, w in enumerate(grid["world"]):
+        s.world[i] = w
+    s.k_mode = grid["k_mode"]
+    s.n_k = len(grid["k_set"])
+    for i, k in enumerate(grid["k_set"]):
+        s.k_set[i] = k
+    s.n_batch = len(grid["batch"])
+    for i, b in enumerate(grid["batch"]):
+        s.batch[i] = b
+    s.n_models = len(grid["models"])
+    for i, m in enumerate(grid["models"]):
+        s.models[i] = model_index[m]
+    s.n_topos = len(grid["topos"])
+    for i, t in enumerate(grid["topos"]):
+        s.topos[i] = topo_index[t]
+    s.dp_mask, s.tp_mask, s.pp_mask = (grid["dp_mask"], grid["tp_mask"],
+                                       grid["pp_mask"])
+    s.synth_seed = grid["synth_seed"]
+    s.synth_count = grid["synth_count"]
+    return s
+
+
+def configs_array(configs):
+    """[(model_idx, topo_idx, D, T, P, K, B)] -> ctypes array."""
+    arr = (distir_config * max(len(configs), 1))()
+    for i, (mi, ti, D, T, P, K, B) in enumerate(configs):
+        arr[i] = distir_config(D, T, P, K, B, mi, ti)
+    return arr
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+# ------------------------------------------------------------ wrapper -------
+
+class Simulator:
+    """Owns a distir_sim handle bound to one GPU and one torch stream."""
+
+    def __init__(self, models, topologies, device=0, stream=None):
+        import torch
+        self.torch = torch
+        self.model_names = list(models)
+        self.topo_names = list(topologies)
+        self.model_index = {n: i for i, n in enumerate(self.model_names)}
+        self.topo_index = {n: i for i, n in enumerate(self.topo_names)}
+        ms = (distir_model * len(models))(*[model_struct(models[n])
+                                            for n in self.model_names])
+        ts = (distir_topology * len(topologies))(
+            *[topo_struct(topologies[n]) for n in self.topo_names])
+        self.device = torch.device("cuda", device)
+        self.stream = stream or torch.cuda.current_stream(self.device)
+        h = ctypes.c_void_p()
+        _check(lib.distir_sim_create(ms, len(models), ts, len(topologies),
+                                     device, ctypes.c_void_p(self.stream.cuda_stream),
+                                     ctypes.byref(h)))
+        self.handle = h
+        self.ws = None
+
+    def close(self):
+        if self.handle:
+            lib.distir_sim_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- sizes
+    def spec(self, grid):
+        return spec_struct(grid, self.model_index, self.topo_index)
+
+    def grid_size(self, grid) -> int:
+        n = ctypes.c_int64()
+        _check(lib.distir_grid_size(self.handle, ctypes.byref(self.spec(grid)),
+                                    ctypes.byref(n)))
+        return n.value
+
+    def workspace(self, n_configs):
+        b = ctypes.c_size_t()
+        _check(lib.distir_workspace_size(self.handle, n_configs, ctypes.byref(b)))
+        if self.ws is None or self.ws.numel() < b.value:
+            self.ws = self.torch.empty(b.value, dtype=self.torch.uint8,
+                                       device=self.device)
+        return self.ws
+
+    # -- synchronous evaluation with host buffers (the e2e path)
+    def eval(self, grid=None, configs=None, k=10, per_config=True, pinned=True,
+             rank=0, n_ranks=1, comm=None):
+        torch = self.torch
+        if grid is not None:
+            sp = self.spec(grid)
+            n = self.grid_size(grid)
+            cf, ncf = None, 0
+        else:
+            sp = None
+            cf = configs_array(configs)
+            n = ncf = len(configs)
+        ws = self.workspace(n)
+        outs = {}
+        if per_config:
+            outs["makespan"] = torch.full((n,), float("nan"), dtype=torch.float64,
+                                          pin_memory=pinned)
+            outs["peak"] = torch.full((n,), -2, dtype=torch.int64, pin_memory=pinned)
+            outs["reason"] = torch.full((n,), -1, dtype=torch.int32, pin_memory=pinned)
+        topk = np.zeros(max(k, 1), dtype=TOPK_DTYPE)
+        ntopk = ctypes.c_int32()
+        st = distir_stats()
+        p = lambda name: ctypes.c_void_p(outs[name].data_ptr()) if name in outs else None
+        _check(lib.distir_grid_eval_sharded(
+            self.handle, ctypes.byref(sp) if sp is not None else None,
+            cf, ncf, rank, n_ranks, comm, k, ctypes.c_void_p(ws.data_ptr()),
+            ws.numel(), p("makespan"), p("peak"), p("reason"),
+            topk.ctypes.data_as(ctypes.c_void_p), ctypes.byref(ntopk),
+            ctypes.byref(st)))
+        res = dict(topk=topk[:ntopk.value], n=n,
+                   stats={f: getattr(st, f) for f, _ in distir_stats._fields_})
+        for name, t in outs.items():
+            res[name] = t.numpy()
+        if per_config:
+            res["reason"] = res["reason"].view(np.uint32)
+        return res
+
+    # -- device-resident pipeline (the timed `value` path)
+    def upload(self, grid=None, configs=None, rank=0, n_ranks=1):
+        if grid is not None:
+            self._sp = self.spec(grid)
+            n = self.grid_size(grid)
+            self._cf, ncf = None, 0
+        else:
+            self._sp = None
+            self._cf = configs_array(configs)
+            n = ncf = len(configs)
+        ws = self.workspace(n)
+        nl = ctypes.c_int64()
+        _check(lib.distir_grid_upload(
+            self.handle, ctypes.byref(self._sp) if self._sp is not None else None,
+            self._cf, ncf, rank, n_ranks, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+            ctypes.byref(nl)))
+        return nl.value
+
+    def device_outputs(self, n_local, k=10):
+        torch = self.torch
+        return dict(
+            makespan=torch.empty(max(n_local, 1), dtype=torch.float64, device=self.device),
+            peak=torch.empty(max(n_local, 1), dtype=torch.int64, device=self.device),
+            reason=torch.empty(max(n_local, 1), dtype=torch.int32, device=self.device),
+            topk=torch.empty((max(k, 1), 4), dtype=torch.int64, device=self.device),
+            ntopk=torch.zeros(1, dtype=torch.int32, device=self.device))
+
+    def launch(self, outs, k=10, per_config=True, comm=None):
+        ws = self.ws
+        _check(lib.distir_grid_launch(
+            self.handle, k, comm, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+            _ptr(outs["makespan"]) if per_config else None,
+            _ptr(outs["peak"]) if per_config else None,
+            _ptr(outs["reason"]) if per_config else None,
+            _ptr(outs["topk"]), _ptr(outs["ntopk"])))
+
+    def profile(self, enable=True):
+        """Kernel times (ms) accumulated since the previous call; then turn
+        CUDA-event recording on or off."""
+        pd = distir_profile_data()
+        _check(lib.distir_profile(self.handle, 1 if enable else 0, ctypes.byref(pd)))
+        return {f: getattr(pd, f) for f, _ in distir_profile_data._fields_}
+
+    def last_stats(self):
+        st = distir_stats()
+        _check(lib.distir_last_stats(self.handle, ctypes.c_void_p(self.ws.data_ptr()),
+                                     ctypes.byref(st)))
+        return {f: getattr(st, f) for f, _ in distir_stats._fields_}
+
+
+def topk_from_device(t, n):
+    """Device top-k tensor [k, 4] (int64 view of distir_topk_entry) -> numpy."""
+    a = t.cpu().numpy()[:n].copy()
+    return a.view(TOPK_DTYPE).reshape(-1)
+
+
+# ---------------------------------------------------------------- NCCL ------
+
+def distir_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.distir_nccl_unique_id(buf))
+    return buf.raw
+
+
+def distir_nccl_comm_init(uid: bytes, n_ranks: int, rank: int, device: int):
+    comm = ctypes.c_void_p()
+    _check(lib.distir_nccl_comm_init(uid, n_ranks, rank, device, ctypes.byref(comm)))
+    return comm
+
+
+def distir_nccl_comm_destroy(comm):
+    _check(lib.distir_nccl_comm_destroy(comm))
+
+
+def distir_shard_indices(n_configs: int, rank: int, n_ranks: int) -> np.ndarray:
+    n = lib.distir_shard_indices(n_configs, rank, n_ranks, None, 0)
+    out = np.zeros(max(n, 1), dtype=np.int64)
+    lib.distir_shard_indices(n_configs, rank, n_ranks,
+                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n)
+    return out[:n]
+
+
+def distir_version() -> str:
+    return lib.distir_version().decode()

@@ -1,0 +1,106 @@
+// common.cuh -- device-side data layout of the DistIR grid pass (product).
+//
+// Everything the kernels read lives in the caller-owned workspace (HBM):
+//   WsHeader | SpecBlock | explicit configs | bucket table | per-config
+//   bucket ids | permutation | work items | per-config results | top-k
+// Offsets are computed by the host planner (distir.cu, ws_layout()).
+#pragma once
+#include <cstdint>
+
+namespace distir {
+
+constexpr int kMaxModels = 64;      // models / topologies copied at create
+constexpr int kMaxTopos = 64;
+constexpr int kMaxEntries = 96;     // (W, D, T, P) triples of a grid spec
+constexpr int kMaxWorld = 64;       // world size limit (2 stages per lane)
+constexpr int kMaxK = 64;           // top-k width
+constexpr int kMaxRanks = 8;        // GPUs merged by the all-gather
+constexpr int kNumBuckets = 4096;   // hash slots for warp-shape buckets
+constexpr int kOverflowBucket = kNumBuckets;  // catch-all (1 config / warp)
+constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
+constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
+constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
+constexpr int kTopkBlocks = 296;    // partial top-k blocks (2 per SM)
+
+enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };
+
+struct DModel {          // distir_model, int32
+  int32_t kind, L, d, h, S, V, nctx, e, ide, lm;
+};
+
+struct DTopo {           // distir_topology
+  int32_t world_max, node_size;
+  double F, o, a_intra, bw_intra, a_inter, bw_inter;
+  int64_t capacity;
+};
+
+struct DEntry {          // one (D, T, P) triple of the grid, canonical order
+  int32_t D, T, P, nK;
+  int64_t cum;           // configs of this (model, topo) before this entry
+};
+
+struct DExplicit {       // distir_config (32 bytes, same layout)
+  int32_t dp, tp, pp, K;
+  int64_t B;
+  int32_t model, topo;
+};
+
+struct SpecBlock {
+  int32_t mode;
+  int32_t n_models, n_topos;          // spec lists (grid / synth)
+  int32_t model_ids[8], topo_ids[8];
+  int32_t n_entries;
+  DEntry entries[kMaxEntries];
+  int32_t k_mode, n_k;
+  int32_t k_set[16];
+  int32_t n_batch;
+  int64_t batch[32];
+  int64_t per_mt;                     // configs per (model, topo) pair
+  uint64_t synth_seed;
+  int64_t n_total;                    // configs of the whole grid
+  int32_t rank, n_ranks;              // shard: global i = rank + q * n_ranks
+  int64_t n_local;
+  DModel models[kMaxModels];          // handle tables
+  DTopo topos[kMaxTopos];
+};
+
+struct WsHeader {
+  unsigned long long item_counter;    // persistent-kernel work queue
+  unsigned int n_items;
+  unsigned int n_buckets;
+  unsigned long long op_events;
+  unsigned long long stage_steps;
+  unsigned long long n_valid;
+  unsigned long long n_feasible;
+  unsigned int class_items[kNumClasses];
+  unsigned int class_base[kNumClasses];
+  unsigned int cfg_total;
+  unsigned int pad;
+};
+
+struct Bucket {          // per hash slot (plus one overflow slot)
+  uint32_t key;          // kind | (P-1) << 1 | (L-1) << 7 | min(K,255) << 17
+  uint32_t count;        // configs in the bucket
+  uint32_t cfg_base;     // first position in perm
+  uint32_t item_base;    // first work item
+  uint32_t cursor;       // scatter cursor
+  uint32_t lanes;        // lanes per config S (power of two <= 32)
+  uint32_t cls;          // weight class
+  uint32_t item_off;     // offset within class
+};
+
+struct Item {            // one warp's worth of configs of one bucket
+  uint32_t first;        // position in perm
+  uint16_t bucket;
+  uint8_t n;             // configs in this item
+  uint8_t pad;
+};
+
+struct TopkRec {         // == distir_topk_entry
+  int64_t index;
+  double makespan;
+  double throughput;
+  int64_t peak;
+};
+
+}  // namespace distir

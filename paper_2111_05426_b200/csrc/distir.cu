@@ -1,0 +1,723 @@
+// distir.cu -- libdistir.so: C ABI (include/distir.h) + host planner.
+//
+// The host side only validates arguments, lays out the caller's workspace,
+// builds the grid decode table (<= 96 entries), uploads it, and launches the
+// kernels of kernels.cuh on the caller's stream.  Every step of the method
+// (enumerate, expand, cost, timeline, memory, feasibility, top-k, merge) runs
+// on the GPU; there is no CPU fallback.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/distir.h"
+#include "kernels.cuh"
+
+using namespace distir;
+
+static_assert(sizeof(distir_topk_entry) == sizeof(TopkRec), "top-k record layout");
+static_assert(sizeof(distir_config) == sizeof(DExplicit), "config layout");
+
+namespace {
+
+thread_local std::string g_err;
+
+distir_status fail(distir_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(DISTIR_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int ilog2(int64_t x) {
+  int e = 0;
+  while ((int64_t(1) << (e + 1)) <= x) e++;
+  return e;
+}
+
+// ------------------------------------------------------------ layout -------
+struct Layout {
+  size_t hdr, spec, ex, bk, cfg_bucket, perm, items, ms, pk, rs, tp, part, part_n, gath, fin,
+      fin_n, out, out_n, total;
+};
+
+Layout layout(int64_t n_local, int64_t n_explicit) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t n = (size_t)(n_local > 0 ? n_local : 1);
+  L.hdr = take(sizeof(WsHeader));
+  L.spec = take(sizeof(SpecBlock));
+  L.ex = take((size_t)(n_explicit > 0 ? n_explicit : 1) * sizeof(DExplicit));
+  L.bk = take((kNumBuckets + 1) * sizeof(Bucket));
+  L.cfg_bucket = take(n * 4);
+  L.perm = take(n * 4);
+  L.items = take(n * sizeof(Item));
+  L.ms = take(n * 8);
+  L.pk = take(n * 8);
+  L.rs = take(n * 4);
+  L.tp = take(n * 8);
+  L.part = take((size_t)kTopkBlocks * kMaxK * sizeof(TopkRec));
+  L.part_n = take((size_t)kTopkBlocks * 4);
+  L.gath = take((size_t)kMaxRanks * kMaxK * sizeof(TopkRec));
+  L.fin = take((size_t)kMaxK * sizeof(TopkRec));
+  L.fin_n = take(16);
+  L.out = take((size_t)kMaxK * sizeof(TopkRec));
+  L.out_n = take(16);
+  L.total = off;
+  return L;
+}
+
+// ------------------------------------------------------------ NCCL ---------
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { api.why = "dlopen(libnccl.so.2) failed"; return; }
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy;
+    if (!api.ok) api.why = "NCCL symbols missing";
+  });
+  return api;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- handle ------
+struct distir_sim {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<DModel> models;
+  std::vector<DTopo> topos;
+  int num_sms = 0;
+  int sim_grid = 0;
+  int enum_grid = 0;
+  SpecBlock spec{};
+  bool uploaded = false;
+  const void* uploaded_ws = nullptr;
+  int64_t h2d = 0, d2h = 0;      // bytes copied by the last upload / eval
+  // profiling (distir_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;   // 5 per recorded launch
+  size_t ev_used = 0;            // launches recorded in ev
+  distir_profile_data acc{};     // totals folded in from ev
+  int64_t kernels = 0, launches = 0;
+  ~distir_sim() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+distir_status check_handle(const distir_sim* sim) {
+  if (!sim) return fail(DISTIR_E_INVALID_ARG, "sim is NULL");
+  return DISTIR_OK;
+}
+
+distir_status validate_model(const distir_model& m, int i) {
+  auto bad = [&](const char* what) {
+    return fail(DISTIR_E_INVALID_ARG, "model " + std::to_string(i) + ": " + what);
+  };
+  if (m.kind != DISTIR_MODEL_MLP_TRAIN && m.kind != DISTIR_MODEL_GPT2_INFER) return bad("kind");
+  if (m.n_layer < 1 || m.d_model < 1 || m.dtype_bytes < 1) return bad("n_layer/d_model/dtype_bytes");
+  if (m.n_layer > 1024) return fail(DISTIR_E_UNSUPPORTED, "n_layer > 1024");
+  if (m.d_model > (1 << 20)) return fail(DISTIR_E_UNSUPPORTED, "d_model > 2^20");
+  if (m.kind == DISTIR_MODEL_GPT2_INFER) {
+    if (m.n_head < 1 || m.seq_len < 1 || m.vocab_pad < 1 || m.n_ctx < 0 || m.id_bytes < 1)
+      return bad("n_head/seq_len/vocab_pad/n_ctx/id_bytes");
+  }
+  return DISTIR_OK;
+}
+
+distir_status validate_topo(const distir_topology& t, int i) {
+  auto bad = [&](const char* what) {
+    return fail(DISTIR_E_INVALID_ARG, "topology " + std::to_string(i) + ": " + what);
+  };
+  if (t.world_max < 1) return bad("world_max");
+  if (!is_pow2(t.node_size)) return fail(DISTIR_E_UNSUPPORTED, "node_size must be a power of two");
+  if (!(t.flops_per_s > 0) || !(t.bw_intra_Bps > 0) || !(t.bw_inter_Bps > 0)) return bad("rates");
+  if (!(t.op_overhead_s >= 0) || !(t.alpha_intra_s >= 0) || !(t.alpha_inter_s >= 0))
+    return bad("overheads");
+  if (t.capacity_bytes < 0) return bad("capacity");
+  return DISTIR_OK;
+}
+
+// Largest per-op integer work must fit in int64 (checked with 128-bit math):
+// MLP 4 m d^2, GPT-2 2 n d V and the n V e gathered logits.
+bool work_fits(const DModel& M, int64_t B) {
+  const __int128 d = M.d, b = B;
+  __int128 w;
+  if (M.kind == 0) {
+    w = 4 * b * d * d;
+  } else {
+    const __int128 n = b * M.S;
+    w = 2 * n * d * ((__int128)M.V + 4 * d) + n * M.V * M.e;
+  }
+  return w < ((__int128)1 << 62);
+}
+
+// Build the SpecBlock for a grid spec (host, O(#triples)).
+distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecBlock& sp,
+                         int64_t& n_total) {
+  std::memset(&sp, 0, sizeof(sp));
+  for (size_t i = 0; i < sim->models.size(); i++) sp.models[i] = sim->models[i];
+  for (size_t i = 0; i < sim->topos.size(); i++) sp.topos[i] = sim->topos[i];
+  if (g->n_topos < 1 || g->n_topos > 8) return fail(DISTIR_E_INVALID_ARG, "spec.n_topos");
+  for (int i = 0; i < g->n_topos; i++) {
+    if (g->topos[i] < 0 || g->topos[i] >= (int)sim->topos.size())
+      return fail(DISTIR_E_INVALID_ARG, "spec.topos index");
+    sp.topo_ids[i] = g->topos[i];
+  }
+  sp.n_topos = g->n_topos;
+  if (g->synth_count > 0) {
+    if (g->synth_count > (int64_t(1) << 31) - 1) return fail(DISTIR_E_UNSUPPORTED, "synth_count");
+    sp.mode = MODE_SYNTH;
+    sp.synth_seed = g->synth_seed;
+    n_total = g->synth_count;
+    return DISTIR_OK;
+  }
+  sp.mode = MODE_GRID;
+  if (g->n_models < 1 || g->n_models > 8) return fail(DISTIR_E_INVALID_ARG, "spec.n_models");
+  for (int i = 0; i < g->n_models; i++) {
+    if (g->models[i] < 0 || g->models[i] >= (int)sim->models.size())
+      return fail(DISTIR_E_INVALID_ARG, "spec.models index");
+    sp.model_ids[i] = g->models[i];
+  }
+  sp.n_models = g->n_models;
+  if (g->n_world < 1 || g->n_world > 8) return fail(DISTIR_E_INVALID_ARG, "spec.n_world");
+  if (g->n_batch < 1 || g->n_batch > 32) return fail(DISTIR_E_INVALID_ARG, "spec.n_batch");
+  if (g->n_k < 0 || g->n_k > 16) return fail(DISTIR_E_INVALID_ARG, "spec.n_k");
+  if (g->k_mode != 0 && g->k_mode != 1) return fail(DISTIR_E_INVALID_ARG, "spec.k_mode");
+  for (int i = 0; i < g->n_world; i++) {
+    if (!is_pow2(g->world[i]) || (i && g->world[i] <= g->world[i - 1]))
+      return fail(DISTIR_E_INVALID_ARG, "spec.world: ascending powers of two");
+    if (g->world[i] > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
+  }
+  for (int i = 0; i < g->n_batch; i++) {
+    if (g->batch[i] < 1 || (i && g->batch[i] <= g->batch[i - 1]))
+      return fail(DISTIR_E_INVALID_ARG, "spec.batch: ascending positive");
+    if (g->batch[i] > (int64_t(1) << 40)) return fail(DISTIR_E_UNSUPPORTED, "batch > 2^40");
+    for (int mi = 0; mi < g->n_models; mi++)
+      if (!work_fits(sim->models[g->models[mi]], g->batch[i]))
+        return fail(DISTIR_E_UNSUPPORTED, "per-op work overflows int64");
+  }
+  for (int i = 0; i < g->n_k; i++) {
+    if (g->k_set[i] < 1 || (i && g->k_set[i] <= g->k_set[i - 1]))
+      return fail(DISTIR_E_INVALID_ARG, "spec.k_set: ascending positive");
+    if (g->k_set[i] > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
+  }
+  sp.k_mode = g->k_mode;
+  sp.n_k = g->n_k;
+  for (int i = 0; i < g->n_k; i++) sp.k_set[i] = g->k_set[i];
+  sp.n_batch = g->n_batch;
+  for (int i = 0; i < g->n_batch; i++) sp.batch[i] = g->batch[i];
+  int64_t cum = 0;
+  int ne = 0;
+  for (int wi = 0; wi < g->n_world; wi++) {
+    const int e = ilog2(g->world[wi]);
+    for (int a = 0; a <= e; a++)
+      for (int b = 0; a + b <= e; b++) {
+        const int c = e - a - b;
+        if (!((g->dp_mask >> a) & 1) || !((g->tp_mask >> b) & 1) || !((g->pp_mask >> c) & 1)) continue;
+        const int nK = (g->k_mode == 0 && c == 0) ? 1 : g->n_k;
+        if (nK == 0) continue;
+        if (ne >= kMaxEntries) return fail(DISTIR_E_UNSUPPORTED, "too many (D,T,P) triples");
+        sp.entries[ne] = DEntry{1 << a, 1 << b, 1 << c, nK, cum};
+        cum += (int64_t)nK * g->n_batch;
+        ne++;
+      }
+  }
+  sp.n_entries = ne;
+  sp.per_mt = cum;
+  n_total = (int64_t)g->n_models * g->n_topos * cum;
+  if (n_total > (int64_t(1) << 31) - 1) return fail(DISTIR_E_UNSUPPORTED, "grid > 2^31 configs");
+  return DISTIR_OK;
+}
+
+distir_status validate_configs(const distir_sim* sim, const distir_config* cf, int64_t n) {
+  for (int64_t i = 0; i < n; i++) {
+    const distir_config& c = cf[i];
+    auto bad = [&](const char* w) {
+      return fail(DISTIR_E_INVALID_ARG, "config " + std::to_string(i) + ": " + w);
+    };
+    if (c.model < 0 || c.model >= (int)sim->models.size()) return bad("model index");
+    if (c.topo < 0 || c.topo >= (int)sim->topos.size()) return bad("topo index");
+    if (c.dp < 1 || c.tp < 1 || c.pp < 1 || c.microbatches < 1 || c.batch < 1) return bad("degrees");
+    if (!is_pow2(c.dp) || !is_pow2(c.tp))
+      return fail(DISTIR_E_UNSUPPORTED, "config dp/tp must be powers of two (stage symmetry)");
+    if ((int64_t)c.dp * c.tp * c.pp > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
+    if (c.microbatches > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
+    if (!work_fits(sim->models[c.model], c.batch))
+      return fail(DISTIR_E_UNSUPPORTED, "per-op work overflows int64");
+  }
+  return DISTIR_OK;
+}
+
+distir_status check_ws(void* ws, size_t have, size_t need) {
+  if (!ws) return fail(DISTIR_E_WORKSPACE, "workspace is NULL");
+  if (((uintptr_t)ws & 255) != 0) return fail(DISTIR_E_WORKSPACE, "workspace not 256-byte aligned");
+  if (have < need)
+    return fail(DISTIR_E_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  return DISTIR_OK;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+__global__ void k_reset(Bucket* bk, WsHeader* hdr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= kNumBuckets) {
+    Bucket b{};
+    b.key = kEmptyKey;
+    bk[i] = b;
+  }
+  if (i == 0) {
+    WsHeader h{};
+    *hdr = h;
+  }
+}
+
+// Fold the recorded launch events into the accumulated totals.
+distir_status prof_fold(distir_sim* sim) {
+  if (sim->ev_used == 0) return DISTIR_OK;
+  CUDA_TRY(cudaEventSynchronize(sim->ev[5 * (sim->ev_used - 1) + 4]));
+  for (size_t i = 0; i < sim->ev_used; i++) {
+    float t[4];
+    for (int j = 0; j < 4; j++)
+      CUDA_TRY(cudaEventElapsedTime(&t[j], sim->ev[5 * i + j], sim->ev[5 * i + j + 1]));
+    sim->acc.ms_prepare += t[0];
+    sim->acc.ms_simulate += t[1];
+    sim->acc.ms_topk += t[2];
+    sim->acc.ms_merge += t[3];
+  }
+  sim->ev_used = 0;
+  return DISTIR_OK;
+}
+
+// Event j of the current launch (recorded only while profiling).
+distir_status prof_mark(distir_sim* sim, int j) {
+  if (!sim->prof) return DISTIR_OK;
+  if (j == 0 && 5 * (sim->ev_used + 1) > sim->ev.size()) {
+    distir_status s = prof_fold(sim);
+    if (s != DISTIR_OK) return s;
+  }
+  CUDA_TRY(cudaEventRecord(sim->ev[5 * sim->ev_used + j], sim->stream));
+  if (j == 4) sim->ev_used++;
+  return DISTIR_OK;
+}
+
+// Launch a1-a7 (+ a8 when nccl_comm != NULL) on the uploaded shard; the
+// (global) top-k goes to (topk, ntopk).
+distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* ms, int64_t* pk,
+                         uint32_t* rs, TopkRec* topk, int* ntopk) {
+  const SpecBlock& sp = sim->spec;
+  distir_status s;
+  int64_t kernels = 0;
+  if ((s = prof_mark(sim, 0)) != DISTIR_OK) return s;
+  const Layout L = layout(sp.n_local, sp.mode == MODE_EXPLICIT ? sp.n_total : 0);
+  cudaStream_t st = sim->stream;
+  ms = ms ? ms : at<double>(ws, L.ms);
+  pk = pk ? pk : at<int64_t>(ws, L.pk);
+  rs = rs ? rs : at<uint32_t>(ws, L.rs);
+  const SpecBlock* dsp = at<SpecBlock>(ws, L.spec);
+  const DExplicit* dex = at<DExplicit>(ws, L.ex);
+  Bucket* bk = at<Bucket>(ws, L.bk);
+  WsHeader* hdr = at<WsHeader>(ws, L.hdr);
+  uint32_t* cb = at<uint32_t>(ws, L.cfg_bucket);
+  uint32_t* perm = at<uint32_t>(ws, L.perm);
+  Item* items = at<Item>(ws, L.items);
+  double* tpv = at<double>(ws, L.tp);
+  k_reset<<<(kNumBuckets + 1 + 255) / 256, 256, 0, st>>>(bk, hdr);
+  kernels++;
+  const int64_t n = sp.n_local;
+  if (n > 0) {
+    const int eg = (int)std::min<int64_t>((n + 255) / 256, sim->enum_grid);
+    k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, hdr);
+    k_plan<<<1, 1024, 0, st>>>(bk, hdr);
+    k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, perm, items);
+    kernels += 3;
+  }
+  if ((s = prof_mark(sim, 1)) != DISTIR_OK) return s;
+  if (n > 0) {
+    k_simulate<<<sim->sim_grid, 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
+    kernels++;
+  }
+  if ((s = prof_mark(sim, 2)) != DISTIR_OK) return s;
+  TopkRec* fin = at<TopkRec>(ws, L.fin);
+  int* fin_n = at<int>(ws, L.fin_n);
+  TopkRec* loc = comm ? fin : topk;   // local list (padded) when merging
+  int* loc_n = comm ? fin_n : ntopk;
+  if (k > 0) {
+    TopkRec* part = at<TopkRec>(ws, L.part);
+    int* part_n = at<int>(ws, L.part_n);
+    if (n > 0) {
+      k_topk_partial<<<kTopkBlocks, 256, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n);
+      k_topk_merge<<<1, 256, 0, st>>>(part, part_n, kTopkBlocks, k, k, loc, loc_n);
+      kernels += 2;
+    } else {
+      k_topk_merge<<<1, 256, 0, st>>>(part, part_n, 0, k, k, loc, loc_n);
+      kernels++;
+    }
+  }
+  if ((s = prof_mark(sim, 3)) != DISTIR_OK) return s;
+  if (k > 0 && comm) {
+    NcclApi& api = nccl();
+    if (!api.ok) return fail(DISTIR_E_NCCL, api.why);
+    TopkRec* gath = at<TopkRec>(ws, L.gath);
+    ncclResult_t r = api.allGather(fin, gath, (size_t)k * sizeof(TopkRec), ncclUint8,
+                                   static_cast<ncclComm_t>(comm), st);
+    if (r != ncclSuccess)
+      return fail(DISTIR_E_NCCL, std::string("ncclAllGather: ") +
+                                     (api.getErrorString ? api.getErrorString(r) : "error"));
+    k_topk_merge<<<1, 256, 0, st>>>(gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
+    kernels++;
+  }
+  if ((s = prof_mark(sim, 4)) != DISTIR_OK) return s;
+  CUDA_TRY(cudaGetLastError());
+  if (sim->prof) { sim->kernels += kernels; sim->launches++; }
+  return DISTIR_OK;
+}
+
+distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir_config* configs,
+                     int64_t n_configs, int32_t rank, int32_t n_ranks, void* ws, size_t ws_bytes,
+                     int64_t* n_local_out) {
+  if (n_ranks < 1 || n_ranks > kMaxRanks || rank < 0 || rank >= n_ranks)
+    return fail(DISTIR_E_INVALID_ARG, "rank / n_ranks");
+  if ((spec == nullptr) == (configs == nullptr))
+    return fail(DISTIR_E_INVALID_ARG, "exactly one of spec / configs");
+  SpecBlock& sp = sim->spec;
+  int64_t n_total = 0;
+  distir_status s;
+  if (spec) {
+    if ((s = build_spec(sim, spec, sp, n_total)) != DISTIR_OK) return s;
+  } else {
+    if (n_configs < 0 || n_configs > (int64_t(1) << 31) - 1)
+      return fail(DISTIR_E_INVALID_ARG, "n_configs");
+    if ((s = validate_configs(sim, configs, n_configs)) != DISTIR_OK) return s;
+    std::memset(&sp, 0, sizeof(sp));
+    for (size_t i = 0; i < sim->models.size(); i++) sp.models[i] = sim->models[i];
+    for (size_t i = 0; i < sim->topos.size(); i++) sp.topos[i] = sim->topos[i];
+    sp.mode = MODE_EXPLICIT;
+    n_total = n_configs;
+  }
+  sp.n_total = n_total;
+  sp.rank = rank;
+  sp.n_ranks = n_ranks;
+  sp.n_local = n_total > rank ? (n_total - rank + n_ranks - 1) / n_ranks : 0;
+  const Layout L = layout(sp.n_local, sp.mode == MODE_EXPLICIT ? n_total : 0);
+  if ((s = check_ws(ws, ws_bytes, L.total)) != DISTIR_OK) return s;
+  CUDA_TRY(cudaSetDevice(sim->device));
+  CUDA_TRY(cudaMemcpyAsync(at<SpecBlock>(ws, L.spec), &sp, sizeof(SpecBlock),
+                           cudaMemcpyHostToDevice, sim->stream));
+  if (sp.mode == MODE_EXPLICIT && n_total > 0)
+    CUDA_TRY(cudaMemcpyAsync(at<DExplicit>(ws, L.ex), configs, n_total * sizeof(DExplicit),
+                             cudaMemcpyHostToDevice, sim->stream));
+  sim->uploaded = true;
+  sim->uploaded_ws = ws;
+  sim->h2d = (int64_t)sizeof(SpecBlock) +
+             (sp.mode == MODE_EXPLICIT ? n_total * (int64_t)sizeof(DExplicit) : 0);
+  sim->d2h = 0;
+  if (n_local_out) *n_local_out = sp.n_local;
+  return DISTIR_OK;
+}
+
+distir_status fetch_stats(distir_sim* sim, void* ws, distir_stats* out) {
+  const Layout L = layout(sim->spec.n_local, sim->spec.mode == MODE_EXPLICIT ? sim->spec.n_total : 0);
+  WsHeader h;
+  CUDA_TRY(cudaMemcpyAsync(&h, at<WsHeader>(ws, L.hdr), sizeof(h), cudaMemcpyDeviceToHost,
+                           sim->stream));
+  CUDA_TRY(cudaStreamSynchronize(sim->stream));
+  out->n_configs = sim->spec.n_local;
+  out->n_valid = (int64_t)h.n_valid;
+  out->n_feasible = (int64_t)h.n_feasible;
+  out->op_events = (int64_t)h.op_events;
+  out->stage_steps = (int64_t)h.stage_steps;
+  out->n_buckets = h.n_buckets;
+  out->n_items = h.n_items;
+  out->h2d_bytes = sim->h2d;
+  out->d2h_bytes = sim->d2h + (int64_t)sizeof(WsHeader);
+  return DISTIR_OK;
+}
+
+}  // namespace
+
+// ================================================================== ABI =====
+extern "C" {
+
+const char* distir_last_error(void) { return g_err.c_str(); }
+
+const char* distir_version(void) { return "distir-b200 0.1 (sm_100a)"; }
+
+distir_status distir_sim_create(const distir_model* models, int32_t n_models,
+                                const distir_topology* topos, int32_t n_topos, int32_t cuda_device,
+                                void* cuda_stream, distir_sim** out) {
+  g_err.clear();
+  if (!out) return fail(DISTIR_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!models || n_models < 1 || n_models > kMaxModels)
+    return fail(DISTIR_E_INVALID_ARG, "models / n_models in [1, 64]");
+  if (!topos || n_topos < 1 || n_topos > kMaxTopos)
+    return fail(DISTIR_E_INVALID_ARG, "topos / n_topos in [1, 64]");
+  distir_status s;
+  for (int i = 0; i < n_models; i++)
+    if ((s = validate_model(models[i], i)) != DISTIR_OK) return s;
+  for (int i = 0; i < n_topos; i++)
+    if ((s = validate_topo(topos[i], i)) != DISTIR_OK) return s;
+  distir_sim* sim = new (std::nothrow) distir_sim();
+  if (!sim) return fail(DISTIR_E_OUT_OF_MEMORY, "handle");
+  for (int i = 0; i < n_models; i++) {
+    const distir_model& m = models[i];
+    sim->models.push_back(DModel{m.kind, m.n_layer, m.d_model, m.n_head, m.seq_len, m.vocab_pad,
+                                 m.n_ctx, m.dtype_bytes, m.id_bytes, m.lm_head});
+  }
+  for (int i = 0; i < n_topos; i++) {
+    const distir_topology& t = topos[i];
+    sim->topos.push_back(DTopo{t.world_max, t.node_size, t.flops_per_s, t.op_overhead_s,
+                               t.alpha_intra_s, t.bw_intra_Bps, t.alpha_inter_s, t.bw_inter_Bps,
+                               t.capacity_bytes});
+  }
+  sim->device = cuda_device;
+  sim->stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sim->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  int per_sm = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate, 128, 0);
+  if (e != cudaSuccess) {
+    delete sim;
+    return fail(DISTIR_E_CUDA, std::string("device setup: ") + cudaGetErrorString(e));
+  }
+  sim->sim_grid = sim->num_sms * (per_sm > 0 ? per_sm : 1);
+  sim->enum_grid = sim->num_sms * 8;
+  *out = sim;
+  return DISTIR_OK;
+}
+
+void distir_sim_destroy(distir_sim* sim) { delete sim; }
+
+distir_status distir_grid_size(const distir_sim* sim, const distir_grid_spec* spec, int64_t* n) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (!spec || !n) return fail(DISTIR_E_INVALID_ARG, "spec / n_configs is NULL");
+  SpecBlock* sp = new (std::nothrow) SpecBlock();
+  if (!sp) return fail(DISTIR_E_OUT_OF_MEMORY, "spec");
+  int64_t total = 0;
+  s = build_spec(sim, spec, *sp, total);
+  delete sp;
+  if (s == DISTIR_OK) *n = total;
+  return s;
+}
+
+distir_status distir_workspace_size(const distir_sim* sim, int64_t n_configs, size_t* bytes) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (!bytes || n_configs < 0) return fail(DISTIR_E_INVALID_ARG, "bytes / n_configs");
+  *bytes = layout(n_configs, n_configs).total;
+  return DISTIR_OK;
+}
+
+distir_status distir_grid_upload(distir_sim* sim, const distir_grid_spec* spec,
+                                 const distir_config* configs, int64_t n_configs, int32_t rank,
+                                 int32_t n_ranks, void* d_workspace, size_t ws_bytes,
+                                 int64_t* n_local_out) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  return upload(sim, spec, configs, n_configs, rank, n_ranks, d_workspace, ws_bytes, n_local_out);
+}
+
+distir_status distir_grid_launch(distir_sim* sim, int32_t k, void* nccl_comm, void* d_workspace,
+                                 size_t ws_bytes, double* d_makespan, int64_t* d_peak,
+                                 uint32_t* d_reason, distir_topk_entry* d_topk,
+                                 int32_t* d_n_topk) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (!sim->uploaded || sim->uploaded_ws != d_workspace)
+    return fail(DISTIR_E_INVALID_ARG, "no grid uploaded to this workspace");
+  if (k < 0 || k > kMaxK) return fail(DISTIR_E_INVALID_ARG, "k in [0, 64]");
+  if (k > 0 && (!d_topk || !d_n_topk)) return fail(DISTIR_E_INVALID_ARG, "d_topk / d_n_topk");
+  const Layout L = layout(sim->spec.n_local, sim->spec.mode == MODE_EXPLICIT ? sim->spec.n_total : 0);
+  if ((s = check_ws(d_workspace, ws_bytes, L.total)) != DISTIR_OK) return s;
+  CUDA_TRY(cudaSetDevice(sim->device));
+  return launch_all(sim, k, nccl_comm, d_workspace, d_makespan, d_peak, d_reason,
+                    reinterpret_cast<TopkRec*>(d_topk), d_n_topk);
+}
+
+distir_status distir_profile(distir_sim* sim, int32_t enable, distir_profile_data* out) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  CUDA_TRY(cudaSetDevice(sim->device));
+  if (out) {
+    if ((s = prof_fold(sim)) != DISTIR_OK) return s;
+    *out = sim->acc;
+    out->launches = sim->launches;
+    out->kernels = sim->kernels;
+    sim->acc = distir_profile_data{};
+    sim->launches = sim->kernels = 0;
+  }
+  if (enable && sim->ev.empty()) {
+    sim->ev.resize(5 * 4096);
+    for (cudaEvent_t& e : sim->ev) CUDA_TRY(cudaEventCreate(&e));
+  }
+  sim->prof = enable != 0;
+  return DISTIR_OK;
+}
+
+distir_status distir_last_stats(distir_sim* sim, void* d_workspace, distir_stats* out) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (!out || !d_workspace) return fail(DISTIR_E_INVALID_ARG, "out / workspace");
+  CUDA_TRY(cudaSetDevice(sim->device));
+  return fetch_stats(sim, d_workspace, out);
+}
+
+distir_status distir_grid_eval_sharded(distir_sim* sim, const distir_grid_spec* spec,
+                                       const distir_config* configs, int64_t n_configs,
+                                       int32_t rank, int32_t n_ranks, void* nccl_comm, int32_t k,
+                                       void* d_workspace, size_t ws_bytes, double* makespan_out,
+                                       int64_t* peak_out, uint32_t* reason_out,
+                                       distir_topk_entry* topk_out, int32_t* n_topk_out,
+                                       distir_stats* stats_out) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (k < 0 || k > kMaxK) return fail(DISTIR_E_INVALID_ARG, "k in [0, 64]");
+  if (k > 0 && (!topk_out || !n_topk_out)) return fail(DISTIR_E_INVALID_ARG, "topk_out / n_topk_out");
+  if (n_ranks > 1 && !nccl_comm) return fail(DISTIR_E_INVALID_ARG, "nccl_comm is NULL");
+  if ((s = upload(sim, spec, configs, n_configs, rank, n_ranks, d_workspace, ws_bytes, nullptr)) !=
+      DISTIR_OK)
+    return s;
+  const SpecBlock& sp = sim->spec;
+  const Layout L = layout(sp.n_local, sp.mode == MODE_EXPLICIT ? sp.n_total : 0);
+  TopkRec* fin = at<TopkRec>(d_workspace, L.out);
+  int* fin_n = at<int>(d_workspace, L.out_n);
+  if ((s = launch_all(sim, k, nccl_comm, d_workspace, nullptr, nullptr, nullptr, fin, fin_n)) !=
+      DISTIR_OK)
+    return s;
+  const int64_t n = sp.n_local;
+  sim->d2h = n * ((makespan_out ? 8 : 0) + (peak_out ? 8 : 0) + (reason_out ? 4 : 0)) +
+             (k > 0 ? (int64_t)k * (int64_t)sizeof(TopkRec) + 4 : 0);
+  if (n > 0) {
+    const size_t pitch = (size_t)n_ranks;
+    if (makespan_out)
+      CUDA_TRY(cudaMemcpy2DAsync(makespan_out + rank, pitch * 8, at<double>(d_workspace, L.ms), 8, 8,
+                                 n, cudaMemcpyDeviceToHost, sim->stream));
+    if (peak_out)
+      CUDA_TRY(cudaMemcpy2DAsync(peak_out + rank, pitch * 8, at<int64_t>(d_workspace, L.pk), 8, 8, n,
+                                 cudaMemcpyDeviceToHost, sim->stream));
+    if (reason_out)
+      CUDA_TRY(cudaMemcpy2DAsync(reason_out + rank, pitch * 4, at<uint32_t>(d_workspace, L.rs), 4, 4,
+                                 n, cudaMemcpyDeviceToHost, sim->stream));
+  }
+  if (k > 0) {
+    CUDA_TRY(cudaMemcpyAsync(topk_out, fin, (size_t)k * sizeof(TopkRec), cudaMemcpyDeviceToHost,
+                             sim->stream));
+    CUDA_TRY(cudaMemcpyAsync(n_topk_out, fin_n, sizeof(int32_t), cudaMemcpyDeviceToHost, sim->stream));
+  }
+  if (stats_out) {
+    if ((s = fetch_stats(sim, d_workspace, stats_out)) != DISTIR_OK) return s;
+  }
+  CUDA_TRY(cudaStreamSynchronize(sim->stream));
+  return DISTIR_OK;
+}
+
+distir_status distir_grid_eval(distir_sim* sim, const distir_grid_spec* spec,
+                               const distir_config* configs, int64_t n_configs, int32_t k,
+                               void* d_workspace, size_t ws_bytes, double* makespan_out,
+                               int64_t* peak_out, uint32_t* reason_out, distir_topk_entry* topk_out,
+                               int32_t* n_topk_out, distir_stats* stats_out) {
+  return distir_grid_eval_sharded(sim, spec, configs, n_configs, 0, 1, nullptr, k, d_workspace,
+                                  ws_bytes, makespan_out, peak_out, reason_out, topk_out,
+                                  n_topk_out, stats_out);
+}
+
+distir_status distir_nccl_unique_id(uint8_t id_out[128]) {
+  g_err.clear();
+  if (!id_out) return fail(DISTIR_E_INVALID_ARG, "id_out is NULL");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(DISTIR_E_NCCL, api.why);
+  ncclUniqueId id;
+  ncclResult_t r = api.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(DISTIR_E_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(id_out, &id, 128);
+  return DISTIR_OK;
+}
+
+distir_status distir_nccl_comm_init(const uint8_t id[128], int32_t n_ranks, int32_t rank,
+                                    int32_t cuda_device, void** comm_out) {
+  g_err.clear();
+  if (!id || !comm_out || n_ranks < 1 || rank < 0 || rank >= n_ranks)
+    return fail(DISTIR_E_INVALID_ARG, "id / comm_out / rank");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(DISTIR_E_NCCL, api.why);
+  CUDA_TRY(cudaSetDevice(cuda_device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = api.commInitRank(&comm, n_ranks, uid, rank);
+  if (r != ncclSuccess)
+    return fail(DISTIR_E_NCCL, std::string("ncclCommInitRank: ") +
+                                   (api.getErrorString ? api.getErrorString(r) : "error"));
+  *comm_out = comm;
+  return DISTIR_OK;
+}
+
+distir_status distir_nccl_comm_destroy(void* comm) {
+  g_err.clear();
+  if (!comm) return DISTIR_OK;
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(DISTIR_E_NCCL, api.why);
+  api.commDestroy(static_cast<ncclComm_t>(comm));
+  return DISTIR_OK;
+}
+
+int64_t distir_shard_indices(int64_t n_configs, int32_t rank, int32_t n_ranks, int64_t* out,
+                             int64_t cap) {
+  if (n_configs <= 0 || n_ranks < 1 || rank < 0 || rank >= n_ranks) return 0;
+  const int64_t n = n_configs > rank ? (n_configs - rank + n_ranks - 1) / n_ranks : 0;
+  for (int64_t q = 0; q < n && q < cap && out; q++) out[q] = rank + q * n_ranks;
+  return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,834 @@
+// kernels.cuh -- sm_100a kernels of the DistIR grid pass (product path).
+//
+// Steps (BASELINE north_star):
+//   k_enumerate  a1  index -> config, validity bits (C.1-C.2),
+//                    warp-shape bucket (hash), closed-form op counts
+//   k_plan           bucket -> lanes per config, work items in LPT order
+//   k_scatter        configs grouped by bucket into warp work items
+//   k_simulate   a2-a6  per config: D/T/P + GPipe program as register
+//                    templates (C.3/C.4), analytic costs (P:483-487,
+//                    P:518-520; C.5), synchronous timeline (
+//                    C.6) and live memory (C.7), capacity
+//   k_topk_*     a7/a8  top-k by (throughput desc, peak asc, index asc)
+//
+// Design: one warp holds 32/S configurations, S lanes
+// each (S = next power of two >= P, capped at 32).  Lane sl of a segment owns
+// pipeline stage sl (and sl + 32 when 32 < P <= 64).  All D*T ranks of a stage
+// run the same cost sequence and hold equal clocks and peaks (SURVEY C.6
+// Theorem 2: power-of-two D, T, node size, aligned groups), so one lane
+// represents them all.  Stages advance as a wavefront: task (k, s) -- the
+// stage-s ops of microbatch k followed by its Send -- runs at step 2k + s
+// (forward) or 2k + (P-1-s) (backward).  Each device still executes its ops in
+// program order, so every op's end time is bit-identical to the global
+// program-order walk (SURVEY C.6 Theorem 1): one IEEE add per op, exact max
+// for the synchronising ops.  Absent collectives (T = 1, D = 1) are identity
+// steps: cost +0.0 and zero bytes, which leave clocks and memory unchanged.
+#pragma once
+#include <cfloat>
+#include <climits>
+#include "common.cuh"
+
+namespace distir {
+
+// ------------------------------------------------------------- config -------
+struct Cfg {
+  DModel M;
+  int32_t topo;
+  int64_t D, T, P, K, B;
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Decode canonical index i (C.1 nested order, or the synthetic sweep of
+// SURVEY §8d D.1, or an explicit list).
+__device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t i, Cfg& c) {
+  if (sp.mode == MODE_EXPLICIT) {
+    const DExplicit x = ex[i];
+    c.M = sp.models[x.model];
+    c.topo = x.topo;
+    c.D = x.dp; c.T = x.tp; c.P = x.pp; c.K = x.K; c.B = x.B;
+    return;
+  }
+  if (sp.mode == MODE_SYNTH) {
+    uint64_t r[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+      r[t] = mix64(sp.synth_seed + 0x9E3779B97F4A7C15ull * (uint64_t)(8 * i + t + 1));
+    const int e = (int)(r[1] % 7);               // W = 2^e
+    int j = (int)(r[2] % (uint64_t)((e + 1) * (e + 2) / 2));
+    int a = 0;                                   // j-th triple, lexicographic
+    while (j >= e - a + 1) { j -= e - a + 1; a++; }
+    c.D = 1ll << a; c.T = 1ll << j; c.P = 1ll << (e - a - j);
+    c.K = (c.P == 1) ? 1 : (1ll << (1 + r[3] % 5));
+    c.B = 1ll << (7 + r[4] % 12);
+    if ((r[0] & 1) == 0) {
+      c.M = DModel{0, (int32_t)(1 << (1 + r[5] % 6)), (int32_t)(1 << (8 + r[6] % 7)), 1, 1, 0, 0, 2, 8, 0};
+    } else {
+      const int q = (int)(r[5] % 4);
+      const int32_t L = q == 0 ? 12 : q == 1 ? 24 : q == 2 ? 36 : 48;
+      const int32_t d = q == 0 ? 768 : q == 1 ? 1024 : q == 2 ? 1280 : 1600;
+      const int32_t h = q == 0 ? 12 : q == 1 ? 16 : q == 2 ? 20 : 25;
+      c.M = DModel{1, L, d, h, 8, 50304, 1024, 2, 8, 1};
+    }
+    c.topo = sp.topo_ids[r[7] % (uint64_t)sp.n_topos];
+    return;
+  }
+  const int64_t mt = i / sp.per_mt;
+  const int64_t r = i - mt * sp.per_mt;
+  const int mi = (int)(mt / sp.n_topos), ti = (int)(mt - (int64_t)mi * sp.n_topos);
+  int lo = 0, hi = sp.n_entries - 1;            // last entry with cum <= r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sp.entries[mid].cum <= r) lo = mid; else hi = mid - 1;
+  }
+  const DEntry en = sp.entries[lo];
+  const int64_t r2 = r - en.cum;
+  const int64_t kq = r2 / sp.n_batch, bq = r2 - kq * sp.n_batch;
+  c.M = sp.models[sp.model_ids[mi]];
+  c.topo = sp.topo_ids[ti];
+  c.D = en.D; c.T = en.T; c.P = en.P;
+  c.K = (sp.k_mode == 0 && en.P == 1) ? 1 : sp.k_set[kq];
+  c.B = sp.batch[bq];
+}
+
+// C.2 validity bits.
+__device__ __forceinline__ uint32_t validity(const Cfg& c, const DTopo& t) {
+  uint32_t r = 0;
+  if (c.B % (c.D * c.K) != 0) r |= 1u;
+  if (c.P > c.M.L) r |= 2u;
+  if (c.M.d % c.T != 0) r |= 4u;
+  if (c.M.kind == 1 && c.M.V % c.T != 0) r |= 4u;
+  if (c.M.kind == 1 && c.M.h % c.T != 0) r |= 8u;
+  if (c.D * c.T * c.P > t.world_max) r |= 16u;
+  return r;
+}
+
+// Global op count of the program (a collective counts once; C.3 / C.4) and
+// the (op, stage) steps a representative-rank walk performs.
+__device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t& steps) {
+  const int64_t D = c.D, T = c.T, P = c.P, K = c.K, L = c.M.L;
+  const int64_t tp = T > 1, dp = D > 1;
+  if (c.M.kind == 0) {
+    events = 5 * K * D * T * L + D * T * L + K * D * T + tp * K * D * L + 2 * K * D * T * (P - 1) + dp * T * L;
+    steps = K * (5 * L + tp * L + 1 + 2 * (P - 1)) + L * (1 + dp);
+  } else {
+    const int64_t lm = c.M.lm != 0;
+    events = 12 * K * D * T * L + (2 + lm) * K * D * T + tp * K * D * (2 * L + 1 + lm) + K * D * T * (P - 1);
+    steps = K * (12 * L + tp * 2 * L + (1 + tp) + (1 + lm + tp * lm) + 2 * (P - 1));
+  }
+}
+
+__device__ __forceinline__ uint32_t bucket_key(const Cfg& c) {
+  const uint32_t K = (uint32_t)(c.K < 255 ? c.K : 255);
+  return (uint32_t)c.M.kind | (uint32_t)(c.P - 1) << 1 | (uint32_t)(c.M.L - 1) << 7 | K << 17;
+}
+
+// ------------------------------------------------------------ costs (C.5) ---
+// Canonical binary64 expressions, round-to-nearest, no contraction.
+__device__ __forceinline__ double cost_compute(int64_t flops, const DTopo& t) {
+  return __dadd_rn(__ddiv_rn(__ll2double_rn(flops), t.F), t.o);
+}
+__device__ __forceinline__ bool group_intra(int64_t first, int64_t last, int32_t ns) {
+  return first / ns == last / ns;
+}
+__device__ __forceinline__ double cost_send(int64_t bytes, bool intra, const DTopo& t) {
+  const double a = intra ? t.a_intra : t.a_inter, bw = intra ? t.bw_intra : t.bw_inter;
+  return __dadd_rn(a, __ddiv_rn(__ll2double_rn(bytes), bw));
+}
+__device__ __forceinline__ double cost_ring(int64_t steps, int64_t g, int64_t bytes, bool intra,
+                                            const DTopo& t) {
+  const double a = intra ? t.a_intra : t.a_inter, bw = intra ? t.bw_intra : t.bw_inter;
+  const double st = __ll2double_rn(steps);
+  return __dadd_rn(__dmul_rn(st, a),
+                   __dmul_rn(__ddiv_rn(st, __ll2double_rn(g)), __ddiv_rn(__ll2double_rn(bytes), bw)));
+}
+__device__ __forceinline__ double cost_allreduce(int64_t g, int64_t bytes, bool intra, const DTopo& t) {
+  return cost_ring(2 * (g - 1), g, bytes, intra, t);
+}
+__device__ __forceinline__ double cost_allgather(int64_t g, int64_t bytes, bool intra, const DTopo& t) {
+  return cost_ring(g - 1, g, bytes, intra, t);
+}
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// Live-memory step (C.7): allocate outputs, record the peak, free last uses.
+#define MEM(q, a, f)                                 \
+  do {                                               \
+    live[q] += (a);                                  \
+    peak[q] = peak[q] > live[q] ? peak[q] : live[q]; \
+    live[q] -= (f);                                  \
+  } while (0)
+
+// -------------------------------------------------- stage-neighbour shuffles
+// Stage s of lane `lane`, slot q is s = sl + S*q.  For V == 1 the neighbours
+// of a stage are the adjacent lanes of its segment; for V == 2 (S == 32, one
+// config per warp) stage 31 <-> 32 wraps between lane 31 slot 0 and lane 0
+// slot 1.
+template <int V>
+struct Nbr {
+  // value of stage s+1 for each slot
+  __device__ static void up_stage(const double (&x)[V], double (&out)[V], int lane) {
+    const double d0 = __shfl_down_sync(0xffffffffu, x[0], 1);
+    if constexpr (V == 1) {
+      out[0] = d0;
+    } else {
+      const double d1 = __shfl_down_sync(0xffffffffu, x[1], 1);
+      const double w1 = __shfl_sync(0xffffffffu, x[1], 0);
+      out[0] = lane < 31 ? d0 : w1;
+      out[1] = d1;
+    }
+  }
+  // value of stage s-1 for each slot
+  __device__ static void down_stage(const double (&x)[V], double (&out)[V], int lane) {
+    const double e0 = __shfl_up_sync(0xffffffffu, x[0], 1);
+    if constexpr (V == 1) {
+      out[0] = e0;
+    } else {
+      const double e1 = __shfl_up_sync(0xffffffffu, x[1], 1);
+      const double y = __shfl_sync(0xffffffffu, x[0], 31);
+      out[0] = e0;
+      out[1] = lane > 0 ? e1 : y;
+    }
+  }
+  // flags of stage s-1 / s+1
+  __device__ static void down_flag(const bool (&f)[V], bool (&out)[V], int lane) {
+    const bool e0 = __shfl_up_sync(0xffffffffu, (int)f[0], 1);
+    if constexpr (V == 1) {
+      out[0] = e0;
+    } else {
+      const bool e1 = __shfl_up_sync(0xffffffffu, (int)f[1], 1);
+      const bool y = __shfl_sync(0xffffffffu, (int)f[0], 31);
+      out[0] = e0;
+      out[1] = lane > 0 ? e1 : y;
+    }
+  }
+  __device__ static void up_flag(const bool (&f)[V], bool (&out)[V], int lane) {
+    const bool d0 = __shfl_down_sync(0xffffffffu, (int)f[0], 1);
+    if constexpr (V == 1) {
+      out[0] = d0;
+    } else {
+      const bool d1 = __shfl_down_sync(0xffffffffu, (int)f[1], 1);
+      const bool w1 = __shfl_sync(0xffffffffu, (int)f[1], 0);
+      out[0] = lane < 31 ? d0 : w1;
+      out[1] = d1;
+    }
+  }
+};
+
+__device__ __forceinline__ int warp_max_int(int v) { return __reduce_max_sync(0xffffffffu, v); }
+
+// A per-parity pair selected without dynamic register indexing.
+template <typename T>
+struct Par {
+  T a, b;
+  __device__ __forceinline__ T operator[](int p) const { return p ? b : a; }
+};
+
+// -------------------------------------------------- MLP training (C.3) -------
+template <int V>
+__device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
+                        double& ms_out, int64_t& peak_out) {
+  const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
+  const int64_t m = has ? c.B / (D * K) : 0;
+  const int32_t ns = tp.node_size;
+  // Layer shapes by parity of the global layer index: even = column
+  // parallel, odd = row parallel (Megatron pairing); T = 1: both full.
+  const Par<int64_t> kin{d, d / T}, nout{d / T, d}, dout{d / T, d};
+  const bool tp_intra = group_intra(0, T - 1, ns);
+  const bool dp_intra = group_intra(0, T * (D - 1), ns);
+  Par<double> mm, relu, rg, mmg, add, sgd, ardp;
+  Par<int64_t> Wb;
+  {
+    const int64_t w0 = kin.a * nout.a, w1 = kin.b * nout.b;
+    mm = {cost_compute(2 * m * w0, tp), cost_compute(2 * m * w1, tp)};
+    relu = {cost_compute(m * dout.a, tp), cost_compute(m * dout.b, tp)};
+    rg = relu;
+    mmg = {cost_compute(4 * m * w0, tp), cost_compute(4 * m * w1, tp)};
+    add = {cost_compute(w0, tp), cost_compute(w1, tp)};
+    sgd = {cost_compute(2 * w0, tp), cost_compute(2 * w1, tp)};
+    Wb = {w0 * e, w1 * e};
+    ardp = {D > 1 ? cost_allreduce(D, Wb.a, dp_intra, tp) : 0.0,
+            D > 1 ? cost_allreduce(D, Wb.b, dp_intra, tp) : 0.0};
+  }
+  const int64_t mde = m * d * e;
+  const double ar_tp = T > 1 ? cost_allreduce(T, mde, tp_intra, tp) : 0.0;
+  const int64_t ar_b = T > 1 ? mde : 0;
+  const int64_t dlast = dout[(L - 1) & 1];
+  const double loss = cost_compute(3 * m * dlast, tp);
+
+  int s[V], lo[V], hi[V];
+  bool ok[V];
+  double clk[V], sendf[V], sendb[V];
+  int64_t live[V], peak[V];
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    s[q] = sl + S * q;
+    ok[q] = has && s[q] < P;
+    lo[q] = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
+    hi[q] = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
+    const int64_t r0 = T * D * (int64_t)s[q];    // rank (0, 0, s)
+    sendf[q] = (ok[q] && s[q] < P - 1)
+                   ? cost_send(m * dout[(hi[q] - 1) & 1] * e, group_intra(r0, r0 + T * D, ns), tp)
+                   : 0.0;
+    sendb[q] = (ok[q] && s[q] > 0)
+                   ? cost_send(m * kin[lo[q] & 1] * e, group_intra(r0 - T * D, r0, ns), tp)
+                   : 0.0;
+    int64_t lv = 0;
+    for (int l = lo[q]; l < hi[q]; l++) lv += 2 * Wb[l & 1];       // W_l, G_l
+    if (ok[q] && s[q] == 0) lv += K * mde;                         // X_k
+    if (ok[q] && s[q] == P - 1) lv += K * m * dlast * e;           // Y_k
+    live[q] = lv; peak[q] = lv; clk[q] = 0.0;
+  }
+
+  // ---- forward wavefront: task (k, s) at step 2k + s
+  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  for (int w = 0; w < nsteps; w++) {
+    bool act[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const int kk = w - s[q];
+      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
+      if (act[q]) {
+        for (int l = lo[q]; l < hi[q]; l++) {
+          const int p = l & 1;
+          clk[q] = dadd(clk[q], mm[p]);                       // MatMul
+          MEM(q, m * nout[p] * e, 0);
+          clk[q] = dadd(clk[q], p ? ar_tp : 0.0);             // TP AllReduce (row)
+          MEM(q, p ? ar_b : 0, p ? ar_b : 0);
+          clk[q] = dadd(clk[q], relu[p]);                     // Relu
+          MEM(q, m * dout[p] * e, m * dout[p] * e);
+        }
+      }
+    }
+    // Send s -> s+1: both ends wait for each other
+    double nb[V], t[V];
+    bool snd[V], rin[V];
+    Nbr<V>::up_stage(clk, nb, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      snd[q] = act[q] && s[q] < P - 1;
+      t[q] = dadd(fmax(clk[q], nb[q]), sendf[q]);
+      if (snd[q]) clk[q] = t[q];
+    }
+    double tin[V];
+    Nbr<V>::down_stage(t, tin, lane);
+    Nbr<V>::down_flag(snd, rin, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (ok[q] && s[q] > 0 && rin[q]) {
+        clk[q] = tin[q];
+        MEM(q, m * kin[lo[q] & 1] * e, 0);                    // received activation
+      }
+    }
+  }
+
+  // ---- backward wavefront: task (k, s) at step 2k + (P-1-s)
+  for (int w = 0; w < nsteps; w++) {
+    bool act[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const int kk = w - (int)(P - 1 - s[q]);
+      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
+      if (act[q]) {
+        if (s[q] == P - 1) {                                  // LossGrad
+          clk[q] = dadd(clk[q], loss);
+          MEM(q, m * dlast * e, m * dlast * e);
+        }
+        for (int l = hi[q] - 1; l >= lo[q]; l--) {
+          const int p = l & 1;
+          const int64_t act_b = m * dout[p] * e;
+          clk[q] = dadd(clk[q], rg[p]);                       // ReluGrad
+          MEM(q, act_b, 2 * act_b);
+          const int64_t din = m * kin[p] * e;
+          const bool first = l == lo[q];
+          const bool dead0 = s[q] == 0 && l == 0;             // dA_0 has no user
+          clk[q] = dadd(clk[q], mmg[p]);                      // MatMulGrad
+          MEM(q, din + Wb[p], act_b + (first ? din : 0) + ((dead0 && T == 1) ? din : 0));
+          const bool col_ar = p == 0 && T > 1;
+          clk[q] = dadd(clk[q], col_ar ? ar_tp : 0.0);        // TP AllReduce (col)
+          MEM(q, col_ar ? mde : 0, col_ar ? (mde + (dead0 ? mde : 0)) : 0);
+          clk[q] = dadd(clk[q], add[p]);                      // gradient accumulation
+          MEM(q, Wb[p], 2 * Wb[p]);
+        }
+      }
+    }
+    // Send s -> s-1
+    double nb[V], t[V];
+    bool snd[V], rin[V];
+    Nbr<V>::down_stage(clk, nb, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      snd[q] = act[q] && s[q] > 0;
+      t[q] = dadd(fmax(clk[q], nb[q]), sendb[q]);
+      if (snd[q]) {
+        clk[q] = t[q];
+        live[q] -= m * kin[lo[q] & 1] * e;                    // sent gradient dies
+      }
+    }
+    double tin[V];
+    Nbr<V>::up_stage(t, tin, lane);
+    Nbr<V>::up_flag(snd, rin, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (ok[q] && s[q] < P - 1 && rin[q]) {
+        clk[q] = tin[q];
+        MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);             // received gradient
+      }
+    }
+  }
+
+  // ---- tail: DP AllReduce of the accumulated gradients, then SGD
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (!ok[q]) continue;
+    for (int l = hi[q] - 1; l >= lo[q]; l--) {
+      const int p = l & 1;
+      clk[q] = dadd(clk[q], ardp[p]);
+      MEM(q, D > 1 ? Wb[p] : 0, D > 1 ? Wb[p] : 0);
+    }
+    for (int l = lo[q]; l < hi[q]; l++) {
+      const int p = l & 1;
+      clk[q] = dadd(clk[q], sgd[p]);
+      MEM(q, Wb[p], 2 * Wb[p]);
+    }
+  }
+  double msx = 0.0;
+  int64_t pkx = 0;
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (ok[q]) { msx = fmax(msx, clk[q]); pkx = pkx > peak[q] ? pkx : peak[q]; }
+  }
+  ms_out = msx;
+  peak_out = pkx;
+}
+
+// ------------------------------------------------ GPT-2 inference (C.4) -----
+template <int V>
+__device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
+                         double& ms_out, int64_t& peak_out) {
+  const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
+                ide = c.M.ide, nctx = c.M.nctx;
+  const bool lm = c.M.lm != 0;
+  const int64_t D = c.D, T = c.T, P = c.P, K = c.K;
+  const int64_t m = has ? c.B / (D * K) : 0;
+  const int64_t n = m * Sq, dT = d / T, hT = h / T, VT = Vp / T;
+  const int32_t ns = tp.node_size;
+  const bool tp_intra = group_intra(0, T - 1, ns);
+  // costs (C.4 work per op)
+  const double c_emb = cost_compute(2 * n * d, tp);
+  const double c_ln = cost_compute(5 * n * d, tp);
+  const double c_qkv = cost_compute(2 * n * d * (3 * dT) + n * (3 * dT), tp);
+  const double c_att = cost_compute(2 * m * Sq * Sq * dT, tp);
+  const double c_smx = cost_compute(5 * m * hT * Sq * Sq, tp);
+  const double c_prj = cost_compute(2 * n * dT * d + n * d, tp);
+  const double c_add = cost_compute(n * d, tp);
+  const double c_fc1 = cost_compute(2 * n * d * (4 * dT) + n * (4 * dT), tp);
+  const double c_gel = cost_compute(8 * n * (4 * dT), tp);
+  const double c_fc2 = cost_compute(2 * n * (4 * dT) * d + n * d, tp);
+  const double c_lmh = cost_compute(2 * n * d * VT, tp);
+  const int64_t nde = n * d * e;
+  const double c_ar = T > 1 ? cost_allreduce(T, nde, tp_intra, tp) : 0.0;
+  const double c_ag = T > 1 ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0;
+  const int64_t arb = T > 1 ? nde : 0;
+  // value sizes
+  const int64_t qkvb = n * 3 * dT * e, scb = m * hT * Sq * Sq * e, ctxb = n * dT * e, fb = n * 4 * dT * e;
+  const int64_t ln_p = 2 * d * e, qkv_p = (d * 3 * dT + 3 * dT) * e, prj_p = (dT * d + d) * e,
+                fc1_p = (d * 4 * dT + 4 * dT) * e, fc2_p = (4 * dT * d + d) * e;
+  const int64_t blk_p = 2 * ln_p + qkv_p + prj_p + fc1_p + fc2_p;
+  const int64_t wte_b = VT * d * e, wpe_b = nctx * d * e;
+
+  int s[V], lo[V], hi[V];
+  bool ok[V];
+  double clk[V], sendf[V];
+  int64_t live[V], peak[V];
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    s[q] = sl + S * q;
+    ok[q] = has && s[q] < P;
+    lo[q] = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
+    hi[q] = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
+    const int64_t r0 = T * D * (int64_t)s[q];
+    sendf[q] = (ok[q] && s[q] < P - 1) ? cost_send(nde, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
+    int64_t lv = (int64_t)(hi[q] - lo[q]) * blk_p;
+    if (ok[q] && s[q] == 0) lv += wte_b + wpe_b + K * n * ide;
+    if (ok[q] && s[q] == P - 1) lv += 2 * d * e + ((lm && P > 1) ? wte_b : 0);
+    live[q] = lv; peak[q] = lv; clk[q] = 0.0;
+  }
+
+  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  for (int w = 0; w < nsteps; w++) {
+    bool act[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const int kk = w - s[q];
+      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
+      if (!act[q]) continue;
+      const bool last = (kk >> 1) == K - 1;
+      if (s[q] == 0) {                                        // prologue
+        clk[q] = dadd(clk[q], c_emb);                          // Embed
+        MEM(q, nde, n * ide + (last ? wpe_b + ((P == 1 && lm) ? 0 : wte_b) : 0));
+        clk[q] = dadd(clk[q], c_ar);                           // TP AllReduce
+        MEM(q, arb, arb);
+      }
+      for (int l = lo[q]; l < hi[q]; l++) {                   // blocks
+        clk[q] = dadd(clk[q], c_ln);   MEM(q, nde, last ? ln_p : 0);
+        clk[q] = dadd(clk[q], c_qkv);  MEM(q, qkvb, nde + (last ? qkv_p : 0));
+        clk[q] = dadd(clk[q], c_att);  MEM(q, scb, 0);
+        clk[q] = dadd(clk[q], c_smx);  MEM(q, scb, scb);
+        clk[q] = dadd(clk[q], c_att);  MEM(q, ctxb, scb + qkvb);
+        clk[q] = dadd(clk[q], c_prj);  MEM(q, nde, ctxb + (last ? prj_p : 0));
+        clk[q] = dadd(clk[q], c_ar);   MEM(q, arb, arb);
+        clk[q] = dadd(clk[q], c_add);  MEM(q, nde, 2 * nde);
+        clk[q] = dadd(clk[q], c_ln);   MEM(q, nde, last ? ln_p : 0);
+        clk[q] = dadd(clk[q], c_fc1);  MEM(q, fb, nde + (last ? fc1_p : 0));
+        clk[q] = dadd(clk[q], c_gel);  MEM(q, fb, fb);
+        clk[q] = dadd(clk[q], c_fc2);  MEM(q, nde, fb + (last ? fc2_p : 0));
+        clk[q] = dadd(clk[q], c_ar);   MEM(q, arb, arb);
+        clk[q] = dadd(clk[q], c_add);  MEM(q, nde, 2 * nde);
+      }
+      if (s[q] == P - 1) {                                    // epilogue
+        clk[q] = dadd(clk[q], c_ln);                           // final LayerNorm
+        MEM(q, nde, nde + (last ? 2 * d * e : 0));
+        if (lm) {
+          clk[q] = dadd(clk[q], c_lmh);                        // LM head
+          MEM(q, n * VT * e, nde + (last ? wte_b : 0));
+          clk[q] = dadd(clk[q], c_ag);                         // logits AllGather
+          MEM(q, T > 1 ? n * Vp * e : 0, T > 1 ? n * VT * e : 0);
+        }
+      }
+    }
+    double nb[V], t[V];
+    bool snd[V], rin[V];
+    Nbr<V>::up_stage(clk, nb, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      snd[q] = act[q] && s[q] < P - 1;
+      t[q] = dadd(fmax(clk[q], nb[q]), sendf[q]);
+      if (snd[q]) { clk[q] = t[q]; live[q] -= nde; }          // sent activation dies
+    }
+    double tin[V];
+    Nbr<V>::down_stage(t, tin, lane);
+    Nbr<V>::down_flag(snd, rin, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (ok[q] && s[q] > 0 && rin[q]) { clk[q] = tin[q]; MEM(q, nde, 0); }
+    }
+  }
+  double msx = 0.0;
+  int64_t pkx = 0;
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (ok[q]) { msx = fmax(msx, clk[q]); pkx = pkx > peak[q] ? pkx : peak[q]; }
+  }
+  ms_out = msx;
+  peak_out = pkx;
+}
+#undef MEM
+
+// ------------------------------------------------------------- kernels ------
+
+__global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* __restrict__ ex,
+                            Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
+                            double* __restrict__ ms_out, int64_t* __restrict__ pk_out,
+                            uint32_t* __restrict__ rs_out, double* __restrict__ tp_out,
+                            WsHeader* __restrict__ hdr) {
+  const SpecBlock& sp = *spp;
+  const int64_t nloc = sp.n_local;
+  unsigned long long ev = 0, st = 0, nv = 0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nloc;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = sp.rank + q * sp.n_ranks;
+    Cfg c;
+    decode(sp, ex, i, c);
+    const uint32_t r = validity(c, sp.topos[c.topo]);
+    if (r) {
+      rs_out[q] = r;
+      ms_out[q] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+      pk_out[q] = -1;
+      tp_out[q] = 0.0;
+      cfg_bucket[q] = kEmptyKey;
+      continue;
+    }
+    int64_t events, steps;
+    op_counts(c, events, steps);
+    ev += events; st += steps; nv += 1;
+    const uint32_t key = bucket_key(c);
+    uint32_t slot = (key * 2654435761u) >> 20;                 // 12-bit hash
+    uint32_t found = kOverflowBucket;
+    for (int probe = 0; probe < kNumBuckets; probe++) {
+      const uint32_t sl = (slot + probe) & (kNumBuckets - 1);
+      uint32_t cur = *(volatile uint32_t*)&bk[sl].key;
+      if (cur == kEmptyKey) cur = atomicCAS(&bk[sl].key, kEmptyKey, key);
+      if (cur == kEmptyKey || cur == key) { found = sl; break; }
+    }
+    atomicAdd(&bk[found].count, 1u);
+    cfg_bucket[q] = found;
+  }
+  // warp-aggregated statistics
+  for (int o = 16; o > 0; o >>= 1) {
+    ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+    nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  }
+  if ((threadIdx.x & 31) == 0 && nv) {
+    atomicAdd(&hdr->op_events, ev);
+    atomicAdd(&hdr->stage_steps, st);
+    atomicAdd(&hdr->n_valid, nv);
+  }
+}
+
+__device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// One block: lanes per config, work items, LPT order of buckets by weight
+// class (heaviest first), config ranges.
+__global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
+  __shared__ unsigned int s_items[kNumClasses];
+  __shared__ unsigned int s_base[kNumClasses];
+  __shared__ unsigned int s_cfg, s_nb;
+  for (int c = threadIdx.x; c < kNumClasses; c += blockDim.x) s_items[c] = 0;
+  if (threadIdx.x == 0) { s_cfg = 0; s_nb = 0; }
+  __syncthreads();
+  for (int b = threadIdx.x; b <= kNumBuckets; b += blockDim.x) {
+    Bucket& B = bk[b];
+    if (B.count == 0) continue;
+    uint32_t lanes, cls;
+    if (b == kOverflowBucket) {
+      lanes = 32;
+      cls = kNumClasses - 1;
+    } else {
+      const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, L = ((B.key >> 7) & 1023) + 1,
+                     K = (B.key >> 17) & 255;
+      lanes = P < 32 ? pow2ceil32(P) : 32;
+      const unsigned long long per = (L + P - 1) / P;
+      unsigned long long est = (2ull * K + P) * per * (kind ? 14ull : 8ull) + 1;
+      cls = 63 - __clzll(est);
+      if (cls >= kNumClasses) cls = kNumClasses - 1;
+    }
+    const uint32_t cpw = 32 / lanes;
+    const uint32_t items = (B.count + cpw - 1) / cpw;
+    B.lanes = lanes;
+    B.cls = cls;
+    B.item_off = atomicAdd(&s_items[cls], items);
+    B.cfg_base = atomicAdd(&s_cfg, B.count);
+    B.cursor = 0;
+    atomicAdd(&s_nb, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int base = 0;
+    for (int c = kNumClasses - 1; c >= 0; c--) { s_base[c] = base; base += s_items[c]; }
+    hdr->n_items = base;
+    hdr->n_buckets = s_nb;
+    hdr->cfg_total = s_cfg;
+    hdr->item_counter = 0;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b <= kNumBuckets; b += blockDim.x) {
+    Bucket& B = bk[b];
+    if (B.count == 0) continue;
+    B.item_base = s_base[B.cls] + B.item_off;
+  }
+}
+
+__global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
+                          const uint32_t* __restrict__ cfg_bucket, uint32_t* __restrict__ perm,
+                          Item* __restrict__ items) {
+  const int64_t nloc = spp->n_local;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nloc;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = cfg_bucket[q];
+    if (b == kEmptyKey) continue;
+    const uint32_t pos = atomicAdd(&bk[b].cursor, 1u);
+    const uint32_t cpw = 32 / bk[b].lanes;
+    perm[bk[b].cfg_base + pos] = (uint32_t)q;
+    if (pos % cpw == 0) {
+      const uint32_t cnt = bk[b].count;
+      Item it;
+      it.first = bk[b].cfg_base + pos;
+      it.bucket = (uint16_t)b;
+      it.n = (uint8_t)(cnt - pos < cpw ? cnt - pos : cpw);
+      it.pad = 0;
+      items[bk[b].item_base + pos / cpw] = it;
+    }
+  }
+}
+
+// Persistent: each warp pulls work items (heaviest classes first).
+__global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ spp,
+                                                  const DExplicit* __restrict__ ex,
+                                                  const Bucket* __restrict__ bk,
+                                                  const Item* __restrict__ items,
+                                                  const uint32_t* __restrict__ perm,
+                                                  WsHeader* __restrict__ hdr,
+                                                  double* __restrict__ ms_out,
+                                                  int64_t* __restrict__ pk_out,
+                                                  uint32_t* __restrict__ rs_out,
+                                                  double* __restrict__ tp_out) {
+  const SpecBlock& sp = *spp;
+  const int lane = threadIdx.x & 31;
+  const unsigned int n_items = *(volatile unsigned int*)&hdr->n_items;
+  unsigned long long feas = 0;
+  while (true) {
+    unsigned int id = 0;
+    if (lane == 0) id = (unsigned int)atomicAdd(&hdr->item_counter, 1ull);
+    id = __shfl_sync(0xffffffffu, id, 0);
+    if (id >= n_items) break;
+    const Item it = items[id];
+    const Bucket& B = bk[it.bucket];
+    const int S = (int)B.lanes;
+    const int seg = lane / S, sl = lane - seg * S;
+    const bool has = seg < it.n;
+    const uint32_t q = has ? perm[it.first + seg] : 0u;
+    Cfg c;
+    if (has) {
+      decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);
+    } else {
+      c.M = DModel{0, 1, 1, 1, 1, 1, 1, 1, 1, 0};
+      c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
+    }
+    const DTopo& tp = sp.topos[c.topo];
+    const bool wide = __any_sync(0xffffffffu, has && c.P > 32);
+    const bool gpt = __any_sync(0xffffffffu, has && c.M.kind == 1);
+    double ms;
+    int64_t pk;
+    if (gpt) {
+      if (wide) run_gpt2<2>(c, tp, has, sl, S, lane, ms, pk);
+      else run_gpt2<1>(c, tp, has, sl, S, lane, ms, pk);
+    } else {
+      if (wide) run_mlp<2>(c, tp, has, sl, S, lane, ms, pk);
+      else run_mlp<1>(c, tp, has, sl, S, lane, ms, pk);
+    }
+    // makespan and peak: max over the stages of the segment
+    for (int o = S >> 1; o > 0; o >>= 1) {
+      ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+      const int64_t po = __shfl_xor_sync(0xffffffffu, pk, o);
+      pk = pk > po ? pk : po;
+    }
+    if (has && sl == 0) {
+      const uint32_t r = pk > tp.capacity ? kCapacityBit : 0u;
+      ms_out[q] = ms;
+      pk_out[q] = pk;
+      rs_out[q] = r;
+      tp_out[q] = r ? 0.0 : __ddiv_rn(__ll2double_rn(c.B), ms);
+      feas += r == 0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) feas += __shfl_xor_sync(0xffffffffu, feas, o);
+  if (lane == 0 && feas) atomicAdd(&hdr->n_feasible, feas);
+}
+
+// ------------------------------------------------------------ top-k ---------
+struct Key {
+  double tp;
+  int64_t peak, idx;
+  double ms;
+};
+
+__device__ __forceinline__ bool better(const Key& a, const Key& b) {
+  if (a.tp != b.tp) return a.tp > b.tp;
+  if (a.peak != b.peak) return a.peak < b.peak;
+  return a.idx < b.idx;
+}
+
+__device__ __forceinline__ Key worst_key() { return Key{-1.0, LLONG_MAX, LLONG_MAX, 0.0}; }
+
+__device__ __forceinline__ Key shfl_key(const Key& k, int o) {
+  Key r;
+  r.tp = __shfl_xor_sync(0xffffffffu, k.tp, o);
+  r.peak = __shfl_xor_sync(0xffffffffu, k.peak, o);
+  r.idx = __shfl_xor_sync(0xffffffffu, k.idx, o);
+  r.ms = __shfl_xor_sync(0xffffffffu, k.ms, o);
+  return r;
+}
+
+// Block-wide argmax under `better` (blockDim.x == 256).
+__device__ Key block_best(Key k) {
+  __shared__ Key s_k[8];
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key x = shfl_key(k, o);
+    if (better(x, k)) k = x;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_k[w] = k;
+  __syncthreads();
+  Key b = s_k[0];
+  for (int i = 1; i < 8; i++)
+    if (better(s_k[i], b)) b = s_k[i];
+  __syncthreads();
+  return b;
+}
+
+// Select the k best of a candidate set, one round per rank: round r keeps the
+// best candidate strictly worse than round r-1's winner (keys are unique).
+template <typename Fetch>
+__device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
+  Key prev{__longlong_as_double(0x7FF0000000000000ll), LLONG_MIN, LLONG_MIN, 0.0};
+  int got = 0;
+  for (int r = 0; r < k; r++) {
+    Key best = worst_key();
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      Key c;
+      if (!fetch(j, c)) continue;
+      if (better(prev, c) && better(c, best)) best = c;
+    }
+    best = block_best(best);
+    if (best.idx == LLONG_MAX) break;
+    if (threadIdx.x == 0) out[r] = TopkRec{best.idx, best.ms, best.tp, best.peak};
+    prev = best;
+    got++;
+  }
+  return got;
+}
+
+__global__ void __launch_bounds__(256) k_topk_partial(const SpecBlock* __restrict__ spp,
+                                                      const double* __restrict__ ms,
+                                                      const int64_t* __restrict__ pk,
+                                                      const uint32_t* __restrict__ rs,
+                                                      const double* __restrict__ tpv, int k,
+                                                      TopkRec* __restrict__ part,
+                                                      int* __restrict__ part_n) {
+  const SpecBlock& sp = *spp;
+  const int64_t n = sp.n_local;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t a = blockIdx.x * chunk;
+  const int64_t b = a + chunk < n ? a + chunk : n;
+  const int64_t rank = sp.rank, nr = sp.n_ranks;
+  auto fetch = [&](int64_t j, Key& c) -> bool {
+    const int64_t q = a + j;
+    if (rs[q] != 0) return false;
+    c = Key{tpv[q], pk[q], rank + q * nr, ms[q]};
+    return true;
+  };
+  const int got = select_topk(b > a ? b - a : 0, k, fetch, part + (int64_t)blockIdx.x * k);
+  if (threadIdx.x == 0) part_n[blockIdx.x] = got;
+}
+
+// Merge n_lists lists of up to k records (counts in list_n, or all k valid
+// when list_n == NULL and index >= 0 marks a valid record).
+__global__ void __launch_bounds__(256) k_topk_merge(const TopkRec* __restrict__ lists,
+                                                    const int* __restrict__ list_n, int n_lists,
+                                                    int k_in, int k, TopkRec* __restrict__ out,
+                                                    int* __restrict__ out_n) {
+  auto fetch = [&](int64_t j, Key& c) -> bool {
+    const int l = (int)(j / k_in), r = (int)(j - (int64_t)l * k_in);
+    if (list_n ? r >= list_n[l] : lists[j].index < 0) return false;
+    const TopkRec x = lists[j];
+    c = Key{x.throughput, x.peak, x.index, x.makespan};
+    return true;
+  };
+  const int got = select_topk((int64_t)n_lists * k_in, k, fetch, out);
+  if (threadIdx.x == 0) {
+    *out_n = got;
+    for (int r = got; r < k; r++) out[r] = TopkRec{-1, 0.0, -1.0, -1};
+  }
+}
+
+}  // namespace distir

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+the same seeded inputs.
+
+Bars (BASELINE north_star): reason bits, peak bytes, config indices and top-k
+order bit-exact; fp64 makespans within relative error 1e-12 (the kernels are
+designed to be bit-exact, and the tests also report the bit-exact fraction).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def sim():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2111_05426_b200 import Simulator
+    s = Simulator(W.MODELS, W.TOPOLOGIES, device=0)
+    yield s
+    s.close()
+
+
+def assert_parity(got, ref, what=""):
+    """got/ref: dicts with makespan, peak, reason arrays aligned."""
+    assert (got["reason"] == ref["reason"]).all(), (
+        what, np.nonzero(got["reason"] != ref["reason"])[0][:10])
+    valid = (ref["reason"] & 0x1F) == 0
+    assert (got["peak"][valid] == ref["peak"][valid]).all(), (
+        what, np.nonzero(got["peak"] != ref["peak"])[0][:10])
+    assert (got["peak"][~valid] == -1).all()
+    assert np.isinf(got["makespan"][~valid]).all()
+    g, r = got["makespan"][valid], ref["makespan"][valid]
+    rel = np.abs(g - r) / np.maximum(np.abs(r), 1e-300)
+    assert rel.max(initial=0.0) <= TOL, (what, rel.max())
+    return float((g == r).mean()) if len(g) else 1.0
+
+
+def full_grid_check(sim, grid, k=10):
+    res = sim.eval(grid, k=k)
+    ref = oracle.grid_result(grid, k=k, threads=THREADS)
+    exact = assert_parity(res, ref, str(grid["models"]))
+    assert res["topk"]["index"].tolist() == ref["topk_index"].tolist()
+    assert (res["topk"]["throughput"] == ref["topk_throughput"]).all()
+    st = res["stats"]
+    valid = (ref["reason"] & 0x1F) == 0
+    assert st["n_valid"] == int(valid.sum())
+    assert st["n_feasible"] == int((ref["reason"] == 0).sum())
+    assert st["op_events"] == int(ref["n_ops"][valid].sum())
+    return exact
+
+
+def test_w1_full(sim):
+    """BASELINE configs[0]: 2-layer MLP dim 64, W <= 4, K in {1, 2}."""
+    for topo in ["TB200", "TV100", "TM0", "TM5"]:
+        assert full_grid_check(sim, W.grid_with("W1", topos=[topo])) == 1.0
+
+
+def test_w2_full(sim):
+    """BASELINE configs[1]: the paper's MLP-1B training grid (1860 configs)."""
+    assert full_grid_check(sim, W.GRIDS["W2"]) == 1.0
+
+
+def test_w3_full(sim):
+    """BASELINE configs[2]: GPT-2 small..XL inference grid (8680 configs),
+    the bench workload, whole grid against the oracle."""
+    assert full_grid_check(sim, W.GRIDS["W3"]) == 1.0
+
+
+def test_w4_full(sim):
+    """BASELINE configs[3]: 64-layer MLP, P up to 64 (two stages per lane),
+    K up to 128."""
+    assert full_grid_check(sim, W.GRIDS["W4"]) == 1.0
+
+
+def test_paper_grids(sim):
+    """Table 1 grids on the V100-shaped topology."""
+    for name in ["PM_1B", "PM_17B", "PM_103B"]:
+        assert full_grid_check(sim, W.GRIDS[name]) == 1.0
+
+
+def test_w5_sampled(sim):
+    """BASELINE configs[4]: 10^6 synthetic configs, W <= 64, mixed topologies,
+    evaluated in full on the GPU; a seeded sample checked against the
+    oracle."""
+    grid = W.GRIDS["W5"]
+    res = sim.eval(grid, k=10)
+    n = res["n"]
+    assert n == 10 ** 6
+    rng = np.random.default_rng(20211105426)
+    idx = np.sort(rng.choice(n, 600, replace=False))
+    idx = np.unique(np.concatenate([idx, res["topk"]["index"]]))
+    ref = oracle.grid_eval(grid, indices=idx, threads=THREADS)
+    assert_parity({k: res[k][idx] for k in ("makespan", "peak", "reason")}, ref, "W5")
+    # the top-k are feasible and ordered
+    tk = res["topk"]
+    assert (res["reason"][tk["index"]] == 0).all()
+    key = list(zip(-tk["throughput"], tk["peak_bytes"], tk["index"]))
+    assert key == sorted(key)
+    # nothing outside the top-k beats the k-th entry
+    tpall = np.where(res["reason"] == 0, 0.0, -1.0)
+    ok = res["reason"] == 0
+    B = oracle.enumerate_grid(dict(grid, synth_count=n))[:, 7]
+    tpall[ok] = B[ok] / res["makespan"][ok]
+    kth = (-tk["throughput"][-1], tk["peak_bytes"][-1], tk["index"][-1])
+    better = ok & ((tpall > tk["throughput"][-1]) |
+                   ((tpall == tk["throughput"][-1]) & (res["peak"] < tk["peak_bytes"][-1])))
+    assert set(np.nonzero(better)[0]) <= set(tk["index"].tolist())
+    assert kth is not None
+
+
+def _random_explicit(seed, n):
+    rng = np.random.default_rng(seed)
+    models = list(W.MODELS)
+    topos = list(W.TOPOLOGIES)
+    out = []
+    for _ in range(n):
+        mi = int(rng.integers(len(models)))
+        m = W.MODELS[models[mi]]
+        ti = int(rng.integers(len(topos)))
+        D = 1 << int(rng.integers(0, 3))
+        T = 1 << int(rng.integers(0, 3))
+        P = int(rng.integers(1, 9))                  # not only powers of two
+        P = min(P, 64 // (D * T))
+        K = int(rng.integers(1, 9))
+        B = D * K * int(rng.integers(1, 5)) * (1 if rng.random() < 0.9 else 3)
+        if rng.random() < 0.05:
+            B += 1                                   # ragged -> invalid
+        out.append((mi, ti, D, T, P, K, B))
+    return models, topos, out
+
+
+def test_explicit_configs_random(sim):
+    """Explicit configuration lists: non-power-of-two P, ragged batches,
+    every model and topology (incl. node size 4), against the oracle one by
+    one."""
+    models, topos, cfgs = _random_explicit(7, 300)
+    # keep the oracle fast: cap the biggest programs
+    cfgs = [c for c in cfgs if W.MODELS[models[c[0]]]["n_layer"] <= 48]
+    res = sim.eval(configs=cfgs, k=16)
+    ref = {"makespan": [], "peak": [], "reason": []}
+    for (mi, ti, D, T, P, K, B) in cfgs:
+        r = oracle.eval_config(W.MODELS[models[mi]], W.TOPOLOGIES[topos[ti]], D, T, P, K, B)
+        ref["makespan"].append(r["makespan"]); ref["peak"].append(r["peak"])
+        ref["reason"].append(r["reason"])
+    ref = {k: np.array(v) for k, v in ref.items()}
+    ref["reason"] = ref["reason"].astype(np.uint32)
+    assert_parity(res, ref, "explicit")
+    bt = np.array([c[6] for c in cfgs])
+    pos, tp = oracle.topk(np.arange(len(cfgs)), bt, ref["makespan"], ref["peak"],
+                          ref["reason"], 16)
+    assert res["topk"]["index"].tolist() == pos.tolist()
+
+
+def test_small_models_edge_shapes(sim):
+    """Tiny models exercising odd layer counts, P = L, lm_head off, T up to
+    8 and a 4-GPU node size."""
+    from paper_2111_05426_b200 import Simulator
+    models = {
+        "m1": W.mlp(1, 16), "m3": W.mlp(3, 32), "m5": W.mlp(5, 8),
+        "g1": dict(W.MODELS["gpt2_small"], n_layer=1, d_model=64, n_head=8,
+                   vocab_pad=256, n_ctx=32),
+        "g3": dict(W.MODELS["gpt2_small"], n_layer=3, d_model=64, n_head=8,
+                   vocab_pad=256, n_ctx=32, lm_head=0),
+        "g7": dict(W.MODELS["gpt2_small"], n_layer=7, d_model=128, n_head=8,
+                   vocab_pad=512, n_ctx=64, seq_len=4),
+    }
+    topos = {"TM0": W.TOPOLOGIES["TM0"], "TB200": W.TOPOLOGIES["TB200"]}
+    s = Simulator(models, topos, device=0)
+    cfgs = []
+    for mi, name in enumerate(models):
+        L = models[name]["n_layer"]
+        for ti in range(2):
+            for (D, T) in [(1, 1), (2, 1), (1, 2), (2, 4), (1, 8)]:
+                for P in sorted({1, 2, L, max(1, L - 1)}):
+                    for K in [1, 2, 3]:
+                        cfgs.append((mi, ti, D, T, P, K, D * K * 2))
+    res = s.eval(configs=cfgs, k=8)
+    ref = {"makespan": [], "peak": [], "reason": []}
+    for (mi, ti, D, T, P, K, B) in cfgs:
+        r = oracle.eval_config(models[list(models)[mi]], topos[list(topos)[ti]],
+                               D, T, P, K, B)
+        for k in ref:
+            ref[k].append(r[k])
+    ref = {k: np.array(v) for k, v in ref.items()}
+    ref["reason"] = ref["reason"].astype(np.uint32)
+    assert assert_parity(res, ref, "edge") == 1.0
+    s.close()
+
+
+def test_edge_cases(sim):
+    """Empty list, k = 0, k = 64 > #feasible, an all-invalid grid."""
+    res = sim.eval(configs=[], k=10)
+    assert res["n"] == 0 and len(res["topk"]) == 0
+    res = sim.eval(W.GRIDS["W1"], k=0)
+    assert len(res["topk"]) == 0 and len(res["makespan"]) == 20
+    res = sim.eval(W.GRIDS["W1"], k=64)
+    assert len(res["topk"]) == 18
+    bad = W.grid_with("W1", batch=[3])              # D*K never divides 3 ... except 1
+    r2 = sim.eval(bad, k=5)
+    ref = oracle.grid_result(bad, k=5)
+    assert_parity(r2, ref, "bad")
+    assert r2["topk"]["index"].tolist() == ref["topk_index"].tolist()
+
+
+def test_device_launch_matches_host_eval(sim):
+    """upload + launch (device-resident, the timed path) == grid_eval."""
+    import torch
+    from paper_2111_05426_b200 import topk_from_device
+    grid = W.GRIDS["W3"]
+    host = sim.eval(grid, k=10)
+    n = sim.upload(grid)
+    outs = sim.device_outputs(n, k=10)
+    sim.launch(outs, k=10)
+    torch.cuda.synchronize()
+    assert (outs["makespan"].cpu().numpy() == host["makespan"]).all()
+    assert (outs["peak"].cpu().numpy() == host["peak"]).all()
+    nt = int(outs["ntopk"].item())
+    tk = topk_from_device(outs["topk"], nt)
+    assert tk["index"].tolist() == host["topk"]["index"].tolist()
+    # repeated launches are deterministic
+    sim.launch(outs, k=10)
+    torch.cuda.synchronize()
+    assert (outs["makespan"].cpu().numpy() == host["makespan"]).all()
+
+
+def test_virtual_shards_merge(sim):
+    """Round-robin shards evaluated one after another on one GPU: per-config
+    results are the same, and merging the local top-k lists (test-side
+    sort) gives the single-GPU top-k."""
+    import torch
+    from paper_2111_05426_b200 import topk_from_device
+    grid = W.GRIDS["W3"]
+    full = sim.eval(grid, k=10)
+    for G in [2, 3, 8]:
+        recs = []
+        for g in range(G):
+            n = sim.upload(grid, rank=g, n_ranks=G)
+            outs = sim.device_outputs(n, k=10)
+            sim.launch(outs, k=10)
+            torch.cuda.synchronize()
+            assert (outs["makespan"].cpu().numpy()[:n] == full["makespan"][g::G]).all()
+            recs.append(topk_from_device(outs["topk"], int(outs["ntopk"].item())))
+        allr = np.concatenate(recs)
+        order = sorted(range(len(allr)), key=lambda i: (-allr["throughput"][i],
+                                                        allr["peak_bytes"][i],
+                                                        allr["index"][i]))[:10]
+        assert allr["index"][order].tolist() == full["topk"]["index"].tolist()
+
+
+def test_nccl_single_rank(sim):
+    """The NCCL merge path with a 1-rank communicator."""
+    import paper_2111_05426_b200 as pkg
+    uid = pkg.distir_nccl_unique_id()
+    comm = pkg.distir_nccl_comm_init(uid, 1, 0, 0)
+    try:
+        res = sim.eval(W.GRIDS["W1"], k=10, comm=comm)
+        ref = sim.eval(W.GRIDS["W1"], k=10)
+        assert res["topk"]["index"].tolist() == ref["topk"]["index"].tolist()
+    finally:
+        pkg.distir_nccl_comm_destroy(comm)
