@@ -27,6 +27,7 @@
 #include <cfloat>
 #include <climits>
 #include "common.cuh"
+#include "exact_add.cuh"
 
 namespace distir {
 
@@ -228,305 +229,7 @@ struct Par {
   __device__ __forceinline__ T operator[](int p) const { return p ? b : a; }
 };
 
-// -------------------------------------------------- MLP training (C.3) -------
-template <int V>
-__device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                        double& ms_out, int64_t& peak_out) {
-  const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
-  const int64_t m = has ? c.B / (D * K) : 0;
-  const int32_t ns = tp.node_size;
-  // Layer shapes by parity of the global layer index: even = column
-  // parallel, odd = row parallel (Megatron pairing); T = 1: both full.
-  const Par<int64_t> kin{d, d / T}, nout{d / T, d}, dout{d / T, d};
-  const bool tp_intra = group_intra(0, T - 1, ns);
-  const bool dp_intra = group_intra(0, T * (D - 1), ns);
-  Par<double> mm, relu, rg, mmg, add, sgd, ardp;
-  Par<int64_t> Wb;
-  {
-    const int64_t w0 = kin.a * nout.a, w1 = kin.b * nout.b;
-    mm = {cost_compute(2 * m * w0, tp), cost_compute(2 * m * w1, tp)};
-    relu = {cost_compute(m * dout.a, tp), cost_compute(m * dout.b, tp)};
-    rg = relu;
-    mmg = {cost_compute(4 * m * w0, tp), cost_compute(4 * m * w1, tp)};
-    add = {cost_compute(w0, tp), cost_compute(w1, tp)};
-    sgd = {cost_compute(2 * w0, tp), cost_compute(2 * w1, tp)};
-    Wb = {w0 * e, w1 * e};
-    ardp = {D > 1 ? cost_allreduce(D, Wb.a, dp_intra, tp) : 0.0,
-            D > 1 ? cost_allreduce(D, Wb.b, dp_intra, tp) : 0.0};
-  }
-  const int64_t mde = m * d * e;
-  const double ar_tp = T > 1 ? cost_allreduce(T, mde, tp_intra, tp) : 0.0;
-  const int64_t ar_b = T > 1 ? mde : 0;
-  const int64_t dlast = dout[(L - 1) & 1];
-  const double loss = cost_compute(3 * m * dlast, tp);
-
-  int s[V], lo[V], hi[V];
-  bool ok[V];
-  double clk[V], sendf[V], sendb[V];
-  int64_t live[V], peak[V];
-#pragma unroll
-  for (int q = 0; q < V; q++) {
-    s[q] = sl + S * q;
-    ok[q] = has && s[q] < P;
-    lo[q] = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
-    hi[q] = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
-    const int64_t r0 = T * D * (int64_t)s[q];    // rank (0, 0, s)
-    sendf[q] = (ok[q] && s[q] < P - 1)
-                   ? cost_send(m * dout[(hi[q] - 1) & 1] * e, group_intra(r0, r0 + T * D, ns), tp)
-                   : 0.0;
-    sendb[q] = (ok[q] && s[q] > 0)
-                   ? cost_send(m * kin[lo[q] & 1] * e, group_intra(r0 - T * D, r0, ns), tp)
-                   : 0.0;
-    int64_t lv = 0;
-    for (int l = lo[q]; l < hi[q]; l++) lv += 2 * Wb[l & 1];       // W_l, G_l
-    if (ok[q] && s[q] == 0) lv += K * mde;                         // X_k
-    if (ok[q] && s[q] == P - 1) lv += K * m * dlast * e;           // Y_k
-    live[q] = lv; peak[q] = lv; clk[q] = 0.0;
-  }
-
-  // ---- forward wavefront: task (k, s) at step 2k + s
-  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
-  for (int w = 0; w < nsteps; w++) {
-    bool act[V];
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      const int kk = w - s[q];
-      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) {
-        for (int l = lo[q]; l < hi[q]; l++) {
-          const int p = l & 1;
-          clk[q] = dadd(clk[q], mm[p]);                       // MatMul
-          MEM(q, m * nout[p] * e, 0);
-          clk[q] = dadd(clk[q], p ? ar_tp : 0.0);             // TP AllReduce (row)
-          MEM(q, p ? ar_b : 0, p ? ar_b : 0);
-          clk[q] = dadd(clk[q], relu[p]);                     // Relu
-          MEM(q, m * dout[p] * e, m * dout[p] * e);
-        }
-      }
-    }
-    // Send s -> s+1: both ends wait for each other
-    double nb[V], t[V];
-    bool snd[V], rin[V];
-    Nbr<V>::up_stage(clk, nb, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      snd[q] = act[q] && s[q] < P - 1;
-      t[q] = dadd(fmax(clk[q], nb[q]), sendf[q]);
-      if (snd[q]) clk[q] = t[q];
-    }
-    double tin[V];
-    Nbr<V>::down_stage(t, tin, lane);
-    Nbr<V>::down_flag(snd, rin, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] > 0 && rin[q]) {
-        clk[q] = tin[q];
-        MEM(q, m * kin[lo[q] & 1] * e, 0);                    // received activation
-      }
-    }
-  }
-
-  // ---- backward wavefront: task (k, s) at step 2k + (P-1-s)
-  for (int w = 0; w < nsteps; w++) {
-    bool act[V];
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      const int kk = w - (int)(P - 1 - s[q]);
-      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) {
-        if (s[q] == P - 1) {                                  // LossGrad
-          clk[q] = dadd(clk[q], loss);
-          MEM(q, m * dlast * e, m * dlast * e);
-        }
-        for (int l = hi[q] - 1; l >= lo[q]; l--) {
-          const int p = l & 1;
-          const int64_t act_b = m * dout[p] * e;
-          clk[q] = dadd(clk[q], rg[p]);                       // ReluGrad
-          MEM(q, act_b, 2 * act_b);
-          const int64_t din = m * kin[p] * e;
-          const bool first = l == lo[q];
-          const bool dead0 = s[q] == 0 && l == 0;             // dA_0 has no user
-          clk[q] = dadd(clk[q], mmg[p]);                      // MatMulGrad
-          MEM(q, din + Wb[p], act_b + (first ? din : 0) + ((dead0 && T == 1) ? din : 0));
-          const bool col_ar = p == 0 && T > 1;
-          clk[q] = dadd(clk[q], col_ar ? ar_tp : 0.0);        // TP AllReduce (col)
-          MEM(q, col_ar ? mde : 0, col_ar ? (mde + (dead0 ? mde : 0)) : 0);
-          clk[q] = dadd(clk[q], add[p]);                      // gradient accumulation
-          MEM(q, Wb[p], 2 * Wb[p]);
-        }
-      }
-    }
-    // Send s -> s-1
-    double nb[V], t[V];
-    bool snd[V], rin[V];
-    Nbr<V>::down_stage(clk, nb, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      snd[q] = act[q] && s[q] > 0;
-      t[q] = dadd(fmax(clk[q], nb[q]), sendb[q]);
-      if (snd[q]) {
-        clk[q] = t[q];
-        live[q] -= m * kin[lo[q] & 1] * e;                    // sent gradient dies
-      }
-    }
-    double tin[V];
-    Nbr<V>::up_stage(t, tin, lane);
-    Nbr<V>::up_flag(snd, rin, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] < P - 1 && rin[q]) {
-        clk[q] = tin[q];
-        MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);             // received gradient
-      }
-    }
-  }
-
-  // ---- tail: DP AllReduce of the accumulated gradients, then SGD
-#pragma unroll
-  for (int q = 0; q < V; q++) {
-    if (!ok[q]) continue;
-    for (int l = hi[q] - 1; l >= lo[q]; l--) {
-      const int p = l & 1;
-      clk[q] = dadd(clk[q], ardp[p]);
-      MEM(q, D > 1 ? Wb[p] : 0, D > 1 ? Wb[p] : 0);
-    }
-    for (int l = lo[q]; l < hi[q]; l++) {
-      const int p = l & 1;
-      clk[q] = dadd(clk[q], sgd[p]);
-      MEM(q, Wb[p], 2 * Wb[p]);
-    }
-  }
-  double msx = 0.0;
-  int64_t pkx = 0;
-#pragma unroll
-  for (int q = 0; q < V; q++) {
-    if (ok[q]) { msx = fmax(msx, clk[q]); pkx = pkx > peak[q] ? pkx : peak[q]; }
-  }
-  ms_out = msx;
-  peak_out = pkx;
-}
-
-// ------------------------------------------------ GPT-2 inference (C.4) -----
-template <int V>
-__device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                         double& ms_out, int64_t& peak_out) {
-  const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
-                ide = c.M.ide, nctx = c.M.nctx;
-  const bool lm = c.M.lm != 0;
-  const int64_t D = c.D, T = c.T, P = c.P, K = c.K;
-  const int64_t m = has ? c.B / (D * K) : 0;
-  const int64_t n = m * Sq, dT = d / T, hT = h / T, VT = Vp / T;
-  const int32_t ns = tp.node_size;
-  const bool tp_intra = group_intra(0, T - 1, ns);
-  // costs (C.4 work per op)
-  const double c_emb = cost_compute(2 * n * d, tp);
-  const double c_ln = cost_compute(5 * n * d, tp);
-  const double c_qkv = cost_compute(2 * n * d * (3 * dT) + n * (3 * dT), tp);
-  const double c_att = cost_compute(2 * m * Sq * Sq * dT, tp);
-  const double c_smx = cost_compute(5 * m * hT * Sq * Sq, tp);
-  const double c_prj = cost_compute(2 * n * dT * d + n * d, tp);
-  const double c_add = cost_compute(n * d, tp);
-  const double c_fc1 = cost_compute(2 * n * d * (4 * dT) + n * (4 * dT), tp);
-  const double c_gel = cost_compute(8 * n * (4 * dT), tp);
-  const double c_fc2 = cost_compute(2 * n * (4 * dT) * d + n * d, tp);
-  const double c_lmh = cost_compute(2 * n * d * VT, tp);
-  const int64_t nde = n * d * e;
-  const double c_ar = T > 1 ? cost_allreduce(T, nde, tp_intra, tp) : 0.0;
-  const double c_ag = T > 1 ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0;
-  const int64_t arb = T > 1 ? nde : 0;
-  // value sizes
-  const int64_t qkvb = n * 3 * dT * e, scb = m * hT * Sq * Sq * e, ctxb = n * dT * e, fb = n * 4 * dT * e;
-  const int64_t ln_p = 2 * d * e, qkv_p = (d * 3 * dT + 3 * dT) * e, prj_p = (dT * d + d) * e,
-                fc1_p = (d * 4 * dT + 4 * dT) * e, fc2_p = (4 * dT * d + d) * e;
-  const int64_t blk_p = 2 * ln_p + qkv_p + prj_p + fc1_p + fc2_p;
-  const int64_t wte_b = VT * d * e, wpe_b = nctx * d * e;
-
-  int s[V], lo[V], hi[V];
-  bool ok[V];
-  double clk[V], sendf[V];
-  int64_t live[V], peak[V];
-#pragma unroll
-  for (int q = 0; q < V; q++) {
-    s[q] = sl + S * q;
-    ok[q] = has && s[q] < P;
-    lo[q] = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
-    hi[q] = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
-    const int64_t r0 = T * D * (int64_t)s[q];
-    sendf[q] = (ok[q] && s[q] < P - 1) ? cost_send(nde, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
-    int64_t lv = (int64_t)(hi[q] - lo[q]) * blk_p;
-    if (ok[q] && s[q] == 0) lv += wte_b + wpe_b + K * n * ide;
-    if (ok[q] && s[q] == P - 1) lv += 2 * d * e + ((lm && P > 1) ? wte_b : 0);
-    live[q] = lv; peak[q] = lv; clk[q] = 0.0;
-  }
-
-  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
-  for (int w = 0; w < nsteps; w++) {
-    bool act[V];
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      const int kk = w - s[q];
-      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (!act[q]) continue;
-      const bool last = (kk >> 1) == K - 1;
-      if (s[q] == 0) {                                        // prologue
-        clk[q] = dadd(clk[q], c_emb);                          // Embed
-        MEM(q, nde, n * ide + (last ? wpe_b + ((P == 1 && lm) ? 0 : wte_b) : 0));
-        clk[q] = dadd(clk[q], c_ar);                           // TP AllReduce
-        MEM(q, arb, arb);
-      }
-      for (int l = lo[q]; l < hi[q]; l++) {                   // blocks
-        clk[q] = dadd(clk[q], c_ln);   MEM(q, nde, last ? ln_p : 0);
-        clk[q] = dadd(clk[q], c_qkv);  MEM(q, qkvb, nde + (last ? qkv_p : 0));
-        clk[q] = dadd(clk[q], c_att);  MEM(q, scb, 0);
-        clk[q] = dadd(clk[q], c_smx);  MEM(q, scb, scb);
-        clk[q] = dadd(clk[q], c_att);  MEM(q, ctxb, scb + qkvb);
-        clk[q] = dadd(clk[q], c_prj);  MEM(q, nde, ctxb + (last ? prj_p : 0));
-        clk[q] = dadd(clk[q], c_ar);   MEM(q, arb, arb);
-        clk[q] = dadd(clk[q], c_add);  MEM(q, nde, 2 * nde);
-        clk[q] = dadd(clk[q], c_ln);   MEM(q, nde, last ? ln_p : 0);
-        clk[q] = dadd(clk[q], c_fc1);  MEM(q, fb, nde + (last ? fc1_p : 0));
-        clk[q] = dadd(clk[q], c_gel);  MEM(q, fb, fb);
-        clk[q] = dadd(clk[q], c_fc2);  MEM(q, nde, fb + (last ? fc2_p : 0));
-        clk[q] = dadd(clk[q], c_ar);   MEM(q, arb, arb);
-        clk[q] = dadd(clk[q], c_add);  MEM(q, nde, 2 * nde);
-      }
-      if (s[q] == P - 1) {                                    // epilogue
-        clk[q] = dadd(clk[q], c_ln);                           // final LayerNorm
-        MEM(q, nde, nde + (last ? 2 * d * e : 0));
-        if (lm) {
-          clk[q] = dadd(clk[q], c_lmh);                        // LM head
-          MEM(q, n * VT * e, nde + (last ? wte_b : 0));
-          clk[q] = dadd(clk[q], c_ag);                         // logits AllGather
-          MEM(q, T > 1 ? n * Vp * e : 0, T > 1 ? n * VT * e : 0);
-        }
-      }
-    }
-    double nb[V], t[V];
-    bool snd[V], rin[V];
-    Nbr<V>::up_stage(clk, nb, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      snd[q] = act[q] && s[q] < P - 1;
-      t[q] = dadd(fmax(clk[q], nb[q]), sendf[q]);
-      if (snd[q]) { clk[q] = t[q]; live[q] -= nde; }          // sent activation dies
-    }
-    double tin[V];
-    Nbr<V>::down_stage(t, tin, lane);
-    Nbr<V>::down_flag(snd, rin, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] > 0 && rin[q]) { clk[q] = tin[q]; MEM(q, nde, 0); }
-    }
-  }
-  double msx = 0.0;
-  int64_t pkx = 0;
-#pragma unroll
-  for (int q = 0; q < V; q++) {
-    if (ok[q]) { msx = fmax(msx, clk[q]); pkx = pkx > peak[q] ? pkx : peak[q]; }
-  }
-  ms_out = msx;
-  peak_out = pkx;
-}
+#include "simulate.cuh"
 #undef MEM
 
 // ------------------------------------------------------------- kernels ------

@@ -1,0 +1,354 @@
+// simulate.cuh -- per-configuration walk of the D/T/P + GPipe program
+// (rows a2-a5).  Included by kernels.cuh inside namespace distir, after the
+// cost helpers, the MEM macro, Par and Nbr.
+//
+// Per lane = one pipeline stage (two when 32 < P <= 64).  A *task* is the
+// stage's ops for one microbatch (SURVEY C.3 / C.4 emission order); its clock
+// advance is applied with add_reps (exact_add.cuh: bit-identical to one IEEE
+// add per op) and its live-memory effect with a precomputed MemProf (exact
+// integer composition of the per-op alloc/peak/free steps of C.7).  Sends
+// between stages are exact max + one add, exchanged with warp shuffles.
+
+// Alternating-parity layer runs: n layers starting at parity p0, layer
+// sequences A (even / column-parallel) and B (odd / row-parallel).
+template <int N>
+struct AltSeq {
+  double A[N], B[N], AB[2 * N];
+  SeqCache cA, cB, cAB;
+  __device__ void init(const double (&a)[N], const double (&b)[N]) {
+#pragma unroll
+    for (int j = 0; j < N; j++) { A[j] = a[j]; B[j] = b[j]; AB[j] = a[j]; AB[N + j] = b[j]; }
+    cA = cB = cAB = seq_cache_empty();
+  }
+  __device__ void run(double& x, int p0, int n) {
+    if (n <= 0) return;
+    if (p0) { add_reps(x, B, 1, cB); n--; }
+    if (n >= 2) add_reps(x, AB, n >> 1, cAB);
+    if (n & 1) add_reps(x, A, 1, cA);
+  }
+};
+
+__device__ __forceinline__ MemProf mem_alt(MemProf A, MemProf B, int p0, int n) {
+  if (n <= 0) return mem_id();
+  MemProf r = mem_id();
+  if (p0) { r = B; n--; }
+  r = mem_then(r, mem_rep(mem_then(A, B), n >> 1));
+  if (n & 1) r = mem_then(r, A);
+  return r;
+}
+
+// -------------------------------------------------- MLP training (C.3) -------
+template <int V>
+__device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
+                        double& ms_out, int64_t& peak_out) {
+  const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
+  const int64_t m = has ? c.B / (D * K) : 0;
+  const int32_t ns = tp.node_size;
+  // Layer shapes by parity of the global layer index: even = column
+  // parallel, odd = row parallel (Megatron pairing); T = 1: both full.
+  const Par<int64_t> kin{d, d / T}, nout{d / T, d}, dout{d / T, d};
+  const bool tp_intra = group_intra(0, T - 1, ns);
+  const bool dp_intra = group_intra(0, T * (D - 1), ns);
+  const int64_t w0 = kin.a * nout.a, w1 = kin.b * nout.b;
+  const Par<int64_t> Wb{w0 * e, w1 * e};
+  const int64_t mde = m * d * e;
+  const double ar_tp = T > 1 ? cost_allreduce(T, mde, tp_intra, tp) : 0.0;
+  const int64_t ar_b = T > 1 ? mde : 0;
+  const int64_t dlast = dout[(L - 1) & 1];
+  const double loss = cost_compute(3 * m * dlast, tp);
+  // forward / backward layer op costs (absent collectives are +0.0)
+  AltSeq<3> fwd;
+  AltSeq<4> bwd;
+  {
+    const double fa[3] = {cost_compute(2 * m * w0, tp), 0.0, cost_compute(m * dout.a, tp)};
+    const double fb[3] = {cost_compute(2 * m * w1, tp), ar_tp, cost_compute(m * dout.b, tp)};
+    fwd.init(fa, fb);
+    const double ba[4] = {fa[2], cost_compute(4 * m * w0, tp), ar_tp, cost_compute(w0, tp)};
+    const double bb[4] = {fb[2], cost_compute(4 * m * w1, tp), 0.0, cost_compute(w1, tp)};
+    bwd.init(ba, bb);
+  }
+  // live-memory profiles of one forward / backward layer (C.7)
+  const MemProf lf_a = mem_then(mem_op(m * nout.a * e, 0), mem_op(m * dout.a * e, m * dout.a * e));
+  const MemProf lf_b = mem_then(mem_then(mem_op(m * nout.b * e, 0), mem_op(ar_b, ar_b)),
+                                mem_op(m * dout.b * e, m * dout.b * e));
+  auto lb = [&](int p, bool first, bool dead0) -> MemProf {
+    const int64_t act_b = m * dout[p] * e, din = m * kin[p] * e;
+    const bool col_ar = p == 0 && T > 1;
+    MemProf r = mem_op(act_b, 2 * act_b);                                  // ReluGrad
+    r = mem_then(r, mem_op(din + Wb[p],
+                           act_b + (first ? din : 0) + ((dead0 && T == 1) ? din : 0)));  // MatMulGrad
+    r = mem_then(r, mem_op(col_ar ? mde : 0, col_ar ? mde + (dead0 ? mde : 0) : 0));   // TP AR
+    return mem_then(r, mem_op(Wb[p], 2 * Wb[p]));                          // Add
+  };
+  const MemProf lb_a = lb(0, false, false), lb_b = lb(1, false, false);
+
+  int s[V], lo[V], hi[V];
+  bool ok[V];
+  double clk[V], sendf[V], sendb[V];
+  int64_t live[V], peak[V];
+  MemProf pf[V], pb[V];
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    s[q] = sl + S * q;
+    ok[q] = has && s[q] < P;
+    lo[q] = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
+    hi[q] = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
+    const int64_t r0 = T * D * (int64_t)s[q];    // rank (0, 0, s)
+    sendf[q] = (ok[q] && s[q] < P - 1)
+                   ? cost_send(m * dout[(hi[q] - 1) & 1] * e, group_intra(r0, r0 + T * D, ns), tp)
+                   : 0.0;
+    sendb[q] = (ok[q] && s[q] > 0)
+                   ? cost_send(m * kin[lo[q] & 1] * e, group_intra(r0 - T * D, r0, ns), tp)
+                   : 0.0;
+    const int nl = hi[q] - lo[q];
+    int64_t lv = (int64_t)((nl + (lo[q] & 1)) >> 1) * 2 * Wb.b +   // odd layers in [lo, hi)
+                 (int64_t)(nl - ((nl + (lo[q] & 1)) >> 1)) * 2 * Wb.a;
+    if (ok[q] && s[q] == 0) lv += K * mde;                       // X_k
+    if (ok[q] && s[q] == P - 1) lv += K * m * dlast * e;         // Y_k
+    live[q] = ok[q] ? lv : 0; peak[q] = live[q]; clk[q] = 0.0;
+    pf[q] = mem_alt(lf_a, lf_b, lo[q] & 1, nl);
+    MemProf b = (ok[q] && s[q] == P - 1) ? mem_op(m * dlast * e, m * dlast * e) : mem_id();
+    if (nl > 1) b = mem_then(b, mem_alt(lb_a, lb_b, (hi[q] - 1) & 1, nl - 1));
+    if (nl > 0) b = mem_then(b, lb(lo[q] & 1, true, s[q] == 0 && lo[q] == 0));
+    pb[q] = b;
+  }
+
+  // ---- forward wavefront: task (k, s) at step 2k + s
+  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  for (int w = 0; w < nsteps; w++) {
+    bool act[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const int kk = w - s[q];
+      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
+      if (act[q]) {
+        fwd.run(clk[q], lo[q] & 1, hi[q] - lo[q]);
+        mem_apply(live[q], peak[q], pf[q]);
+      }
+    }
+    // Send s -> s+1: both ends wait for each other
+    double nb[V], t[V];
+    bool snd[V], rin[V];
+    Nbr<V>::up_stage(clk, nb, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      snd[q] = act[q] && s[q] < P - 1;
+      t[q] = dadd(fmax(clk[q], nb[q]), sendf[q]);
+      if (snd[q]) clk[q] = t[q];
+    }
+    double tin[V];
+    Nbr<V>::down_stage(t, tin, lane);
+    Nbr<V>::down_flag(snd, rin, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (ok[q] && s[q] > 0 && rin[q]) {
+        clk[q] = tin[q];
+        MEM(q, m * kin[lo[q] & 1] * e, 0);                    // received activation
+      }
+    }
+  }
+
+  // ---- backward wavefront: task (k, s) at step 2k + (P-1-s)
+  for (int w = 0; w < nsteps; w++) {
+    bool act[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const int kk = w - (int)(P - 1 - s[q]);
+      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
+      if (act[q]) {
+        if (s[q] == P - 1) clk[q] = dadd(clk[q], loss);       // LossGrad
+        bwd.run(clk[q], (hi[q] - 1) & 1, hi[q] - lo[q]);
+        mem_apply(live[q], peak[q], pb[q]);
+      }
+    }
+    // Send s -> s-1
+    double nb[V], t[V];
+    bool snd[V], rin[V];
+    Nbr<V>::down_stage(clk, nb, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      snd[q] = act[q] && s[q] > 0;
+      t[q] = dadd(fmax(clk[q], nb[q]), sendb[q]);
+      if (snd[q]) {
+        clk[q] = t[q];
+        live[q] -= m * kin[lo[q] & 1] * e;                    // sent gradient dies
+      }
+    }
+    double tin[V];
+    Nbr<V>::up_stage(t, tin, lane);
+    Nbr<V>::up_flag(snd, rin, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (ok[q] && s[q] < P - 1 && rin[q]) {
+        clk[q] = tin[q];
+        MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);             // received gradient
+      }
+    }
+  }
+
+  // ---- tail: DP AllReduce of the accumulated gradients, then SGD (once per
+  // stage: plain op-by-op walk)
+  const Par<double> ardp{D > 1 ? cost_allreduce(D, Wb.a, dp_intra, tp) : 0.0,
+                         D > 1 ? cost_allreduce(D, Wb.b, dp_intra, tp) : 0.0};
+  const Par<double> sgd{cost_compute(2 * w0, tp), cost_compute(2 * w1, tp)};
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (!ok[q]) continue;
+    for (int l = hi[q] - 1; l >= lo[q]; l--) {
+      const int p = l & 1;
+      clk[q] = dadd(clk[q], ardp[p]);
+      MEM(q, D > 1 ? Wb[p] : 0, D > 1 ? Wb[p] : 0);
+    }
+    for (int l = lo[q]; l < hi[q]; l++) {
+      const int p = l & 1;
+      clk[q] = dadd(clk[q], sgd[p]);
+      MEM(q, Wb[p], 2 * Wb[p]);
+    }
+  }
+  double msx = 0.0;
+  int64_t pkx = 0;
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (ok[q]) { msx = fmax(msx, clk[q]); pkx = pkx > peak[q] ? pkx : peak[q]; }
+  }
+  ms_out = msx;
+  peak_out = pkx;
+}
+
+// ------------------------------------------------ GPT-2 inference (C.4) -----
+template <int V>
+__device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
+                         double& ms_out, int64_t& peak_out) {
+  const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
+                ide = c.M.ide, nctx = c.M.nctx;
+  const bool lm = c.M.lm != 0;
+  const int64_t D = c.D, T = c.T, P = c.P, K = c.K;
+  const int64_t m = has ? c.B / (D * K) : 0;
+  const int64_t n = m * Sq, dT = d / T, hT = h / T, VT = Vp / T;
+  const int32_t ns = tp.node_size;
+  const bool tp_intra = group_intra(0, T - 1, ns);
+  const int64_t nde = n * d * e;
+  // op costs (C.4 work per op); absent collectives are +0.0
+  const double c_ar = T > 1 ? cost_allreduce(T, nde, tp_intra, tp) : 0.0;
+  const double c_ln = cost_compute(5 * n * d, tp);
+  const double c_att = cost_compute(2 * m * Sq * Sq * dT, tp);
+  const double c_add = cost_compute(n * d, tp);
+  const double pro[2] = {cost_compute(2 * n * d, tp), c_ar};
+  const double blk[14] = {c_ln,
+                          cost_compute(2 * n * d * (3 * dT) + n * (3 * dT), tp),
+                          c_att,
+                          cost_compute(5 * m * hT * Sq * Sq, tp),
+                          c_att,
+                          cost_compute(2 * n * dT * d + n * d, tp),
+                          c_ar,
+                          c_add,
+                          c_ln,
+                          cost_compute(2 * n * d * (4 * dT) + n * (4 * dT), tp),
+                          cost_compute(8 * n * (4 * dT), tp),
+                          cost_compute(2 * n * (4 * dT) * d + n * d, tp),
+                          c_ar,
+                          c_add};
+  const double epi[3] = {c_ln, lm ? cost_compute(2 * n * d * VT, tp) : 0.0,
+                         (lm && T > 1) ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0};
+  // live-memory profiles (C.7), for a normal and for the last microbatch
+  // (whose ops free the parameters at their last use)
+  const int64_t arb = T > 1 ? nde : 0;
+  const int64_t qkvb = n * 3 * dT * e, scb = m * hT * Sq * Sq * e, ctxb = n * dT * e, fb = n * 4 * dT * e;
+  const int64_t ln_p = 2 * d * e, qkv_p = (d * 3 * dT + 3 * dT) * e, prj_p = (dT * d + d) * e,
+                fc1_p = (d * 4 * dT + 4 * dT) * e, fc2_p = (4 * dT * d + d) * e;
+  const int64_t blk_p = 2 * ln_p + qkv_p + prj_p + fc1_p + fc2_p;
+  const int64_t wte_b = VT * d * e, wpe_b = nctx * d * e;
+  MemProf mblk[2], mpro[2], mepi[2];
+#pragma unroll
+  for (int last = 0; last < 2; last++) {
+    MemProf r = mem_op(nde, last ? ln_p : 0);                       // LayerNorm ln_1
+    r = mem_then(r, mem_op(qkvb, nde + (last ? qkv_p : 0)));         // QKV
+    r = mem_then(r, mem_op(scb, 0));                                 // scores
+    r = mem_then(r, mem_op(scb, scb));                               // softmax
+    r = mem_then(r, mem_op(ctxb, scb + qkvb));                       // context
+    r = mem_then(r, mem_op(nde, ctxb + (last ? prj_p : 0)));         // proj
+    r = mem_then(r, mem_op(arb, arb));                               // TP AllReduce
+    r = mem_then(r, mem_op(nde, 2 * nde));                           // residual
+    r = mem_then(r, mem_op(nde, last ? ln_p : 0));                   // LayerNorm ln_2
+    r = mem_then(r, mem_op(fb, nde + (last ? fc1_p : 0)));           // FC1
+    r = mem_then(r, mem_op(fb, fb));                                 // GeLU
+    r = mem_then(r, mem_op(nde, fb + (last ? fc2_p : 0)));           // FC2
+    r = mem_then(r, mem_op(arb, arb));                               // TP AllReduce
+    mblk[last] = mem_then(r, mem_op(nde, 2 * nde));                  // residual
+    mpro[last] = mem_then(mem_op(nde, n * ide + (last ? wpe_b + ((P == 1 && lm) ? 0 : wte_b) : 0)),
+                          mem_op(arb, arb));                         // Embed, TP AllReduce
+    MemProf ep = mem_op(nde, nde + (last ? 2 * d * e : 0));          // final LayerNorm
+    if (lm) {
+      ep = mem_then(ep, mem_op(n * VT * e, nde + (last ? wte_b : 0)));           // LM head
+      ep = mem_then(ep, mem_op(T > 1 ? n * Vp * e : 0, T > 1 ? n * VT * e : 0));  // AllGather
+    }
+    mepi[last] = ep;
+  }
+
+  int s[V], nb[V];
+  bool ok[V];
+  double clk[V], sendf[V];
+  int64_t live[V], peak[V];
+  MemProf ptask0[V], ptask1[V];   // normal / last microbatch
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    s[q] = sl + S * q;
+    ok[q] = has && s[q] < P;
+    const int lo = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
+    const int hi = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
+    nb[q] = hi - lo;
+    const int64_t r0 = T * D * (int64_t)s[q];
+    sendf[q] = (ok[q] && s[q] < P - 1) ? cost_send(nde, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
+    int64_t lv = (int64_t)nb[q] * blk_p;
+    if (ok[q] && s[q] == 0) lv += wte_b + wpe_b + K * n * ide;
+    if (ok[q] && s[q] == P - 1) lv += 2 * d * e + ((lm && P > 1) ? wte_b : 0);
+    live[q] = ok[q] ? lv : 0; peak[q] = live[q]; clk[q] = 0.0;
+#pragma unroll
+    for (int last = 0; last < 2; last++) {
+      MemProf r = (s[q] == 0) ? mpro[last] : mem_id();
+      r = mem_then(r, mem_rep(mblk[last], nb[q]));
+      if (s[q] == P - 1) r = mem_then(r, mepi[last]);
+      if (last) ptask1[q] = r; else ptask0[q] = r;
+    }
+  }
+  SeqCache cpro = seq_cache_empty(), cblk = seq_cache_empty(), cepi = seq_cache_empty();
+
+  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  for (int w = 0; w < nsteps; w++) {
+    bool act[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const int kk = w - s[q];
+      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
+      if (!act[q]) continue;
+      if (s[q] == 0) add_reps(clk[q], pro, 1, cpro);              // prologue
+      add_reps(clk[q], blk, nb[q], cblk);                         // blocks
+      if (s[q] == P - 1) add_reps(clk[q], epi, 1, cepi);          // epilogue
+      mem_apply(live[q], peak[q], (kk >> 1) == K - 1 ? ptask1[q] : ptask0[q]);
+    }
+    double nbv[V], t[V];
+    bool snd[V], rin[V];
+    Nbr<V>::up_stage(clk, nbv, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      snd[q] = act[q] && s[q] < P - 1;
+      t[q] = dadd(fmax(clk[q], nbv[q]), sendf[q]);
+      if (snd[q]) { clk[q] = t[q]; live[q] -= nde; }          // sent activation dies
+    }
+    double tin[V];
+    Nbr<V>::down_stage(t, tin, lane);
+    Nbr<V>::down_flag(snd, rin, lane);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (ok[q] && s[q] > 0 && rin[q]) { clk[q] = tin[q]; MEM(q, nde, 0); }
+    }
+  }
+  double msx = 0.0;
+  int64_t pkx = 0;
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (ok[q]) { msx = fmax(msx, clk[q]); pkx = pkx > peak[q] ? pkx : peak[q]; }
+  }
+  ms_out = msx;
+  peak_out = pkx;
+}
