@@ -276,10 +276,17 @@ class Simulator:
     # -- synchronous evaluation with host buffers (the e2e path)
     def eval(self, grid=None, configs=None, k=10, per_config=True, pinned=True,
              rank=0, n_ranks=1, comm=None):
+        """Synchronous evaluation through distir_grid_eval_sharded with host
+        buffers (spec H2D and results D2H inside the call).  Per-config
+        outputs are global-indexed numpy copies (only this rank's entries are
+        written when n_ranks > 1)."""
         torch = self.torch
         if grid is not None:
-            sp = self.spec(grid)
-            n = self.grid_size(grid)
+            key = repr(sorted(grid.items()))
+            if getattr(self, "_spec_key", None) != key:
+                self._spec_cache = (self.spec(grid), self.grid_size(grid))
+                self._spec_key = key
+            sp, n = self._spec_cache
             cf, ncf = None, 0
         else:
             sp = None
@@ -288,10 +295,18 @@ class Simulator:
         ws = self.workspace(n)
         outs = {}
         if per_config:
-            outs["makespan"] = torch.full((n,), float("nan"), dtype=torch.float64,
-                                          pin_memory=pinned)
-            outs["peak"] = torch.full((n,), -2, dtype=torch.int64, pin_memory=pinned)
-            outs["reason"] = torch.full((n,), -1, dtype=torch.int32, pin_memory=pinned)
+            bufs = getattr(self, "_host_bufs", None)
+            if bufs is None or bufs[0].numel() < max(n, 1) or bufs[3] != pinned:
+                m = max(n, 1)
+                bufs = (torch.empty(m, dtype=torch.float64, pin_memory=pinned),
+                        torch.empty(m, dtype=torch.int64, pin_memory=pinned),
+                        torch.empty(m, dtype=torch.int32, pin_memory=pinned), pinned)
+                self._host_bufs = bufs
+            outs = {"makespan": bufs[0], "peak": bufs[1], "reason": bufs[2]}
+            if n_ranks > 1:       # entries of other ranks stay untouched: mark them
+                bufs[0][:n].fill_(float("nan"))
+                bufs[1][:n].fill_(-2)
+                bufs[2][:n].fill_(-1)
         topk = np.zeros(max(k, 1), dtype=TOPK_DTYPE)
         ntopk = ctypes.c_int32()
         st = distir_stats()
@@ -305,7 +320,7 @@ class Simulator:
         res = dict(topk=topk[:ntopk.value], n=n,
                    stats={f: getattr(st, f) for f, _ in distir_stats._fields_})
         for name, t in outs.items():
-            res[name] = t.numpy()
+            res[name] = t.numpy()[:n].copy()
         if per_config:
             res["reason"] = res["reason"].view(np.uint32)
         return res

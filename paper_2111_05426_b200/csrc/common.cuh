@@ -16,11 +16,15 @@ constexpr int kMaxWorld = 64;       // world size limit (2 stages per lane)
 constexpr int kMaxK = 64;           // top-k width
 constexpr int kMaxRanks = 8;        // GPUs merged by the all-gather
 constexpr int kNumBuckets = 4096;   // hash slots for warp-shape buckets
-constexpr int kOverflowBucket = kNumBuckets;  // catch-all (1 config / warp)
+constexpr int kOverflowBucket = kNumBuckets;  // catch-alls: + kind (1 config / warp)
+constexpr int kBucketSlots = kNumBuckets + 2;
+constexpr int kGroups = 4;          // simulate kernels: (MLP, GPT-2) x (1, 2 stages/lane)
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
-constexpr int kTopkBlocks = 296;    // partial top-k blocks (2 per SM)
+constexpr int kTopkBlocks = 1024;   // max partial top-k blocks
+constexpr int kTopkThreads = 512;   // threads per partial top-k block
+constexpr int kTopkIPT = 8;         // candidates per thread held in registers
 
 enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };
 
@@ -65,15 +69,14 @@ struct SpecBlock {
 };
 
 struct WsHeader {
-  unsigned long long item_counter;    // persistent-kernel work queue
+  unsigned int item_counter[kGroups]; // persistent-kernel work queues
+  unsigned int group_begin[kGroups + 1];  // item ranges per simulate kernel
   unsigned int n_items;
   unsigned int n_buckets;
   unsigned long long op_events;
   unsigned long long stage_steps;
   unsigned long long n_valid;
   unsigned long long n_feasible;
-  unsigned int class_items[kNumClasses];
-  unsigned int class_base[kNumClasses];
   unsigned int cfg_total;
   unsigned int pad;
 };
@@ -85,8 +88,9 @@ struct Bucket {          // per hash slot (plus one overflow slot)
   uint32_t item_base;    // first work item
   uint32_t cursor;       // scatter cursor
   uint32_t lanes;        // lanes per config S (power of two <= 32)
-  uint32_t cls;          // weight class
-  uint32_t item_off;     // offset within class
+  uint16_t cls;          // weight class
+  uint16_t group;        // simulate kernel: kind * 2 + (two stages per lane)
+  uint32_t item_off;     // offset within (group, class)
 };
 
 struct Item {            // one warp's worth of configs of one bucket

@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -67,7 +68,7 @@ Layout layout(int64_t n_local, int64_t n_explicit) {
   L.hdr = take(sizeof(WsHeader));
   L.spec = take(sizeof(SpecBlock));
   L.ex = take((size_t)(n_explicit > 0 ? n_explicit : 1) * sizeof(DExplicit));
-  L.bk = take((kNumBuckets + 1) * sizeof(Bucket));
+  L.bk = take(kBucketSlots * sizeof(Bucket));
   L.cfg_bucket = take(n * 4);
   L.perm = take(n * 4);
   L.items = take(n * sizeof(Item));
@@ -119,13 +120,34 @@ NcclApi& nccl() {
 }  // namespace
 
 // ------------------------------------------------------------- handle ------
+struct GraphCache {
+  cudaGraph_t graph = nullptr;    // kept alive: its node handles address exec's nodes
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  cudaEvent_t ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // placeholders
+  cudaGraphNode_t evnode[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool ev_ring = false;          // event nodes currently point into the ring
+  int64_t kernels = 0;
+  // key
+  const void* ws = nullptr;
+  double* ms = nullptr;
+  int64_t* pk = nullptr;
+  uint32_t* rs = nullptr;
+  TopkRec* topk = nullptr;
+  int* ntopk = nullptr;
+  int k = -1;
+  void* comm = nullptr;
+  int64_t n_local = -1, n_total = -1;
+  int32_t mode = -1;
+};
+
 struct distir_sim {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::vector<DModel> models;
   std::vector<DTopo> topos;
   int num_sms = 0;
-  int sim_grid = 0;
+  int sim_grid[kGroups] = {0, 0, 0, 0};
   int enum_grid = 0;
   SpecBlock spec{};
   bool uploaded = false;
@@ -137,8 +159,15 @@ struct distir_sim {
   size_t ev_used = 0;            // launches recorded in ev
   distir_profile_data acc{};     // totals folded in from ev
   int64_t kernels = 0, launches = 0;
+  GraphCache graph;
+  bool use_graph = true;
   ~distir_sim() {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    if (graph.graph) cudaGraphDestroy(graph.graph);
+    for (cudaEvent_t e : graph.ph)
+      if (e) cudaEventDestroy(e);
+    if (graph.cap) cudaStreamDestroy(graph.cap);
   }
 };
 
@@ -303,7 +332,7 @@ T* at(void* ws, size_t off) {
 
 __global__ void k_reset(Bucket* bk, WsHeader* hdr) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i <= kNumBuckets) {
+  if (i < kBucketSlots) {
     Bucket b{};
     b.key = kEmptyKey;
     bk[i] = b;
@@ -331,28 +360,22 @@ distir_status prof_fold(distir_sim* sim) {
   return DISTIR_OK;
 }
 
-// Event j of the current launch (recorded only while profiling).
-distir_status prof_mark(distir_sim* sim, int j) {
-  if (!sim->prof) return DISTIR_OK;
-  if (j == 0 && 5 * (sim->ev_used + 1) > sim->ev.size()) {
-    distir_status s = prof_fold(sim);
-    if (s != DISTIR_OK) return s;
-  }
-  CUDA_TRY(cudaEventRecord(sim->ev[5 * sim->ev_used + j], sim->stream));
-  if (j == 4) sim->ev_used++;
-  return DISTIR_OK;
-}
-
-// Launch a1-a7 (+ a8 when nccl_comm != NULL) on the uploaded shard; the
-// (global) top-k goes to (topk, ntopk).
-distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* ms, int64_t* pk,
-                         uint32_t* rs, TopkRec* topk, int* ntopk) {
+// Enqueue a1-a7 (+ a8 when comm != NULL) of the uploaded shard on stream st;
+// the (global) top-k goes to (topk, ntopk).  ev[0..4] (or NULL) are recorded
+// between the phases; with `external` they become event-record nodes of a
+// captured graph.  Returns the number of kernels enqueued in *kernels.
+distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* ev, bool external,
+                          int k, void* comm, void* ws, double* ms, int64_t* pk, uint32_t* rs,
+                          TopkRec* topk, int* ntopk, int64_t* kernels_out) {
   const SpecBlock& sp = sim->spec;
-  distir_status s;
   int64_t kernels = 0;
-  if ((s = prof_mark(sim, 0)) != DISTIR_OK) return s;
+  auto mark = [&](int j) -> cudaError_t {
+    if (!ev) return cudaSuccess;
+    return external ? cudaEventRecordWithFlags(ev[j], st, cudaEventRecordExternal)
+                    : cudaEventRecord(ev[j], st);
+  };
+  CUDA_TRY(mark(0));
   const Layout L = layout(sp.n_local, sp.mode == MODE_EXPLICIT ? sp.n_total : 0);
-  cudaStream_t st = sim->stream;
   ms = ms ? ms : at<double>(ws, L.ms);
   pk = pk ? pk : at<int64_t>(ws, L.pk);
   rs = rs ? rs : at<uint32_t>(ws, L.rs);
@@ -364,7 +387,7 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
   uint32_t* perm = at<uint32_t>(ws, L.perm);
   Item* items = at<Item>(ws, L.items);
   double* tpv = at<double>(ws, L.tp);
-  k_reset<<<(kNumBuckets + 1 + 255) / 256, 256, 0, st>>>(bk, hdr);
+  k_reset<<<(kBucketSlots + 255) / 256, 256, 0, st>>>(bk, hdr);
   kernels++;
   const int64_t n = sp.n_local;
   if (n > 0) {
@@ -374,12 +397,15 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
     k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, perm, items);
     kernels += 3;
   }
-  if ((s = prof_mark(sim, 1)) != DISTIR_OK) return s;
+  CUDA_TRY(mark(1));
   if (n > 0) {
-    k_simulate<<<sim->sim_grid, 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
-    kernels++;
+    k_simulate<0, 1><<<sim->sim_grid[0], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
+    k_simulate<0, 2><<<sim->sim_grid[1], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
+    k_simulate<1, 1><<<sim->sim_grid[2], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
+    k_simulate<1, 2><<<sim->sim_grid[3], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
+    kernels += 4;
   }
-  if ((s = prof_mark(sim, 2)) != DISTIR_OK) return s;
+  CUDA_TRY(mark(2));
   TopkRec* fin = at<TopkRec>(ws, L.fin);
   int* fin_n = at<int>(ws, L.fin_n);
   TopkRec* loc = comm ? fin : topk;   // local list (padded) when merging
@@ -388,15 +414,17 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
     TopkRec* part = at<TopkRec>(ws, L.part);
     int* part_n = at<int>(ws, L.part_n);
     if (n > 0) {
-      k_topk_partial<<<kTopkBlocks, 256, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n);
-      k_topk_merge<<<1, 256, 0, st>>>(part, part_n, kTopkBlocks, k, k, loc, loc_n);
+      const int64_t per = (int64_t)kTopkThreads * kTopkIPT;
+      const int nblk = (int)std::min<int64_t>(kTopkBlocks, (n + per - 1) / per);
+      k_topk_partial<<<nblk, kTopkThreads, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n);
+      k_topk_merge<<<1, kTopkThreads, 0, st>>>(part, part_n, nblk, k, k, loc, loc_n);
       kernels += 2;
     } else {
-      k_topk_merge<<<1, 256, 0, st>>>(part, part_n, 0, k, k, loc, loc_n);
+      k_topk_merge<<<1, kTopkThreads, 0, st>>>(part, part_n, 0, k, k, loc, loc_n);
       kernels++;
     }
   }
-  if ((s = prof_mark(sim, 3)) != DISTIR_OK) return s;
+  CUDA_TRY(mark(3));
   if (k > 0 && comm) {
     NcclApi& api = nccl();
     if (!api.ok) return fail(DISTIR_E_NCCL, api.why);
@@ -406,12 +434,95 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
     if (r != ncclSuccess)
       return fail(DISTIR_E_NCCL, std::string("ncclAllGather: ") +
                                      (api.getErrorString ? api.getErrorString(r) : "error"));
-    k_topk_merge<<<1, 256, 0, st>>>(gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
+    k_topk_merge<<<1, kTopkThreads, 0, st>>>(gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
     kernels++;
   }
-  if ((s = prof_mark(sim, 4)) != DISTIR_OK) return s;
+  CUDA_TRY(mark(4));
   CUDA_TRY(cudaGetLastError());
-  if (sim->prof) { sim->kernels += kernels; sim->launches++; }
+  *kernels_out = kernels;
+  return DISTIR_OK;
+}
+
+// Launch the pipeline on the handle's stream.  The kernel sequence is captured
+// once into a CUDA graph per (workspace, outputs, k, comm, shard size) and
+// replayed (one launch instead of 7-8); the profiling event-record nodes are
+// re-pointed at the next ring entry before each replay.  DISTIR_NO_GRAPH=1
+// launches the kernels directly.
+distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* ms, int64_t* pk,
+                         uint32_t* rs, TopkRec* topk, int* ntopk) {
+  distir_status s;
+  GraphCache& G = sim->graph;
+  const bool key_ok = G.exec && G.ws == ws && G.ms == ms && G.pk == pk && G.rs == rs &&
+                      G.topk == topk && G.ntopk == ntopk && G.k == k && G.comm == comm &&
+                      G.n_local == sim->spec.n_local && G.n_total == sim->spec.n_total &&
+                      G.mode == sim->spec.mode;
+  if (sim->use_graph && !key_ok) {
+    if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
+    if (G.graph) { cudaGraphDestroy(G.graph); G.graph = nullptr; }
+    if (!G.cap) CUDA_TRY(cudaStreamCreateWithFlags(&G.cap, cudaStreamNonBlocking));
+    if (!G.ph[0])
+      for (int j = 0; j < 5; j++) CUDA_TRY(cudaEventCreate(&G.ph[j]));
+    CUDA_TRY(cudaStreamBeginCapture(G.cap, cudaStreamCaptureModeThreadLocal));
+    int64_t kern = 0;
+    s = enqueue_all(sim, G.cap, G.ph, true, k, comm, ws, ms, pk, rs, topk, ntopk, &kern);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(G.cap, &g);
+    if (s != DISTIR_OK) { if (g) cudaGraphDestroy(g); return s; }
+    if (e != cudaSuccess || !g) {
+      // capture unsupported here (e.g. NCCL build): launch directly from now on
+      cudaGetLastError();
+      sim->use_graph = false;
+    } else {
+      e = cudaGraphInstantiate(&G.exec, g, 0);
+      size_t nn = 0;
+      if (e == cudaSuccess) e = cudaGraphGetNodes(g, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (e == cudaSuccess && nn) e = cudaGraphGetNodes(g, nodes.data(), &nn);
+      for (int j = 0; j < 5; j++) G.evnode[j] = nullptr;
+      for (size_t i = 0; e == cudaSuccess && i < nn; i++) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeEventRecord)
+          continue;
+        cudaEvent_t ev;
+        if (cudaGraphEventRecordNodeGetEvent(nodes[i], &ev) != cudaSuccess) continue;
+        for (int j = 0; j < 5; j++)
+          if (ev == G.ph[j]) G.evnode[j] = nodes[i];
+      }
+      G.graph = g;
+      CUDA_TRY(e);
+      G.ws = ws; G.ms = ms; G.pk = pk; G.rs = rs; G.topk = topk; G.ntopk = ntopk; G.k = k;
+      G.comm = comm; G.n_local = sim->spec.n_local; G.n_total = sim->spec.n_total;
+      G.mode = sim->spec.mode; G.kernels = kern; G.ev_ring = false;
+    }
+  }
+  if (sim->use_graph && G.exec) {
+    if (sim->prof) {
+      if (5 * (sim->ev_used + 1) > sim->ev.size() && (s = prof_fold(sim)) != DISTIR_OK) return s;
+      for (int j = 0; j < 5; j++)
+        if (G.evnode[j])
+          CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.exec, G.evnode[j],
+                                                        sim->ev[5 * sim->ev_used + j]));
+      G.ev_ring = true;
+    } else if (G.ev_ring) {
+      for (int j = 0; j < 5; j++)
+        if (G.evnode[j]) CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.exec, G.evnode[j], G.ph[j]));
+      G.ev_ring = false;
+    }
+    CUDA_TRY(cudaGraphLaunch(G.exec, sim->stream));
+    if (sim->prof) { sim->ev_used++; sim->kernels += G.kernels; sim->launches++; }
+    return DISTIR_OK;
+  }
+  // direct launches
+  const cudaEvent_t* ev = nullptr;
+  if (sim->prof) {
+    if (5 * (sim->ev_used + 1) > sim->ev.size() && (s = prof_fold(sim)) != DISTIR_OK) return s;
+    ev = &sim->ev[5 * sim->ev_used];
+  }
+  int64_t kern = 0;
+  if ((s = enqueue_all(sim, sim->stream, ev, false, k, comm, ws, ms, pk, rs, topk, ntopk, &kern)) !=
+      DISTIR_OK)
+    return s;
+  if (sim->prof) { sim->ev_used++; sim->kernels += kern; sim->launches++; }
   return DISTIR_OK;
 }
 
@@ -517,13 +628,18 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   sim->stream = static_cast<cudaStream_t>(cuda_stream);
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sim->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
-  int per_sm = 0;
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate, 128, 0);
+  int per_sm[kGroups] = {0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_simulate<0, 1>, 128, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_simulate<0, 2>, 128, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], k_simulate<1, 1>, 128, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[3], k_simulate<1, 2>, 128, 0);
   if (e != cudaSuccess) {
     delete sim;
     return fail(DISTIR_E_CUDA, std::string("device setup: ") + cudaGetErrorString(e));
   }
-  sim->sim_grid = sim->num_sms * (per_sm > 0 ? per_sm : 1);
+  for (int g = 0; g < kGroups; g++) sim->sim_grid[g] = sim->num_sms * (per_sm[g] > 0 ? per_sm[g] : 1);
+  const char* ng = getenv("DISTIR_NO_GRAPH");
+  sim->use_graph = !(ng && ng[0] == '1');
   sim->enum_grid = sim->num_sms * 8;
   *out = sim;
   return DISTIR_OK;
@@ -711,6 +827,18 @@ distir_status distir_nccl_comm_destroy(void* comm) {
   api.commDestroy(static_cast<ncclComm_t>(comm));
   return DISTIR_OK;
 }
+
+#ifdef DISTIR_INSTR
+// Debug: read and reset the instrumentation counters (not part of distir.h).
+int distir_debug_counters(unsigned long long* out, int n) {
+  unsigned long long h[16];
+  if (cudaMemcpyFromSymbol(h, g_distir_instr, sizeof(h)) != cudaSuccess) return -1;
+  for (int i = 0; i < n && i < 16; i++) out[i] = h[i];
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_distir_instr, z, sizeof(z));
+  return 0;
+}
+#endif
 
 int64_t distir_shard_indices(int64_t n_configs, int32_t rank, int32_t n_ranks, int64_t* out,
                              int64_t cap) {

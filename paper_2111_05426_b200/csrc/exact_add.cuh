@@ -5,25 +5,26 @@
 // same short op sequence (a GPT-2 block, a pair of MLP layers) many times,
 // so a stage's clock is a long serial chain of adds.  This header evaluates
 // that chain EXACTLY -- bit-identical to performing every addition -- in
-// O(1) per repetition run instead of O(ops):
+// O(1) per task instead of O(ops):
 //
 //   Let x > 0 be a normal double in binade E (2^E <= x < 2^(E+1)) and
-//   u = 2^(E-52) its ulp, so x = M*u with M an integer in [2^52, 2^53).
-//   For a >= 0 the exact sum x + a lies on the same binade's grid (spacing u)
-//   as long as x + a < 2^(E+1); then RN(x + a) = (M + RNI(a/u)) * u, where
-//   RNI rounds to the nearest integer -- unambiguous unless a/u is exactly
-//   half an odd integer (a tie, broken by the parity of the running total).
-//   Hence, for an op sequence a_1..a_N with no tie at binade E and
-//   r_j = RNI(a_j/u), applying it n times from x yields exactly
-//   (M + n*sum_j r_j) * u provided M + n*sum_j r_j <= 2^53 - 1 (every
-//   intermediate exact sum then stays below 2^(E+1)).  Otherwise one
-//   repetition is performed op by op (it crosses into the next binade, or
-//   contains a tie), the cache is recomputed for the new binade, and the
-//   remaining repetitions continue.  a/u is exact (power-of-two scaling);
-//   all integer-valued doubles involved stay below 2^53.
+//   u = 2^(E-52) its ulp, so x = M*u with M its 53-bit significand
+//   (2^52 <= M < 2^53).  For a >= 0 the exact sum x + a lies on the same
+//   binade's grid (spacing u) as long as x + a < 2^(E+1); then
+//   RN(x + a) = (M + i)*u where i rounds a/u to the nearest integer -- and
+//   when a/u is exactly m + 1/2 (a tie), to the i in {m, m+1} that makes
+//   M + i even.  So one pass of a sequence a_1..a_N adds an integer number of
+//   ulps that depends only on the binade and on the parity of M (R0 / R1),
+//   and n passes add a closed-form total S (the parity sequence has period
+//   <= 2), provided M + S <= 2^53 - 1: every intermediate exact sum then stays
+//   below 2^(E+1).  That condition is checked by computing y = x + S*u: the
+//   exact value (M + S)*u is representable iff M + S < 2^53, so y keeps x's
+//   exponent exactly when the aggregation is valid (and is then exact).
+//   Passes that would cross into the next binade are performed op by op; the
+//   cache is then recomputed for the new binade.
 //
-// The kernels only ever call add_reps; the fallback path is the plain
-// sequence of __dadd_rn, so the aggregation can never change a result.
+// The fallback path is the plain sequence of __dadd_rn, so aggregation can
+// never change a result (host check: tests/native/exact_add_check.cpp).
 #pragma once
 #include <cstdint>
 
@@ -35,18 +36,18 @@
 #endif
 #endif
 
+#ifndef DISTIR_COUNT
+#define DISTIR_COUNT(i)
+#endif
+
 namespace distir {
 
 #ifdef __CUDA_ARCH__
 DISTIR_HD double xadd(double a, double b) { return __dadd_rn(a, b); }
-DISTIR_HD double xmul(double a, double b) { return __dmul_rn(a, b); }
 DISTIR_HD int64_t d2bits(double x) { return __double_as_longlong(x); }
 DISTIR_HD double bits2d(int64_t b) { return __longlong_as_double(b); }
-DISTIR_HD double xfloor(double x) { return floor(x); }
-DISTIR_HD double xrint(double x) { return rint(x); }
 #else
 DISTIR_HD double xadd(double a, double b) { return a + b; }
-DISTIR_HD double xmul(double a, double b) { return a * b; }
 DISTIR_HD int64_t d2bits(double x) {
   int64_t b;
   __builtin_memcpy(&b, &x, 8);
@@ -57,80 +58,190 @@ DISTIR_HD double bits2d(int64_t b) {
   __builtin_memcpy(&x, &b, 8);
   return x;
 }
+#endif
+
+constexpr int64_t kMant = (int64_t(1) << 52) - 1;
+constexpr int64_t kHidden = int64_t(1) << 52;
+constexpr int64_t kTwo53 = int64_t(1) << 53;
+constexpr double kTwo53d = 9007199254740992.0;
+constexpr double kNever = 1.152921504606846976e18;   // 2^60: never fits a binade
+
+#ifdef __CUDA_ARCH__
+DISTIR_HD double xmul(double a, double b) { return __dmul_rn(a, b); }
+DISTIR_HD double xfloor(double x) { return floor(x); }
+DISTIR_HD double xrint(double x) { return rint(x); }
+#else
+DISTIR_HD double xmul(double a, double b) { return a * b; }
 DISTIR_HD double xfloor(double x) { return __builtin_floor(x); }
 DISTIR_HD double xrint(double x) { return __builtin_rint(x); }
 #endif
 
-constexpr double kTwo53m1 = 9007199254740991.0;  // 2^53 - 1
-
-// Per-sequence cache: binade exponent field, sum of per-op ulp increments,
-// and whether any op is a tie at that binade.
-struct SeqCache {
-  int32_t ef;      // biased exponent field of the cached binade (-1 = none)
-  bool tie;
-  double R;        // sum_j RNI(a_j / u), an integer < 2^53 (or >= 2^53: never fits)
-};
-
-DISTIR_HD SeqCache seq_cache_empty() { return SeqCache{-1, false, 0.0}; }
-
-// x's biased exponent field; usable binades need 53 <= ef <= 2046 - 53 so
-// that u and 1/u are normal powers of two.
+// x's biased exponent field.
 DISTIR_HD int32_t exp_field(double x) { return (int32_t)((d2bits(x) >> 52) & 0x7FF); }
 
-template <int N>
-DISTIR_HD void seq_plain(double& x, const double (&a)[N]) {
-#pragma unroll
-  for (int j = 0; j < N; j++) x = xadd(x, a[j]);
+DISTIR_HD int odd(double integral) { return (int)((int64_t)integral & 1); }
+
+DISTIR_HD void seq_plain(double& x, const double* a, int n) {
+  for (int j = 0; j < n; j++) x = xadd(x, a[j]);
 }
 
-template <int N>
-DISTIR_HD void seq_refresh(SeqCache& c, int32_t ef, const double (&a)[N]) {
-  // 1/u = 2^(52 - E) = 2^(1075 - ef); its biased field = 1075 - ef + 1023.
-  const double inv_u = bits2d((int64_t)(2098 - ef) << 52);
+// Ulps added by one pass of a[0..n) at binade field ef, from an even (R0) and
+// an odd (R1) significand.  Returns false when the pass can never fit the
+// binade (an op of at least 2^52 ulps).  Exact: a*2^k is exact, floor/rint of
+// such a double are exact, and sums of integers below 2^53 are exact.
+DISTIR_HD bool seg_pass(const double* a, int n, int32_t ef, double& R0, double& R1) {
+  const double inv_u = bits2d((int64_t)(2098 - ef) << 52);    // 2^(52-E)
   double R = 0.0;
-  bool tie = false;
-#pragma unroll
-  for (int j = 0; j < N; j++) {
-    const double q = xmul(a[j], inv_u);          // exact: power-of-two scale
-    const double fl = xfloor(q);
-    tie |= (xadd(q, -fl) == 0.5);
-    R = xadd(R, xrint(q));                       // exact while R < 2^53
+  bool tie = false, never = false;
+  for (int j = 0; j < n; j++) {
+    const double q = xmul(a[j], inv_u);
+    never |= !(q < kTwo53d);
+    tie |= (xadd(q, -xfloor(q)) == 0.5);
+    R = xadd(R, xrint(q));
   }
-  c.ef = ef;
-  c.tie = tie;
-  c.R = R;
+  if (never) return false;
+  R0 = R1 = R;
+  if (tie) {                      // resolve ties by the running parity
+    R0 = R1 = 0.0;
+    int p0 = 0, p1 = 1;
+    for (int j = 0; j < n; j++) {
+      const double q = xmul(a[j], inv_u);
+      const double fl = xfloor(q);
+      const double fr = xadd(q, -fl);
+      double i0 = fr > 0.5 ? xadd(fl, 1.0) : fl, i1 = i0;
+      if (fr == 0.5) {
+        const int of = odd(fl);
+        i0 = (p0 ^ of) ? xadd(fl, 1.0) : fl;
+        i1 = (p1 ^ of) ? xadd(fl, 1.0) : fl;
+      }
+      p0 ^= odd(i0);
+      p1 ^= odd(i1);
+      R0 = xadd(R0, i0);
+      R1 = xadd(R1, i1);
+    }
+  }
+  return R0 < kTwo53d && R1 < kTwo53d;
 }
 
-// x <- N*reps successive RN additions of a[0..N), computed exactly.
-template <int N>
-DISTIR_HD void add_reps(double& x, const double (&a)[N], int64_t reps, SeqCache& c) {
-  while (reps > 0) {
-    const int32_t ef = exp_field(x);
-    if (x <= 0.0 || ef < 53 || ef > 1993) {      // zero / tiny / huge: plain
-      seq_plain(x, a);
-      reps--;
-      continue;
+// Total ulps of n passes from significand parity p (the parity sequence has
+// period <= 2); kNever when it cannot fit a binade.
+DISTIR_HD double reps_total(double R0, double R1, int p, int64_t n) {
+  const double Ra = p ? R1 : R0, Rb = p ? R0 : R1;
+  if (n == 1) return Ra;
+  const double dn = (double)n;
+  double s;
+  if (!odd(Ra)) s = xmul(dn, Ra);                              // parity stays
+  else if (!odd(Rb)) s = xadd(Ra, xmul(dn - 1.0, Rb));         // flips once
+  else {                                                        // alternates
+    const double h = (double)(n >> 1);
+    s = xadd(xmul(dn - h, Ra), xmul(h, Rb));
+  }
+  return s < kTwo53d ? s : kNever;                              // monotone rounding
+}
+
+// A task is a list of segments: `reps` passes over the op costs a[0..n).
+struct Seg {
+  const double* a;
+  int n;
+  int64_t reps;
+};
+
+// Per-task cache for one binade: the x increment of the whole task from an
+// even / odd significand (-1: the task never fits this binade), and each
+// segment's per-pass ulp increments (R[2i], R[2i+1]; kNever if a pass never
+// fits) in caller-provided storage (shared memory).
+struct TaskCache {
+  int32_t ef;
+  double Su0, Su1;
+  double* R;
+};
+
+DISTIR_HD TaskCache task_cache_make(double* store) { return TaskCache{-1, -1.0, -1.0, store}; }
+
+template <int NS>
+DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
+  DISTIR_COUNT(2);
+  double T[2] = {0.0, 0.0};
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    double R0 = kNever, R1 = kNever;
+    if (sg[i].reps > 0 && !seg_pass(sg[i].a, sg[i].n, ef, R0, R1)) { R0 = R1 = kNever; ok = false; }
+    c.R[2 * i] = R0;
+    c.R[2 * i + 1] = R1;
+    if (sg[i].reps <= 0 || !ok) continue;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+      const int pe = p ^ odd(T[p]);                 // parity entering segment i
+      const double s = reps_total(R0, R1, pe, sg[i].reps);
+      T[p] = s < kNever ? xadd(T[p], s) : kNever;
     }
-    if (ef != c.ef) seq_refresh(c, ef, a);
-    if (!c.tie) {
-      const double inv_u = bits2d((int64_t)(2098 - ef) << 52);
-      const double u = bits2d((int64_t)(ef - 52) << 52);
-      const double M = xmul(x, inv_u);           // integer in [2^52, 2^53)
-      const double avail = xadd(kTwo53m1, -M);   // exact
-      int64_t fit = reps;
-      if (c.R > 0.0) {
-        const double f = xfloor(avail / c.R);
-        if (f < (double)reps) fit = (int64_t)f;
-        while (fit > 0 && xmul((double)fit, c.R) > avail) fit--;
-      }
-      if (fit > 0) {
-        x = xadd(x, xmul(xmul((double)fit, c.R), u));   // exact: lands on the grid
-        reps -= fit;
+  }
+  const double u = bits2d((int64_t)(ef - 52) << 52);
+  c.ef = ef;
+  c.Su0 = (ok && T[0] < kTwo53d) ? xmul(T[0], u) : -1.0;     // exact
+  c.Su1 = (ok && T[1] < kTwo53d) ? xmul(T[1], u) : -1.0;
+}
+
+// x <- every addition of the task, in order, computed exactly.  Fast path:
+// one add when the whole task stays inside x's binade.  Otherwise each
+// segment advances by whole passes while they fit (closed form, or a short
+// parity walk when the binade has ties), the pass that leaves the binade is
+// done op by op, and the cache moves to the new binade.
+template <int NS>
+DISTIR_HD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
+  DISTIR_COUNT(0);
+  {
+    const int64_t xb = d2bits(x);
+    const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+    if (x > 0.0 && ef >= 53 && ef <= 1993) {
+      if (ef != c.ef) task_refresh(c, ef, sg);
+      const double Su = (xb & 1) ? c.Su1 : c.Su0;
+      if (Su >= 0.0) {
+        const double y = xadd(x, Su);
+        if (exp_field(y) == ef) { x = y; DISTIR_COUNT(1); return; }
       }
     }
-    if (reps > 0) {                              // crossing (or tie): op by op
-      seq_plain(x, a);
-      reps--;
+  }
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    int64_t reps = sg[i].reps;
+    while (reps > 0) {
+      const int64_t xb = d2bits(x);
+      const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+      if (x > 0.0 && ef >= 53 && ef <= 1993) {
+        if (ef != c.ef) task_refresh(c, ef, sg);
+        const double R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
+        if (R0 < kNever) {
+          int64_t M = (xb & kMant) | kHidden;
+          const int64_t r0 = (int64_t)R0, r1 = (int64_t)R1;
+          const int64_t before = reps;
+          if (r0 == r1) {                            // no tie: closed form
+            const int64_t avail = kTwo53 - 1 - M;
+            int64_t fit = r0 > 0 ? (int64_t)((double)avail / (double)r0) : reps;
+            if (fit > reps) fit = reps;
+            while (fit > 0 && fit * r0 > avail) fit--;
+            while (fit < reps && (fit + 1) * r0 <= avail) fit++;
+            M += fit * r0;
+            reps -= fit;
+          } else {                                   // ties: walk the parity
+            int p = (int)(M & 1);
+            while (reps > 0) {
+              const int64_t r = p ? r1 : r0;
+              if (M + r > kTwo53 - 1) break;
+              M += r;
+              p ^= (int)(r & 1);
+              reps--;
+            }
+          }
+          if (reps != before) x = bits2d(((int64_t)ef << 52) | (M & kMant));   // exact
+        }
+      }
+      if (reps > 0) {                                // the crossing pass
+        DISTIR_COUNT(3);
+        seq_plain(x, sg[i].a, sg[i].n);
+        reps--;
+      }
     }
   }
 }

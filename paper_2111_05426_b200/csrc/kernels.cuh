@@ -24,8 +24,18 @@
 // for the synchronising ops.  Absent collectives (T = 1, D = 1) are identity
 // steps: cost +0.0 and zero bytes, which leave clocks and memory unchanged.
 #pragma once
+#include <nv/target>
 #include <cfloat>
 #include <climits>
+#ifdef DISTIR_INSTR
+// Debug instrumentation (tools/probe_instr.py): warp-aggregated event counts.
+__device__ unsigned long long g_distir_instr[16];
+__device__ __forceinline__ void distir_count(int i) {
+  const unsigned m_ = __activemask();
+  if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));
+}
+#define DISTIR_COUNT(i) NV_IF_TARGET(NV_IS_DEVICE, (distir_count(i);))
+#endif
 #include "common.cuh"
 #include "exact_add.cuh"
 
@@ -195,29 +205,6 @@ struct Nbr {
       out[1] = lane > 0 ? e1 : y;
     }
   }
-  // flags of stage s-1 / s+1
-  __device__ static void down_flag(const bool (&f)[V], bool (&out)[V], int lane) {
-    const bool e0 = __shfl_up_sync(0xffffffffu, (int)f[0], 1);
-    if constexpr (V == 1) {
-      out[0] = e0;
-    } else {
-      const bool e1 = __shfl_up_sync(0xffffffffu, (int)f[1], 1);
-      const bool y = __shfl_sync(0xffffffffu, (int)f[0], 31);
-      out[0] = e0;
-      out[1] = lane > 0 ? e1 : y;
-    }
-  }
-  __device__ static void up_flag(const bool (&f)[V], bool (&out)[V], int lane) {
-    const bool d0 = __shfl_down_sync(0xffffffffu, (int)f[0], 1);
-    if constexpr (V == 1) {
-      out[0] = d0;
-    } else {
-      const bool d1 = __shfl_down_sync(0xffffffffu, (int)f[1], 1);
-      const bool w1 = __shfl_sync(0xffffffffu, (int)f[1], 0);
-      out[0] = lane < 31 ? d0 : w1;
-      out[1] = d1;
-    }
-  }
 };
 
 __device__ __forceinline__ int warp_max_int(int v) { return __reduce_max_sync(0xffffffffu, v); }
@@ -261,7 +248,7 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
     ev += events; st += steps; nv += 1;
     const uint32_t key = bucket_key(c);
     uint32_t slot = (key * 2654435761u) >> 20;                 // 12-bit hash
-    uint32_t found = kOverflowBucket;
+    uint32_t found = kOverflowBucket + (uint32_t)c.M.kind;
     for (int probe = 0; probe < kNumBuckets; probe++) {
       const uint32_t sl = (slot + probe) & (kNumBuckets - 1);
       uint32_t cur = *(volatile uint32_t*)&bk[sl].key;
@@ -290,22 +277,25 @@ __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
   return p;
 }
 
-// One block: lanes per config, work items, LPT order of buckets by weight
-// class (heaviest first), config ranges.
+// One block: lanes per config, simulate kernel (group), work items numbered
+// group-major and heaviest weight class first within a group (LPT order for
+// the persistent simulate kernels), config ranges.
 __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
-  __shared__ unsigned int s_items[kNumClasses];
-  __shared__ unsigned int s_base[kNumClasses];
+  __shared__ unsigned int s_items[kGroups][kNumClasses];
+  __shared__ unsigned int s_base[kGroups][kNumClasses];
   __shared__ unsigned int s_cfg, s_nb;
-  for (int c = threadIdx.x; c < kNumClasses; c += blockDim.x) s_items[c] = 0;
+  for (int c = threadIdx.x; c < kGroups * kNumClasses; c += blockDim.x)
+    s_items[c / kNumClasses][c % kNumClasses] = 0;
   if (threadIdx.x == 0) { s_cfg = 0; s_nb = 0; }
   __syncthreads();
-  for (int b = threadIdx.x; b <= kNumBuckets; b += blockDim.x) {
+  for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
     Bucket& B = bk[b];
     if (B.count == 0) continue;
-    uint32_t lanes, cls;
-    if (b == kOverflowBucket) {
+    uint32_t lanes, cls, group;
+    if (b >= kOverflowBucket) {        // mixed shapes: one config per warp
       lanes = 32;
       cls = kNumClasses - 1;
+      group = (uint32_t)(b - kOverflowBucket) * 2 + 1;
     } else {
       const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, L = ((B.key >> 7) & 1023) + 1,
                      K = (B.key >> 17) & 255;
@@ -314,12 +304,14 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
       unsigned long long est = (2ull * K + P) * per * (kind ? 14ull : 8ull) + 1;
       cls = 63 - __clzll(est);
       if (cls >= kNumClasses) cls = kNumClasses - 1;
+      group = kind * 2 + (P > 32 ? 1 : 0);
     }
     const uint32_t cpw = 32 / lanes;
     const uint32_t items = (B.count + cpw - 1) / cpw;
     B.lanes = lanes;
-    B.cls = cls;
-    B.item_off = atomicAdd(&s_items[cls], items);
+    B.cls = (uint16_t)cls;
+    B.group = (uint16_t)group;
+    B.item_off = atomicAdd(&s_items[group][cls], items);
     B.cfg_base = atomicAdd(&s_cfg, B.count);
     B.cursor = 0;
     atomicAdd(&s_nb, 1u);
@@ -327,17 +319,21 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int base = 0;
-    for (int c = kNumClasses - 1; c >= 0; c--) { s_base[c] = base; base += s_items[c]; }
+    for (int g = 0; g < kGroups; g++) {
+      hdr->group_begin[g] = base;
+      hdr->item_counter[g] = 0;
+      for (int c = kNumClasses - 1; c >= 0; c--) { s_base[g][c] = base; base += s_items[g][c]; }
+    }
+    hdr->group_begin[kGroups] = base;
     hdr->n_items = base;
     hdr->n_buckets = s_nb;
     hdr->cfg_total = s_cfg;
-    hdr->item_counter = 0;
   }
   __syncthreads();
-  for (int b = threadIdx.x; b <= kNumBuckets; b += blockDim.x) {
+  for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
     Bucket& B = bk[b];
     if (B.count == 0) continue;
-    B.item_base = s_base[B.cls] + B.item_off;
+    B.item_base = s_base[B.group][B.cls] + B.item_off;
   }
 }
 
@@ -364,7 +360,9 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
   }
 }
 
-// Persistent: each warp pulls work items (heaviest classes first).
+// Persistent simulate kernel for one group (model kind x stages per lane):
+// each warp pulls work items of its group, heaviest weight class first.
+template <int KIND, int V>
 __global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ spp,
                                                   const DExplicit* __restrict__ ex,
                                                   const Bucket* __restrict__ bk,
@@ -375,15 +373,20 @@ __global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ 
                                                   int64_t* __restrict__ pk_out,
                                                   uint32_t* __restrict__ rs_out,
                                                   double* __restrict__ tp_out) {
+  constexpr int G = KIND * 2 + (V == 2 ? 1 : 0);
   const SpecBlock& sp = *spp;
   const int lane = threadIdx.x & 31;
-  const unsigned int n_items = *(volatile unsigned int*)&hdr->n_items;
+  const unsigned int first = hdr->group_begin[G], end = hdr->group_begin[G + 1];
+  // per-lane rows: op costs, then per-slot task-cache increments
+  constexpr int ROW = KIND == 1 ? 19 + 6 * V : 15 + 14 * V;
+  __shared__ double s_row[128][ROW];
+  double* row = s_row[threadIdx.x];
   unsigned long long feas = 0;
   while (true) {
     unsigned int id = 0;
-    if (lane == 0) id = (unsigned int)atomicAdd(&hdr->item_counter, 1ull);
+    if (lane == 0) id = first + atomicAdd(&hdr->item_counter[G], 1u);
     id = __shfl_sync(0xffffffffu, id, 0);
-    if (id >= n_items) break;
+    if (id >= end) break;
     const Item it = items[id];
     const Bucket& B = bk[it.bucket];
     const int S = (int)B.lanes;
@@ -394,21 +397,25 @@ __global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ 
     if (has) {
       decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);
     } else {
-      c.M = DModel{0, 1, 1, 1, 1, 1, 1, 1, 1, 0};
+      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0};
       c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
     }
     const DTopo& tp = sp.topos[c.topo];
-    const bool wide = __any_sync(0xffffffffu, has && c.P > 32);
-    const bool gpt = __any_sync(0xffffffffu, has && c.M.kind == 1);
     double ms;
     int64_t pk;
-    if (gpt) {
-      if (wide) run_gpt2<2>(c, tp, has, sl, S, lane, ms, pk);
-      else run_gpt2<1>(c, tp, has, sl, S, lane, ms, pk);
-    } else {
-      if (wide) run_mlp<2>(c, tp, has, sl, S, lane, ms, pk);
-      else run_mlp<1>(c, tp, has, sl, S, lane, ms, pk);
+#ifdef DISTIR_INSTR
+    const long long t0 = clock64();
+#endif
+    if constexpr (KIND == 1) run_gpt2<V>(c, tp, has, sl, S, lane, row, ms, pk);
+    else run_mlp<V>(c, tp, has, sl, S, lane, row, ms, pk);
+#ifdef DISTIR_INSTR
+    if (lane == 0) {
+      const unsigned long long dt = (unsigned long long)(clock64() - t0);
+      atomicAdd(&g_distir_instr[5], dt);
+      atomicAdd(&g_distir_instr[7], 1ull);
+      atomicMax(&g_distir_instr[8], dt);
     }
+#endif
     // makespan and peak: max over the stages of the segment
     for (int o = S >> 1; o > 0; o >>= 1) {
       ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
@@ -452,28 +459,99 @@ __device__ __forceinline__ Key shfl_key(const Key& k, int o) {
   return r;
 }
 
-// Block-wide argmax under `better` (blockDim.x == 256).
+// Block-wide best under `better` (blockDim.x a multiple of 32, <= 1024).
+// No trailing barrier: the next call rewrites s_k only after every thread
+// has passed this call's second barrier.
 __device__ Key block_best(Key k) {
-  __shared__ Key s_k[8];
+  __shared__ Key s_k[32];
+  __shared__ Key s_b;
   for (int o = 16; o > 0; o >>= 1) {
     const Key x = shfl_key(k, o);
     if (better(x, k)) k = x;
   }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) s_k[w] = k;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_k[w] = k;
   __syncthreads();
-  Key b = s_k[0];
-  for (int i = 1; i < 8; i++)
-    if (better(s_k[i], b)) b = s_k[i];
+  if (w == 0) {
+    Key x = lane < (int)(blockDim.x >> 5) ? s_k[lane] : worst_key();
+    for (int o = 16; o > 0; o >>= 1) {
+      const Key y = shfl_key(x, o);
+      if (better(y, x)) x = y;
+    }
+    if (lane == 0) s_b = x;
+  }
   __syncthreads();
-  return b;
+  return s_b;
+}
+
+__device__ __forceinline__ Key best_sentinel() {
+  return Key{__longlong_as_double(0x7FF0000000000000ll), LLONG_MIN, LLONG_MIN, 0.0};
+}
+
+__device__ __forceinline__ Key warp_best(Key k) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key x = shfl_key(k, o);
+    if (better(x, k)) k = x;
+  }
+  return k;
 }
 
 // Select the k best of a candidate set, one round per rank: round r keeps the
 // best candidate strictly worse than round r-1's winner (keys are unique).
+// Register path (n <= IPT*blockDim): every warp first selects the top k of
+// its own lanes' candidates with warp shuffles only (no block barriers),
+// then warp 0 merges the per-warp lists from shared memory.
+template <int IPT, typename Fetch>
+__device__ int select_topk_reg(int64_t n, int k, Fetch fetch, TopkRec* out) {
+  __shared__ Key s_cand[kTopkThreads / 32][kMaxK];
+  __shared__ int s_cnt[kTopkThreads / 32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  Key it[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; i++) {
+    const int64_t j = threadIdx.x + (int64_t)i * blockDim.x;
+    if (!(j < n && fetch(j, it[i]))) it[i] = worst_key();
+  }
+  Key prev = best_sentinel();
+  int got = 0;
+  for (int r = 0; r < k; r++) {
+    Key best = worst_key();
+#pragma unroll
+    for (int i = 0; i < IPT; i++)
+      if (better(prev, it[i]) && better(it[i], best)) best = it[i];
+    best = warp_best(best);
+    if (best.idx == LLONG_MAX) break;
+    if (lane == 0) s_cand[w][r] = best;
+    prev = best;
+    got++;
+  }
+  if (lane == 0) s_cnt[w] = got;
+  __syncthreads();
+  got = 0;
+  if (w == 0) {
+    prev = best_sentinel();
+    for (int r = 0; r < k; r++) {
+      Key best = worst_key();
+      for (int j = lane; j < nw * k; j += 32) {
+        const int ww = j / k, rr = j - ww * k;
+        if (rr >= s_cnt[ww]) continue;
+        const Key c = s_cand[ww][rr];
+        if (better(prev, c) && better(c, best)) best = c;
+      }
+      best = warp_best(best);
+      if (best.idx == LLONG_MAX) break;
+      if (lane == 0) out[r] = TopkRec{best.idx, best.ms, best.tp, best.peak};
+      prev = best;
+      got++;
+    }
+  }
+  return got;    // valid in warp 0
+}
+
+// General path: candidates re-read every round.
 template <typename Fetch>
-__device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
-  Key prev{__longlong_as_double(0x7FF0000000000000ll), LLONG_MIN, LLONG_MIN, 0.0};
+__device__ int select_topk_scan(int64_t n, int k, Fetch fetch, TopkRec* out) {
+  Key prev = best_sentinel();
   int got = 0;
   for (int r = 0; r < k; r++) {
     Key best = worst_key();
@@ -491,13 +569,17 @@ __device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
   return got;
 }
 
-__global__ void __launch_bounds__(256) k_topk_partial(const SpecBlock* __restrict__ spp,
-                                                      const double* __restrict__ ms,
-                                                      const int64_t* __restrict__ pk,
-                                                      const uint32_t* __restrict__ rs,
-                                                      const double* __restrict__ tpv, int k,
-                                                      TopkRec* __restrict__ part,
-                                                      int* __restrict__ part_n) {
+template <typename Fetch>
+__device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
+  if (n <= (int64_t)kTopkIPT * blockDim.x) return select_topk_reg<kTopkIPT>(n, k, fetch, out);
+  return select_topk_scan(n, k, fetch, out);
+}
+
+// One block per contiguous slice of the shard.
+__global__ void __launch_bounds__(kTopkThreads) k_topk_partial(
+    const SpecBlock* __restrict__ spp, const double* __restrict__ ms,
+    const int64_t* __restrict__ pk, const uint32_t* __restrict__ rs,
+    const double* __restrict__ tpv, int k, TopkRec* __restrict__ part, int* __restrict__ part_n) {
   const SpecBlock& sp = *spp;
   const int64_t n = sp.n_local;
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
@@ -514,16 +596,17 @@ __global__ void __launch_bounds__(256) k_topk_partial(const SpecBlock* __restric
   if (threadIdx.x == 0) part_n[blockIdx.x] = got;
 }
 
-// Merge n_lists lists of up to k records (counts in list_n, or all k valid
-// when list_n == NULL and index >= 0 marks a valid record).
-__global__ void __launch_bounds__(256) k_topk_merge(const TopkRec* __restrict__ lists,
-                                                    const int* __restrict__ list_n, int n_lists,
-                                                    int k_in, int k, TopkRec* __restrict__ out,
-                                                    int* __restrict__ out_n) {
+// Merge n_lists lists of up to k_in records (counts in list_n, or, when
+// list_n == NULL, index >= 0 marks a valid record); pads `out` to k.
+__global__ void __launch_bounds__(kTopkThreads) k_topk_merge(const TopkRec* __restrict__ lists,
+                                                     const int* __restrict__ list_n, int n_lists,
+                                                     int k_in, int k, TopkRec* __restrict__ out,
+                                                     int* __restrict__ out_n) {
   auto fetch = [&](int64_t j, Key& c) -> bool {
-    const int l = (int)(j / k_in), r = (int)(j - (int64_t)l * k_in);
-    if (list_n ? r >= list_n[l] : lists[j].index < 0) return false;
-    const TopkRec x = lists[j];
+    const int jj = (int)j;
+    const int l = jj / k_in, r = jj - l * k_in;
+    if (list_n ? r >= list_n[l] : lists[jj].index < 0) return false;
+    const TopkRec x = lists[jj];
     c = Key{x.throughput, x.peak, x.index, x.makespan};
     return true;
   };

@@ -4,29 +4,13 @@
 //
 // Per lane = one pipeline stage (two when 32 < P <= 64).  A *task* is the
 // stage's ops for one microbatch (SURVEY C.3 / C.4 emission order); its clock
-// advance is applied with add_reps (exact_add.cuh: bit-identical to one IEEE
-// add per op) and its live-memory effect with a precomputed MemProf (exact
-// integer composition of the per-op alloc/peak/free steps of C.7).  Sends
-// between stages are exact max + one add, exchanged with warp shuffles.
-
-// Alternating-parity layer runs: n layers starting at parity p0, layer
-// sequences A (even / column-parallel) and B (odd / row-parallel).
-template <int N>
-struct AltSeq {
-  double A[N], B[N], AB[2 * N];
-  SeqCache cA, cB, cAB;
-  __device__ void init(const double (&a)[N], const double (&b)[N]) {
-#pragma unroll
-    for (int j = 0; j < N; j++) { A[j] = a[j]; B[j] = b[j]; AB[j] = a[j]; AB[N + j] = b[j]; }
-    cA = cB = cAB = seq_cache_empty();
-  }
-  __device__ void run(double& x, int p0, int n) {
-    if (n <= 0) return;
-    if (p0) { add_reps(x, B, 1, cB); n--; }
-    if (n >= 2) add_reps(x, AB, n >> 1, cAB);
-    if (n & 1) add_reps(x, A, 1, cA);
-  }
-};
+// advance is applied with add_task (exact_add.cuh: bit-identical to one IEEE
+// add per op, one add per task in the common case) and its live-memory
+// effect with a precomputed MemProf (exact integer composition of the per-op
+// alloc/peak/free steps of C.7).  Sends between stages are exact max + one
+// add, exchanged with warp shuffles.  Op costs live in a per-lane row of
+// shared memory (`row`), read only when a task's binade cache is refreshed
+// or a task crosses a binade.
 
 __device__ __forceinline__ MemProf mem_alt(MemProf A, MemProf B, int p0, int n) {
   if (n <= 0) return mem_id();
@@ -38,9 +22,20 @@ __device__ __forceinline__ MemProf mem_alt(MemProf A, MemProf B, int p0, int n) 
 }
 
 // -------------------------------------------------- MLP training (C.3) -------
+// Alternating-parity layer runs as task segments: n layers starting at
+// parity p0 over per-parity op sequences A (offset oa) and B = A + na (the
+// pair AB is contiguous in the row).
+__device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, int n, Seg& b, Seg& ab,
+                                         Seg& a) {
+  const int n1 = n - (p0 && n > 0);
+  b = Seg{row + oa + na, na, (p0 && n > 0) ? 1 : 0};
+  ab = Seg{row + oa, 2 * na, n1 >> 1};
+  a = Seg{row + oa, na, n1 & 1};
+}
+
 template <int V>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                        double& ms_out, int64_t& peak_out) {
+                        double* row, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
   const int64_t m = has ? c.B / (D * K) : 0;
   const int32_t ns = tp.node_size;
@@ -56,16 +51,17 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   const int64_t ar_b = T > 1 ? mde : 0;
   const int64_t dlast = dout[(L - 1) & 1];
   const double loss = cost_compute(3 * m * dlast, tp);
-  // forward / backward layer op costs (absent collectives are +0.0)
-  AltSeq<3> fwd;
-  AltSeq<4> bwd;
+  // forward / backward layer op costs (absent collectives are +0.0), in the
+  // lane's row: fwd A [0,3) B [3,6), bwd A [6,10) B [10,14), LossGrad [14]
   {
-    const double fa[3] = {cost_compute(2 * m * w0, tp), 0.0, cost_compute(m * dout.a, tp)};
-    const double fb[3] = {cost_compute(2 * m * w1, tp), ar_tp, cost_compute(m * dout.b, tp)};
-    fwd.init(fa, fb);
-    const double ba[4] = {fa[2], cost_compute(4 * m * w0, tp), ar_tp, cost_compute(w0, tp)};
-    const double bb[4] = {fb[2], cost_compute(4 * m * w1, tp), 0.0, cost_compute(w1, tp)};
-    bwd.init(ba, bb);
+    const double relu_a = cost_compute(m * dout.a, tp), relu_b = cost_compute(m * dout.b, tp);
+    row[0] = cost_compute(2 * m * w0, tp); row[1] = 0.0; row[2] = relu_a;
+    row[3] = cost_compute(2 * m * w1, tp); row[4] = ar_tp; row[5] = relu_b;
+    row[6] = relu_a; row[7] = cost_compute(4 * m * w0, tp); row[8] = ar_tp;
+    row[9] = cost_compute(w0, tp);
+    row[10] = relu_b; row[11] = cost_compute(4 * m * w1, tp); row[12] = 0.0;
+    row[13] = cost_compute(w1, tp);
+    row[14] = loss;
   }
   // live-memory profiles of one forward / backward layer (C.7)
   const MemProf lf_a = mem_then(mem_op(m * nout.a * e, 0), mem_op(m * dout.a * e, m * dout.a * e));
@@ -87,6 +83,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   double clk[V], sendf[V], sendb[V];
   int64_t live[V], peak[V];
   MemProf pf[V], pb[V];
+  TaskCache cf[V], cb[V];
 #pragma unroll
   for (int q = 0; q < V; q++) {
     s[q] = sl + S * q;
@@ -111,6 +108,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if (nl > 1) b = mem_then(b, mem_alt(lb_a, lb_b, (hi[q] - 1) & 1, nl - 1));
     if (nl > 0) b = mem_then(b, lb(lo[q] & 1, true, s[q] == 0 && lo[q] == 0));
     pb[q] = b;
+    cf[q] = task_cache_make(row + 15 + 14 * q);      // 3 fwd segments
+    cb[q] = task_cache_make(row + 15 + 14 * q + 6);  // 4 bwd segments
   }
 
   // ---- forward wavefront: task (k, s) at step 2k + s
@@ -122,26 +121,28 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       const int kk = w - s[q];
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
       if (act[q]) {
-        fwd.run(clk[q], lo[q] & 1, hi[q] - lo[q]);
+        Seg sg[3];
+        alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
+        add_task(clk[q], sg, cf[q]);
         mem_apply(live[q], peak[q], pf[q]);
       }
     }
-    // Send s -> s+1: both ends wait for each other
+    // Send s -> s+1: both ends wait for each other; the end
+    // time travels back to the receiver (-1 = nothing sent)
     double nb[V], t[V];
-    bool snd[V], rin[V];
     Nbr<V>::up_stage(clk, nb, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      snd[q] = act[q] && s[q] < P - 1;
-      t[q] = dadd(fmax(clk[q], nb[q]), sendf[q]);
-      if (snd[q]) clk[q] = t[q];
+      const bool snd = act[q] && s[q] < P - 1;
+      const double end = dadd(fmax(clk[q], nb[q]), sendf[q]);
+      if (snd) clk[q] = end;
+      t[q] = snd ? end : -1.0;
     }
     double tin[V];
     Nbr<V>::down_stage(t, tin, lane);
-    Nbr<V>::down_flag(snd, rin, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] > 0 && rin[q]) {
+      if (ok[q] && s[q] > 0 && tin[q] >= 0.0) {
         clk[q] = tin[q];
         MEM(q, m * kin[lo[q] & 1] * e, 0);                    // received activation
       }
@@ -156,30 +157,31 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       const int kk = w - (int)(P - 1 - s[q]);
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
       if (act[q]) {
-        if (s[q] == P - 1) clk[q] = dadd(clk[q], loss);       // LossGrad
-        bwd.run(clk[q], (hi[q] - 1) & 1, hi[q] - lo[q]);
+        Seg sg[4];                                             // LossGrad, layers desc
+        sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
+        alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
+        add_task(clk[q], sg, cb[q]);
         mem_apply(live[q], peak[q], pb[q]);
       }
     }
     // Send s -> s-1
     double nb[V], t[V];
-    bool snd[V], rin[V];
     Nbr<V>::down_stage(clk, nb, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      snd[q] = act[q] && s[q] > 0;
-      t[q] = dadd(fmax(clk[q], nb[q]), sendb[q]);
-      if (snd[q]) {
-        clk[q] = t[q];
+      const bool snd = act[q] && s[q] > 0;
+      const double end = dadd(fmax(clk[q], nb[q]), sendb[q]);
+      if (snd) {
+        clk[q] = end;
         live[q] -= m * kin[lo[q] & 1] * e;                    // sent gradient dies
       }
+      t[q] = snd ? end : -1.0;
     }
     double tin[V];
     Nbr<V>::up_stage(t, tin, lane);
-    Nbr<V>::up_flag(snd, rin, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] < P - 1 && rin[q]) {
+      if (ok[q] && s[q] < P - 1 && tin[q] >= 0.0) {
         clk[q] = tin[q];
         MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);             // received gradient
       }
@@ -218,7 +220,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 // ------------------------------------------------ GPT-2 inference (C.4) -----
 template <int V>
 __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                         double& ms_out, int64_t& peak_out) {
+                         double* row, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
                 ide = c.M.ide, nctx = c.M.nctx;
   const bool lm = c.M.lm != 0;
@@ -233,23 +235,26 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   const double c_ln = cost_compute(5 * n * d, tp);
   const double c_att = cost_compute(2 * m * Sq * Sq * dT, tp);
   const double c_add = cost_compute(n * d, tp);
-  const double pro[2] = {cost_compute(2 * n * d, tp), c_ar};
-  const double blk[14] = {c_ln,
-                          cost_compute(2 * n * d * (3 * dT) + n * (3 * dT), tp),
-                          c_att,
-                          cost_compute(5 * m * hT * Sq * Sq, tp),
-                          c_att,
-                          cost_compute(2 * n * dT * d + n * d, tp),
-                          c_ar,
-                          c_add,
-                          c_ln,
-                          cost_compute(2 * n * d * (4 * dT) + n * (4 * dT), tp),
-                          cost_compute(8 * n * (4 * dT), tp),
-                          cost_compute(2 * n * (4 * dT) * d + n * d, tp),
-                          c_ar,
-                          c_add};
-  const double epi[3] = {c_ln, lm ? cost_compute(2 * n * d * VT, tp) : 0.0,
-                         (lm && T > 1) ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0};
+  // the lane's row: prologue [0,2), block [2,16), epilogue [16,19)
+  row[0] = cost_compute(2 * n * d, tp);                                  // Embed
+  row[1] = c_ar;                                                         // TP AllReduce
+  row[2] = c_ln;                                                         // ln_1
+  row[3] = cost_compute(2 * n * d * (3 * dT) + n * (3 * dT), tp);        // QKV
+  row[4] = c_att;                                                        // scores
+  row[5] = cost_compute(5 * m * hT * Sq * Sq, tp);                       // softmax
+  row[6] = c_att;                                                        // context
+  row[7] = cost_compute(2 * n * dT * d + n * d, tp);                     // proj
+  row[8] = c_ar;                                                         // TP AllReduce
+  row[9] = c_add;                                                        // residual
+  row[10] = c_ln;                                                        // ln_2
+  row[11] = cost_compute(2 * n * d * (4 * dT) + n * (4 * dT), tp);       // FC1
+  row[12] = cost_compute(8 * n * (4 * dT), tp);                          // GeLU
+  row[13] = cost_compute(2 * n * (4 * dT) * d + n * d, tp);              // FC2
+  row[14] = c_ar;                                                        // TP AllReduce
+  row[15] = c_add;                                                       // residual
+  row[16] = c_ln;                                                        // ln_f
+  row[17] = lm ? cost_compute(2 * n * d * VT, tp) : 0.0;                 // LM head
+  row[18] = (lm && T > 1) ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0;  // AllGather
   // live-memory profiles (C.7), for a normal and for the last microbatch
   // (whose ops free the parameters at their last use)
   const int64_t arb = T > 1 ? nde : 0;
@@ -290,6 +295,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   double clk[V], sendf[V];
   int64_t live[V], peak[V];
   MemProf ptask0[V], ptask1[V];   // normal / last microbatch
+  TaskCache tc[V];
 #pragma unroll
   for (int q = 0; q < V; q++) {
     s[q] = sl + S * q;
@@ -310,37 +316,38 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       if (s[q] == P - 1) r = mem_then(r, mepi[last]);
       if (last) ptask1[q] = r; else ptask0[q] = r;
     }
+    tc[q] = task_cache_make(row + 19 + 6 * q);       // 3 segments
   }
-  SeqCache cpro = seq_cache_empty(), cblk = seq_cache_empty(), cepi = seq_cache_empty();
 
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
   for (int w = 0; w < nsteps; w++) {
+    if (lane == 0) DISTIR_COUNT(4);
     bool act[V];
 #pragma unroll
     for (int q = 0; q < V; q++) {
       const int kk = w - s[q];
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
       if (!act[q]) continue;
-      if (s[q] == 0) add_reps(clk[q], pro, 1, cpro);              // prologue
-      add_reps(clk[q], blk, nb[q], cblk);                         // blocks
-      if (s[q] == P - 1) add_reps(clk[q], epi, 1, cepi);          // epilogue
+      const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
+                         Seg{row + 2, 14, nb[q]},                   // blocks
+                         Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
+      add_task(clk[q], sg, tc[q]);
       mem_apply(live[q], peak[q], (kk >> 1) == K - 1 ? ptask1[q] : ptask0[q]);
     }
     double nbv[V], t[V];
-    bool snd[V], rin[V];
     Nbr<V>::up_stage(clk, nbv, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      snd[q] = act[q] && s[q] < P - 1;
-      t[q] = dadd(fmax(clk[q], nbv[q]), sendf[q]);
-      if (snd[q]) { clk[q] = t[q]; live[q] -= nde; }          // sent activation dies
+      const bool snd = act[q] && s[q] < P - 1;
+      const double end = dadd(fmax(clk[q], nbv[q]), sendf[q]);
+      if (snd) { clk[q] = end; live[q] -= nde; }              // sent activation dies
+      t[q] = snd ? end : -1.0;
     }
     double tin[V];
     Nbr<V>::down_stage(t, tin, lane);
-    Nbr<V>::down_flag(snd, rin, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] > 0 && rin[q]) { clk[q] = tin[q]; MEM(q, nde, 0); }
+      if (ok[q] && s[q] > 0 && tin[q] >= 0.0) { clk[q] = tin[q]; MEM(q, nde, 0); }
     }
   }
   double msx = 0.0;

@@ -1,0 +1,50 @@
+"""Instrumented probe (build with -DDISTIR_INSTR): per grid, counts of
+add_task calls / fast-path hits / cache refreshes / crossing passes / warp
+steps, and warp cycles per work item.  Not part of the product."""
+import ctypes
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import workloads as W
+import paper_2111_05426_b200 as pkg
+from paper_2111_05426_b200 import Simulator
+
+NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles"]
+
+
+def counters():
+    buf = (ctypes.c_ulonglong * 16)()
+    pkg.lib.distir_debug_counters(buf, 16)
+    return list(buf)
+
+
+def main():
+    sim = Simulator(W.MODELS, W.TOPOLOGIES)
+    names = list(W.MODELS)
+    mi = {n: i for i, n in enumerate(names)}
+    tb = list(W.TOPOLOGIES).index("TB200")
+    cases = [("xl P2 K128", None, [(mi["gpt2_xl"], tb, 8, 1, 2, 128, 1 << 20)]),
+             ("16x xl P2 K128", None, [(mi["gpt2_xl"], tb, 8, 1, 2, 128, 1 << e) for e in range(7, 21)])]
+    cases += [(g, W.GRIDS[g], None) for g in ["W3", "W2", "W5"]]
+    for name, grid, cfgs in cases:
+        n = sim.upload(grid=grid, configs=cfgs)
+        outs = sim.device_outputs(n, k=10)
+        sim.launch(outs, k=10)
+        torch.cuda.synchronize()
+        counters()
+        sim.profile(True)
+        sim.launch(outs, k=10)
+        p = sim.profile(False)
+        c = counters()
+        d = dict(zip(NAMES, c))
+        print("%-16s sim %.3f ms  tasks %d fast %.3f refresh/task %.3f plain/task %.3f steps %d "
+              "items %d avg_item_cyc %.0f max_item_cyc %d" % (
+                  name, p["ms_simulate"], d["tasks"], d["fast"] / max(d["tasks"], 1),
+                  d["refresh"] / max(d["tasks"], 1), d["plain"] / max(d["tasks"], 1), d["steps"],
+                  d["items"], d["item_cycles"] / max(d["items"], 1), d["max_item_cycles"]))
+
+
+if __name__ == "__main__":
+    main()
