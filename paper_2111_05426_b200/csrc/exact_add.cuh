@@ -28,11 +28,23 @@
 #pragma once
 #include <cstdint>
 
+#ifndef DISTIR_COLD_NOINLINE
+#define DISTIR_COLD_NOINLINE 0
+#endif
+#ifndef DISTIR_UNROLL_SEG
+#define DISTIR_UNROLL_SEG 0
+#endif
 #ifndef DISTIR_HD
 #ifdef __CUDACC__
 #define DISTIR_HD __host__ __device__ __forceinline__
+#if DISTIR_COLD_NOINLINE
+#define DISTIR_HD_COLD __host__ __device__ __noinline__
+#else
+#define DISTIR_HD_COLD __host__ __device__ __forceinline__
+#endif
 #else
 #define DISTIR_HD inline
+#define DISTIR_HD_COLD inline
 #endif
 #endif
 
@@ -81,8 +93,16 @@ DISTIR_HD int32_t exp_field(double x) { return (int32_t)((d2bits(x) >> 52) & 0x7
 
 DISTIR_HD int odd(double integral) { return (int)((int64_t)integral & 1); }
 
+constexpr int kSegMax = 14;   // longest op sequence of a segment (GPT-2 block)
+
 DISTIR_HD void seq_plain(double& x, const double* a, int n) {
+#if DISTIR_UNROLL_SEG
+#pragma unroll
+  for (int j = 0; j < kSegMax; j++)
+    if (j < n) x = xadd(x, a[j]);
+#else
   for (int j = 0; j < n; j++) x = xadd(x, a[j]);
+#endif
 }
 
 // Ulps added by one pass of a[0..n) at binade field ef, from an even (R0) and
@@ -93,7 +113,11 @@ DISTIR_HD bool seg_pass(const double* a, int n, int32_t ef, double& R0, double& 
   const double inv_u = bits2d((int64_t)(2098 - ef) << 52);    // 2^(52-E)
   double R = 0.0;
   bool tie = false, never = false;
-  for (int j = 0; j < n; j++) {
+#if DISTIR_UNROLL_SEG
+#pragma unroll
+#endif
+  for (int j = 0; j < kSegMax; j++) {             // the ops are independent
+    if (j >= n) break;
     const double q = xmul(a[j], inv_u);
     never |= !(q < kTwo53d);
     tie |= (xadd(q, -xfloor(q)) == 0.5);
@@ -104,7 +128,8 @@ DISTIR_HD bool seg_pass(const double* a, int n, int32_t ef, double& R0, double& 
   if (tie) {                      // resolve ties by the running parity
     R0 = R1 = 0.0;
     int p0 = 0, p1 = 1;
-    for (int j = 0; j < n; j++) {
+    for (int j = 0; j < kSegMax; j++) {
+      if (j >= n) break;
       const double q = xmul(a[j], inv_u);
       const double fl = xfloor(q);
       const double fr = xadd(q, -fl);
@@ -183,24 +208,33 @@ DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
   c.Su1 = (ok && T[1] < kTwo53d) ? xmul(T[1], u) : -1.0;
 }
 
-// x <- every addition of the task, in order, computed exactly.  Fast path:
-// one add when the whole task stays inside x's binade.  Otherwise each
-// segment advances by whole passes while they fit (closed form, or a short
-// parity walk when the binade has ties), the pass that leaves the binade is
-// done op by op, and the cache moves to the new binade.
+// Fast path of a task: when x lies in the cached binade and the whole task
+// stays inside it, x <- x + Su (exact) and true; otherwise x is untouched
+// and false.  Branch-free (the caller branches once, warp-uniformly, on the
+// rare misses).
+DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
+  const int64_t xb = d2bits(x);
+  const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+  const double Su = (xb & 1) ? c.Su1 : c.Su0;
+  const double y = xadd(x, Su);
+  const bool ok = x > 0.0 && ef == c.ef && Su >= 0.0 && exp_field(y) == ef;
+  x = ok ? y : x;
+  return ok;
+}
+
+// x <- every addition of the task, in order, computed exactly: the cache is
+// moved to x's binade and the fast path retried; otherwise each segment
+// advances by whole passes while they fit (closed form, or a short parity
+// walk when the binade has ties), the pass that leaves the binade is done op
+// by op, and the cache follows x into the new binade.
 template <int NS>
-DISTIR_HD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
+DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
   DISTIR_COUNT(0);
   {
-    const int64_t xb = d2bits(x);
-    const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+    const int32_t ef = exp_field(x);
     if (x > 0.0 && ef >= 53 && ef <= 1993) {
       if (ef != c.ef) task_refresh(c, ef, sg);
-      const double Su = (xb & 1) ? c.Su1 : c.Su0;
-      if (Su >= 0.0) {
-        const double y = xadd(x, Su);
-        if (exp_field(y) == ef) { x = y; DISTIR_COUNT(1); return; }
-      }
+      if (task_fast(x, c)) { DISTIR_COUNT(1); return; }
     }
   }
 #pragma unroll

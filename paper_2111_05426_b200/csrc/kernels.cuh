@@ -436,185 +436,174 @@ __global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ 
 }
 
 // ------------------------------------------------------------ top-k ---------
+// The C.8 total order -- throughput desc, peak asc, index asc -- as an
+// unsigned lexicographic key (larger = better): a = bits of the throughput
+// (a non-negative double, so its bit pattern orders like its value; 0 marks
+// "no candidate": feasible throughputs are > 0), b = ~peak, c = ~index.
 struct Key {
-  double tp;
-  int64_t peak, idx;
+  uint64_t a, b, c;
   double ms;
 };
 
-__device__ __forceinline__ bool better(const Key& a, const Key& b) {
-  if (a.tp != b.tp) return a.tp > b.tp;
-  if (a.peak != b.peak) return a.peak < b.peak;
-  return a.idx < b.idx;
+__device__ __forceinline__ Key make_key(double tp, int64_t peak, int64_t idx, double ms) {
+  return Key{(uint64_t)__double_as_longlong(tp), ~(uint64_t)peak, ~(uint64_t)idx, ms};
+}
+__device__ __forceinline__ Key no_key() { return Key{0, 0, 0, 0.0}; }
+__device__ __forceinline__ bool better(const Key& x, const Key& y) {      // x > y
+  return x.a > y.a || (x.a == y.a && (x.b > y.b || (x.b == y.b && x.c > y.c)));
+}
+__device__ __forceinline__ TopkRec key_rec(const Key& k) {
+  return TopkRec{(int64_t)~k.c, k.ms, __longlong_as_double((long long)k.a), (int64_t)~k.b};
+}
+__device__ __forceinline__ void cswap(Key& x, Key& y) {                    // x >= y after
+  const bool sw = better(y, x);
+  const Key t = x;
+  x = sw ? y : x;
+  y = sw ? t : y;
 }
 
-__device__ __forceinline__ Key worst_key() { return Key{-1.0, LLONG_MAX, LLONG_MAX, 0.0}; }
-
-__device__ __forceinline__ Key shfl_key(const Key& k, int o) {
-  Key r;
-  r.tp = __shfl_xor_sync(0xffffffffu, k.tp, o);
-  r.peak = __shfl_xor_sync(0xffffffffu, k.peak, o);
-  r.idx = __shfl_xor_sync(0xffffffffu, k.idx, o);
-  r.ms = __shfl_xor_sync(0xffffffffu, k.ms, o);
-  return r;
-}
-
-// Block-wide best under `better` (blockDim.x a multiple of 32, <= 1024).
-// No trailing barrier: the next call rewrites s_k only after every thread
-// has passed this call's second barrier.
-__device__ Key block_best(Key k) {
-  __shared__ Key s_k[32];
-  __shared__ Key s_b;
-  for (int o = 16; o > 0; o >>= 1) {
-    const Key x = shfl_key(k, o);
-    if (better(x, k)) k = x;
-  }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) s_k[w] = k;
-  __syncthreads();
-  if (w == 0) {
-    Key x = lane < (int)(blockDim.x >> 5) ? s_k[lane] : worst_key();
-    for (int o = 16; o > 0; o >>= 1) {
-      const Key y = shfl_key(x, o);
-      if (better(y, x)) x = y;
-    }
-    if (lane == 0) s_b = x;
-  }
-  __syncthreads();
-  return s_b;
-}
-
-__device__ __forceinline__ Key best_sentinel() {
-  return Key{__longlong_as_double(0x7FF0000000000000ll), LLONG_MIN, LLONG_MIN, 0.0};
-}
-
+// Warp-wide best key (all lanes get it), comparing (a, b, c) only.
 __device__ __forceinline__ Key warp_best(Key k) {
   for (int o = 16; o > 0; o >>= 1) {
-    const Key x = shfl_key(k, o);
-    if (better(x, k)) k = x;
+    Key x;
+    x.a = __shfl_xor_sync(0xffffffffu, k.a, o);
+    x.b = __shfl_xor_sync(0xffffffffu, k.b, o);
+    x.c = __shfl_xor_sync(0xffffffffu, k.c, o);
+    if (better(x, k)) { k.a = x.a; k.b = x.b; k.c = x.c; }
   }
   return k;
 }
 
-// Select the k best of a candidate set, one round per rank: round r keeps the
-// best candidate strictly worse than round r-1's winner (keys are unique).
-// Register path (n <= IPT*blockDim): every warp first selects the top k of
-// its own lanes' candidates with warp shuffles only (no block barriers),
-// then warp 0 merges the per-warp lists from shared memory.
-template <int IPT, typename Fetch>
-__device__ int select_topk_reg(int64_t n, int k, Fetch fetch, TopkRec* out) {
+// Top k of a candidate set held in registers (n <= kTopkIPT * blockDim.x).
+// Each thread sorts its <= 8 candidates (sorting network), each warp then
+// extracts its top k by k rounds of warp-best over the lanes' heads (the
+// winning lane pops its head), and warp 0 merges the per-warp lists the same
+// way.  No block barrier inside the rounds.  Result valid in warp 0.
+template <typename Fetch>
+__device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
   __shared__ Key s_cand[kTopkThreads / 32][kMaxK];
   __shared__ int s_cnt[kTopkThreads / 32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  Key it[IPT];
+  Key it[kTopkIPT];
 #pragma unroll
-  for (int i = 0; i < IPT; i++) {
+  for (int i = 0; i < kTopkIPT; i++) {
     const int64_t j = threadIdx.x + (int64_t)i * blockDim.x;
-    if (!(j < n && fetch(j, it[i]))) it[i] = worst_key();
+    if (!(j < n && fetch(j, it[i]))) it[i] = no_key();
   }
-  Key prev = best_sentinel();
-  int got = 0;
+  // Batcher odd-even merge sort of 8 (19 comparators), descending
+  cswap(it[0], it[1]); cswap(it[2], it[3]); cswap(it[4], it[5]); cswap(it[6], it[7]);
+  cswap(it[0], it[2]); cswap(it[1], it[3]); cswap(it[4], it[6]); cswap(it[5], it[7]);
+  cswap(it[1], it[2]); cswap(it[5], it[6]);
+  cswap(it[0], it[4]); cswap(it[1], it[5]); cswap(it[2], it[6]); cswap(it[3], it[7]);
+  cswap(it[2], it[4]); cswap(it[3], it[5]);
+  cswap(it[1], it[2]); cswap(it[3], it[4]); cswap(it[5], it[6]);
+  int head = 0, got = 0;
   for (int r = 0; r < k; r++) {
-    Key best = worst_key();
+    Key mine = no_key();
 #pragma unroll
-    for (int i = 0; i < IPT; i++)
-      if (better(prev, it[i]) && better(it[i], best)) best = it[i];
-    best = warp_best(best);
-    if (best.idx == LLONG_MAX) break;
-    if (lane == 0) s_cand[w][r] = best;
-    prev = best;
+    for (int i = 0; i < kTopkIPT; i++)
+      if (i == head) mine = it[i];
+    const Key best = warp_best(mine);
+    if (best.a == 0) break;
+    if (mine.a != 0 && mine.c == best.c) {         // this lane's head won
+      s_cand[w][r] = mine;
+      head++;
+    }
     got++;
   }
   if (lane == 0) s_cnt[w] = got;
   __syncthreads();
   got = 0;
   if (w == 0) {
-    prev = best_sentinel();
+    int ptr = 0;
+    const int cnt = lane < nw ? s_cnt[lane] : 0;
     for (int r = 0; r < k; r++) {
-      Key best = worst_key();
-      for (int j = lane; j < nw * k; j += 32) {
-        const int ww = j / k, rr = j - ww * k;
-        if (rr >= s_cnt[ww]) continue;
-        const Key c = s_cand[ww][rr];
-        if (better(prev, c) && better(c, best)) best = c;
+      const Key mine = ptr < cnt ? s_cand[lane][ptr] : no_key();
+      const Key best = warp_best(mine);
+      if (best.a == 0) break;
+      if (mine.a != 0 && mine.c == best.c) {
+        out[r] = key_rec(mine);
+        ptr++;
       }
-      best = warp_best(best);
-      if (best.idx == LLONG_MAX) break;
-      if (lane == 0) out[r] = TopkRec{best.idx, best.ms, best.tp, best.peak};
-      prev = best;
       got++;
     }
   }
   return got;    // valid in warp 0
 }
 
-// General path: candidates re-read every round.
+// Stream candidates [0, n) of `fetch` through select_topk in chunks of
+// kTopkIPT*kTopkThreads - kMaxK, carrying the best-so-far list (in shared
+// memory) into every chunk.  Chunks c = first, first + step, ...  Returns the
+// list length (all threads); the list is in s_acc.
 template <typename Fetch>
-__device__ int select_topk_scan(int64_t n, int k, Fetch fetch, TopkRec* out) {
-  Key prev = best_sentinel();
-  int got = 0;
-  for (int r = 0; r < k; r++) {
-    Key best = worst_key();
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-      Key c;
-      if (!fetch(j, c)) continue;
-      if (better(prev, c) && better(c, best)) best = c;
-    }
-    best = block_best(best);
-    if (best.idx == LLONG_MAX) break;
-    if (threadIdx.x == 0) out[r] = TopkRec{best.idx, best.ms, best.tp, best.peak};
-    prev = best;
-    got++;
+__device__ int topk_stream(int64_t n, int64_t first, int64_t step, int k, Fetch fetch,
+                           TopkRec* s_acc, int* s_acc_n) {
+  const int64_t per = (int64_t)kTopkIPT * kTopkThreads - kMaxK;
+  if (threadIdx.x == 0) *s_acc_n = 0;
+  __syncthreads();
+  for (int64_t c = first; c * per < n || (c == first && n == 0); c += step) {
+    const int64_t base = c * per;
+    const int64_t len = n - base < per ? (n - base > 0 ? n - base : 0) : per;
+    const int acc_n = *s_acc_n;
+    auto f2 = [&](int64_t j, Key& key) -> bool {
+      if (j < acc_n) {
+        const TopkRec x = s_acc[j];
+        key = make_key(x.throughput, x.peak, x.index, x.makespan);
+        return true;
+      }
+      return fetch(base + (j - acc_n), key);
+    };
+    const int got = select_topk(acc_n + len, k, f2, s_acc);
+    __syncthreads();
+    if (threadIdx.x == 0) *s_acc_n = got;
+    __syncthreads();
   }
-  return got;
+  return *s_acc_n;
 }
 
-template <typename Fetch>
-__device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
-  if (n <= (int64_t)kTopkIPT * blockDim.x) return select_topk_reg<kTopkIPT>(n, k, fetch, out);
-  return select_topk_scan(n, k, fetch, out);
-}
-
-// One block per contiguous slice of the shard.
+// Partial top-k of the shard: grid-strided chunks per block.
 __global__ void __launch_bounds__(kTopkThreads) k_topk_partial(
     const SpecBlock* __restrict__ spp, const double* __restrict__ ms,
     const int64_t* __restrict__ pk, const uint32_t* __restrict__ rs,
     const double* __restrict__ tpv, int k, TopkRec* __restrict__ part, int* __restrict__ part_n) {
+  __shared__ TopkRec s_acc[kMaxK];
+  __shared__ int s_acc_n;
   const SpecBlock& sp = *spp;
   const int64_t n = sp.n_local;
-  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t a = blockIdx.x * chunk;
-  const int64_t b = a + chunk < n ? a + chunk : n;
   const int64_t rank = sp.rank, nr = sp.n_ranks;
-  auto fetch = [&](int64_t j, Key& c) -> bool {
-    const int64_t q = a + j;
+  auto fetch = [&](int64_t q, Key& c) -> bool {
     if (rs[q] != 0) return false;
-    c = Key{tpv[q], pk[q], rank + q * nr, ms[q]};
+    c = make_key(tpv[q], pk[q], rank + q * nr, ms[q]);
     return true;
   };
-  const int got = select_topk(b > a ? b - a : 0, k, fetch, part + (int64_t)blockIdx.x * k);
+  const int got = topk_stream(n, blockIdx.x, gridDim.x, k, fetch, s_acc, &s_acc_n);
+  TopkRec* o = part + (int64_t)blockIdx.x * k;
+  for (int r = threadIdx.x; r < got; r += blockDim.x) o[r] = s_acc[r];
   if (threadIdx.x == 0) part_n[blockIdx.x] = got;
 }
 
-// Merge n_lists lists of up to k_in records (counts in list_n, or, when
-// list_n == NULL, index >= 0 marks a valid record); pads `out` to k.
+// Merge lists of up to k_in records: `n_lists` lists with counts in list_n,
+// or, when list_n == NULL, records with index >= 0 are valid.  One block;
+// pads `out` to k.
 __global__ void __launch_bounds__(kTopkThreads) k_topk_merge(const TopkRec* __restrict__ lists,
-                                                     const int* __restrict__ list_n, int n_lists,
-                                                     int k_in, int k, TopkRec* __restrict__ out,
-                                                     int* __restrict__ out_n) {
+                                                            const int* __restrict__ list_n,
+                                                            int n_lists, int k_in, int k,
+                                                            TopkRec* __restrict__ out,
+                                                            int* __restrict__ out_n) {
+  __shared__ TopkRec s_acc[kMaxK];
+  __shared__ int s_acc_n;
   auto fetch = [&](int64_t j, Key& c) -> bool {
     const int jj = (int)j;
     const int l = jj / k_in, r = jj - l * k_in;
     if (list_n ? r >= list_n[l] : lists[jj].index < 0) return false;
     const TopkRec x = lists[jj];
-    c = Key{x.throughput, x.peak, x.index, x.makespan};
+    c = make_key(x.throughput, x.peak, x.index, x.makespan);
     return true;
   };
-  const int got = select_topk((int64_t)n_lists * k_in, k, fetch, out);
-  if (threadIdx.x == 0) {
-    *out_n = got;
-    for (int r = got; r < k; r++) out[r] = TopkRec{-1, 0.0, -1.0, -1};
-  }
+  const int got = topk_stream((int64_t)n_lists * k_in, 0, 1, k, fetch, s_acc, &s_acc_n);
+  for (int r = threadIdx.x; r < k; r += blockDim.x)
+    out[r] = r < got ? s_acc[r] : TopkRec{-1, 0.0, -1.0, -1};
+  if (threadIdx.x == 0) *out_n = got;
 }
 
 }  // namespace distir

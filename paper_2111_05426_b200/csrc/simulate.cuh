@@ -120,11 +120,12 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) {
       const int kk = w - s[q];
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) {
+      if (act[q]) mem_apply(live[q], peak[q], pf[q]);
+      const bool slow = act[q] && !task_fast(clk[q], cf[q]);
+      if (__any_sync(0xffffffffu, slow) && slow) {
         Seg sg[3];
         alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
         add_task(clk[q], sg, cf[q]);
-        mem_apply(live[q], peak[q], pf[q]);
       }
     }
     // Send s -> s+1: both ends wait for each other; the end
@@ -156,12 +157,13 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) {
       const int kk = w - (int)(P - 1 - s[q]);
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) {
+      if (act[q]) mem_apply(live[q], peak[q], pb[q]);
+      const bool slow = act[q] && !task_fast(clk[q], cb[q]);
+      if (__any_sync(0xffffffffu, slow) && slow) {
         Seg sg[4];                                             // LossGrad, layers desc
         sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
         alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
         add_task(clk[q], sg, cb[q]);
-        mem_apply(live[q], peak[q], pb[q]);
       }
     }
     // Send s -> s-1
@@ -327,12 +329,14 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     for (int q = 0; q < V; q++) {
       const int kk = w - s[q];
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (!act[q]) continue;
-      const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
-                         Seg{row + 2, 14, nb[q]},                   // blocks
-                         Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
-      add_task(clk[q], sg, tc[q]);
-      mem_apply(live[q], peak[q], (kk >> 1) == K - 1 ? ptask1[q] : ptask0[q]);
+      if (act[q]) mem_apply(live[q], peak[q], (kk >> 1) == K - 1 ? ptask1[q] : ptask0[q]);
+      const bool slow = act[q] && !task_fast(clk[q], tc[q]);
+      if (__any_sync(0xffffffffu, slow) && slow) {
+        const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
+                           Seg{row + 2, 14, nb[q]},                   // blocks
+                           Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
+        add_task(clk[q], sg, tc[q]);
+      }
     }
     double nbv[V], t[V];
     Nbr<V>::up_stage(clk, nbv, lane);
