@@ -18,7 +18,12 @@ constexpr int kMaxRanks = 8;        // GPUs merged by the all-gather
 constexpr int kNumBuckets = 4096;   // hash slots for warp-shape buckets
 constexpr int kOverflowBucket = kNumBuckets;  // catch-alls: + kind (1 config / warp)
 constexpr int kBucketSlots = kNumBuckets + 2;
-constexpr int kGroups = 4;          // simulate kernels: (MLP, GPT-2) x (1, 2 stages/lane)
+// Simulate kernels ("groups"): model kind x schedule mode.  Modes 0-2: one
+// lane walks a whole configuration in program order, P <= 1 / 2 / 4 stages;
+// modes 3-4: wavefront, one lane per stage (mode 4: two stages per lane,
+// 32 < P <= 64, and the catch-all buckets).
+constexpr int kModes = 5;
+constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
@@ -89,7 +94,7 @@ struct Bucket {          // per hash slot (plus one overflow slot)
   uint32_t cursor;       // scatter cursor
   uint32_t lanes;        // lanes per config S (power of two <= 32)
   uint16_t cls;          // weight class
-  uint16_t group;        // simulate kernel: kind * 2 + (two stages per lane)
+  uint16_t group;        // simulate kernel: kind * kModes + mode
   uint32_t item_off;     // offset within (group, class)
 };
 

@@ -147,7 +147,7 @@ struct distir_sim {
   std::vector<DModel> models;
   std::vector<DTopo> topos;
   int num_sms = 0;
-  int sim_grid[kGroups] = {0, 0, 0, 0};
+  int sim_grid[kGroups] = {};
   int enum_grid = 0;
   SpecBlock spec{};
   bool uploaded = false;
@@ -399,10 +399,22 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   }
   CUDA_TRY(mark(1));
   if (n > 0) {
-    k_simulate<0, 1><<<sim->sim_grid[0], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
-    k_simulate<0, 2><<<sim->sim_grid[1], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
-    k_simulate<1, 1><<<sim->sim_grid[2], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
-    k_simulate<1, 2><<<sim->sim_grid[3], 128, 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv);
+#define DISTIR_SIM(KD, MD) \
+  k_simulate<KD, MD><<<sim->sim_grid[KD * kModes + MD], sim_tpb(KD, MD), 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv)
+#if DISTIR_SEQ_MAXP >= 1
+    DISTIR_SIM(0, 0); DISTIR_SIM(1, 0);
+    kernels += 2;
+#endif
+#if DISTIR_SEQ_MAXP >= 2
+    DISTIR_SIM(0, 1); DISTIR_SIM(1, 1);
+    kernels += 2;
+#endif
+#if DISTIR_SEQ_MAXP >= 3
+    DISTIR_SIM(0, 2); DISTIR_SIM(1, 2);
+    kernels += 2;
+#endif
+    DISTIR_SIM(0, 3); DISTIR_SIM(0, 4); DISTIR_SIM(1, 3); DISTIR_SIM(1, 4);
+#undef DISTIR_SIM
     kernels += 4;
   }
   CUDA_TRY(mark(2));
@@ -628,11 +640,14 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   sim->stream = static_cast<cudaStream_t>(cuda_stream);
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sim->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
-  int per_sm[kGroups] = {0, 0, 0, 0};
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_simulate<0, 1>, 128, 0);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_simulate<0, 2>, 128, 0);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], k_simulate<1, 1>, 128, 0);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[3], k_simulate<1, 2>, 128, 0);
+  int per_sm[kGroups] = {};
+  const void* fns[kGroups] = {
+      (const void*)k_simulate<0, 0>, (const void*)k_simulate<0, 1>, (const void*)k_simulate<0, 2>,
+      (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<1, 0>,
+      (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>, (const void*)k_simulate<1, 3>,
+      (const void*)k_simulate<1, 4>};
+  for (int g = 0; g < kGroups && e == cudaSuccess; g++)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], fns[g], sim_tpb(g / kModes, g % kModes), 0);
   if (e != cudaSuccess) {
     delete sim;
     return fail(DISTIR_E_CUDA, std::string("device setup: ") + cudaGetErrorString(e));

@@ -277,6 +277,15 @@ __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
   return p;
 }
 
+// P <= DISTIR_SEQ_MAXP: one lane walks a whole configuration in program order
+// (modes 0-2).  Measured on B200 (tools/variants.sh, W1-W5): the per-lane
+// program-order walk helps isolated P = 1 chains but loses on every grid
+// (more configurations per warp = more divergent binade crossings per step),
+// so the default routes every P to the wavefront kernels.
+#ifndef DISTIR_SEQ_MAXP
+#define DISTIR_SEQ_MAXP 0
+#endif
+
 // One block: lanes per config, simulate kernel (group), work items numbered
 // group-major and heaviest weight class first within a group (LPT order for
 // the persistent simulate kernels), config ranges.
@@ -295,16 +304,23 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
     if (b >= kOverflowBucket) {        // mixed shapes: one config per warp
       lanes = 32;
       cls = kNumClasses - 1;
-      group = (uint32_t)(b - kOverflowBucket) * 2 + 1;
+      group = (uint32_t)(b - kOverflowBucket) * kModes + 4;
     } else {
-      const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, L = ((B.key >> 7) & 1023) + 1,
-                     K = (B.key >> 17) & 255;
-      lanes = P < 32 ? pow2ceil32(P) : 32;
-      const unsigned long long per = (L + P - 1) / P;
-      unsigned long long est = (2ull * K + P) * per * (kind ? 14ull : 8ull) + 1;
-      cls = 63 - __clzll(est);
+      const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, K = (B.key >> 17) & 255;
+      uint32_t mode;
+      unsigned long long est;            // serial chain, in tasks
+      if (P <= DISTIR_SEQ_MAXP) {
+        lanes = 1;
+        mode = P == 1 ? 0 : (P == 2 ? 1 : 2);
+        est = (unsigned long long)K * P * (kind ? 1ull : 2ull);
+      } else {
+        lanes = P < 32 ? pow2ceil32(P) : 32;
+        mode = P > 32 ? 4 : 3;
+        est = (2ull * K + P) * (kind ? 1ull : 2ull) * 2;
+      }
+      cls = 63 - __clzll(est + 1);
       if (cls >= kNumClasses) cls = kNumClasses - 1;
-      group = kind * 2 + (P > 32 ? 1 : 0);
+      group = kind * kModes + mode;
     }
     const uint32_t cpw = 32 / lanes;
     const uint32_t items = (B.count + cpw - 1) / cpw;
@@ -362,8 +378,18 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
 
 // Persistent simulate kernel for one group (model kind x stages per lane):
 // each warp pulls work items of its group, heaviest weight class first.
-template <int KIND, int V>
-__global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ spp,
+__host__ __device__ constexpr int sim_v(int mode) {
+  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : mode == 3 ? 1 : 2;
+}
+__host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per lane row
+  return kind == 1 ? 19 + 6 * sim_v(mode) : 15 + 14 * sim_v(mode);
+}
+__host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per block
+  return sim_row(kind, mode) * 8 * 128 <= 48 * 1024 ? 128 : 64;
+}
+
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(sim_tpb(KIND, MODE)) k_simulate(const SpecBlock* __restrict__ spp,
                                                   const DExplicit* __restrict__ ex,
                                                   const Bucket* __restrict__ bk,
                                                   const Item* __restrict__ items,
@@ -373,19 +399,32 @@ __global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ 
                                                   int64_t* __restrict__ pk_out,
                                                   uint32_t* __restrict__ rs_out,
                                                   double* __restrict__ tp_out) {
-  constexpr int G = KIND * 2 + (V == 2 ? 1 : 0);
+  constexpr int G = KIND * kModes + MODE;
+  constexpr bool SEQ = MODE < 3;
+  constexpr int V = sim_v(MODE);
   const SpecBlock& sp = *spp;
   const int lane = threadIdx.x & 31;
   const unsigned int first = hdr->group_begin[G], end = hdr->group_begin[G + 1];
+  // Warp w starts on item first + w (no atomic; heaviest items go to the
+  // first warps), then pulls items past the grid's warp count from a queue.
+  const unsigned int n_warps = gridDim.x * (blockDim.x >> 5);
+  const unsigned int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  bool first_item = true;
   // per-lane rows: op costs, then per-slot task-cache increments
-  constexpr int ROW = KIND == 1 ? 19 + 6 * V : 15 + 14 * V;
-  __shared__ double s_row[128][ROW];
+  constexpr int ROW = sim_row(KIND, MODE);
+  __shared__ double s_row[sim_tpb(KIND, MODE)][ROW];
   double* row = s_row[threadIdx.x];
   unsigned long long feas = 0;
   while (true) {
-    unsigned int id = 0;
-    if (lane == 0) id = first + atomicAdd(&hdr->item_counter[G], 1u);
-    id = __shfl_sync(0xffffffffu, id, 0);
+    unsigned int id;
+    if (first_item) {
+      id = first + gw;
+      first_item = false;
+    } else {
+      id = 0;
+      if (lane == 0) id = first + n_warps + atomicAdd(&hdr->item_counter[G], 1u);
+      id = __shfl_sync(0xffffffffu, id, 0);
+    }
     if (id >= end) break;
     const Item it = items[id];
     const Bucket& B = bk[it.bucket];
@@ -406,8 +445,8 @@ __global__ void __launch_bounds__(128) k_simulate(const SpecBlock* __restrict__ 
 #ifdef DISTIR_INSTR
     const long long t0 = clock64();
 #endif
-    if constexpr (KIND == 1) run_gpt2<V>(c, tp, has, sl, S, lane, row, ms, pk);
-    else run_mlp<V>(c, tp, has, sl, S, lane, row, ms, pk);
+    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, ms, pk);
+    else run_mlp<V, SEQ>(c, tp, has, sl, S, lane, row, ms, pk);
 #ifdef DISTIR_INSTR
     if (lane == 0) {
       const unsigned long long dt = (unsigned long long)(clock64() - t0);

@@ -33,7 +33,7 @@ __device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, in
   a = Seg{row + oa, na, n1 & 1};
 }
 
-template <int V>
+template <int V, bool SEQ>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                         double* row, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
@@ -112,6 +112,55 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     cb[q] = task_cache_make(row + 15 + 14 * q + 6);  // 4 bwd segments
   }
 
+  auto fwd_task = [&](int q, bool act) {
+    if (act) mem_apply(live[q], peak[q], pf[q]);
+    const bool slow = act && !task_fast(clk[q], cf[q]);
+    if (__any_sync(0xffffffffu, slow) && slow) {
+      Seg sg[3];
+      alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
+      add_task(clk[q], sg, cf[q]);
+    }
+  };
+  auto bwd_task = [&](int q, bool act) {
+    if (act) mem_apply(live[q], peak[q], pb[q]);
+    const bool slow = act && !task_fast(clk[q], cb[q]);
+    if (__any_sync(0xffffffffu, slow) && slow) {
+      Seg sg[4];                                               // LossGrad, layers desc
+      sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
+      alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
+      add_task(clk[q], sg, cb[q]);
+    }
+  };
+  if constexpr (SEQ) {
+    // ---- program order (one lane owns all P <= V stages)
+    const int K_ = warp_max_int(has ? (int)K : 0);
+    for (int k = 0; k < K_; k++) {
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        fwd_task(q, ok[q] && k < K);
+        if (q + 1 < V && ok[q] && q + 1 < P) {                // Send q -> q+1
+          const double end = dadd(fmax(clk[q], clk[q + 1 < V ? q + 1 : q]), sendf[q]);
+          clk[q] = end;
+          clk[q + 1 < V ? q + 1 : q] = end;
+          MEM(q + 1 < V ? q + 1 : q, m * kin[lo[q + 1 < V ? q + 1 : q] & 1] * e, 0);
+        }
+      }
+    }
+    for (int k = 0; k < K_; k++) {
+#pragma unroll
+      for (int q = V - 1; q >= 0; q--) {
+        bwd_task(q, ok[q] && k < K);
+        if (q > 0 && ok[q]) {                                  // Send q -> q-1
+          const int qm = q > 0 ? q - 1 : 0;
+          const double end = dadd(fmax(clk[q], clk[qm]), sendb[q]);
+          clk[q] = end;
+          clk[qm] = end;
+          live[q] -= m * kin[lo[q] & 1] * e;                   // sent gradient dies
+          MEM(qm, m * dout[(hi[qm] - 1) & 1] * e, 0);          // received gradient
+        }
+      }
+    }
+  } else {
   // ---- forward wavefront: task (k, s) at step 2k + s
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
   for (int w = 0; w < nsteps; w++) {
@@ -120,13 +169,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) {
       const int kk = w - s[q];
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) mem_apply(live[q], peak[q], pf[q]);
-      const bool slow = act[q] && !task_fast(clk[q], cf[q]);
-      if (__any_sync(0xffffffffu, slow) && slow) {
-        Seg sg[3];
-        alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
-        add_task(clk[q], sg, cf[q]);
-      }
+      fwd_task(q, act[q]);
     }
     // Send s -> s+1: both ends wait for each other; the end
     // time travels back to the receiver (-1 = nothing sent)
@@ -157,14 +200,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) {
       const int kk = w - (int)(P - 1 - s[q]);
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) mem_apply(live[q], peak[q], pb[q]);
-      const bool slow = act[q] && !task_fast(clk[q], cb[q]);
-      if (__any_sync(0xffffffffu, slow) && slow) {
-        Seg sg[4];                                             // LossGrad, layers desc
-        sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
-        alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
-        add_task(clk[q], sg, cb[q]);
-      }
+      bwd_task(q, act[q]);
     }
     // Send s -> s-1
     double nb[V], t[V];
@@ -189,6 +225,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       }
     }
   }
+  }  // wavefront
 
   // ---- tail: DP AllReduce of the accumulated gradients, then SGD (once per
   // stage: plain op-by-op walk)
@@ -220,7 +257,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 }
 
 // ------------------------------------------------ GPT-2 inference (C.4) -----
-template <int V>
+template <int V, bool SEQ>
 __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                          double* row, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
@@ -321,6 +358,34 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     tc[q] = task_cache_make(row + 19 + 6 * q);       // 3 segments
   }
 
+  auto task = [&](int q, bool act, bool last) {
+    if (act) mem_apply(live[q], peak[q], last ? ptask1[q] : ptask0[q]);
+    const bool slow = act && !task_fast(clk[q], tc[q]);
+    if (__any_sync(0xffffffffu, slow) && slow) {
+      const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
+                         Seg{row + 2, 14, nb[q]},                   // blocks
+                         Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
+      add_task(clk[q], sg, tc[q]);
+    }
+  };
+  if constexpr (SEQ) {
+    // ---- program order (one lane owns all P <= V stages)
+    const int K_ = warp_max_int(has ? (int)K : 0);
+    for (int k = 0; k < K_; k++) {
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        task(q, ok[q] && k < K, k == K - 1);
+        if (q + 1 < V && ok[q] && q + 1 < P) {                // Send q -> q+1
+          const int qp = q + 1 < V ? q + 1 : q;
+          const double end = dadd(fmax(clk[q], clk[qp]), sendf[q]);
+          clk[q] = end;
+          clk[qp] = end;
+          live[q] -= nde;                                      // sent activation dies
+          MEM(qp, nde, 0);                                     // received activation
+        }
+      }
+    }
+  } else {
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
   for (int w = 0; w < nsteps; w++) {
     if (lane == 0) DISTIR_COUNT(4);
@@ -329,14 +394,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     for (int q = 0; q < V; q++) {
       const int kk = w - s[q];
       act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      if (act[q]) mem_apply(live[q], peak[q], (kk >> 1) == K - 1 ? ptask1[q] : ptask0[q]);
-      const bool slow = act[q] && !task_fast(clk[q], tc[q]);
-      if (__any_sync(0xffffffffu, slow) && slow) {
-        const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
-                           Seg{row + 2, 14, nb[q]},                   // blocks
-                           Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
-        add_task(clk[q], sg, tc[q]);
-      }
+      task(q, act[q], (kk >> 1) == K - 1);
     }
     double nbv[V], t[V];
     Nbr<V>::up_stage(clk, nbv, lane);
@@ -354,6 +412,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       if (ok[q] && s[q] > 0 && tin[q] >= 0.0) { clk[q] = tin[q]; MEM(q, nde, 0); }
     }
   }
+  }  // wavefront
   double msx = 0.0;
   int64_t pkx = 0;
 #pragma unroll
