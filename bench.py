@@ -45,7 +45,7 @@ ISSUE_PEAK_NOTE = "148 SMs x 4 SMSPs x 32 lanes x 1 instr/clk x sm_max_mhz"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="distir", choices=["distir", "reference"])
     ap.add_argument("--workload", default="W3")
@@ -89,7 +89,7 @@ class ClockSampler:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None

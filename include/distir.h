@@ -264,6 +264,43 @@ distir_status distir_nccl_comm_destroy(void* comm);
 int64_t distir_shard_indices(int64_t n_configs, int32_t rank, int32_t n_ranks,
                              int64_t* out, int64_t cap);
 
+/* ---------------------------------------------- raw-program mode (f3) ----
+ * Simulate arbitrary explicit DistIR programs (straight-line ops,
+ * each on a device set; an op starts when all its devices are free and blocks
+ * them all; values live from creation to last use), e.g. the Fig. 3
+ * traces or hand-written strategies.  All arrays are HOST arrays:
+ *   programs[i]: n_dev devices (1..64); its ops are ops[op_base, op_base +
+ *   n_ops); its values are values[value_base, value_base + n_values); its
+ *   per-device outputs go to clock_out / peak_out[out_base, out_base + n_dev).
+ *   ops[j]: cost in seconds (>= 0); device ids idx[dev_off, dev_off + n_dev),
+ *   input value ids idx[in_off, ...+n_in), output ids idx[out_off, ...+n_out)
+ *   -- ids are local to the program.
+ *   values[v]: device, flags (bit 0 parameter: live from t = 0; bit 1
+ *   returned: never freed), bytes.
+ * Outputs (host; any but makespan_out may be NULL): makespan per program,
+ * final clock and peak live bytes per device, start and end time per op.
+ * Synchronous.  Errors: INVALID_ARG for out-of-range ids/offsets. */
+typedef struct {
+  int32_t n_dev, dev_off, n_in, in_off, n_out, out_off;
+  double cost;
+} distir_raw_op;
+typedef struct {
+  int32_t dev, flags;
+  int64_t bytes;
+} distir_raw_value;
+typedef struct {
+  int32_t n_dev, n_ops, op_base, n_values, value_base, out_base;
+} distir_raw_program;
+
+distir_status distir_raw_workspace_size(int32_t n_programs, int64_t n_ops, int64_t n_idx,
+                                        int64_t n_values, int64_t n_out, size_t* bytes);
+distir_status distir_raw_eval(distir_sim* sim, const distir_raw_program* programs,
+                              int32_t n_programs, const distir_raw_op* ops, int64_t n_ops,
+                              const int32_t* idx, int64_t n_idx, const distir_raw_value* values,
+                              int64_t n_values, int64_t n_out, void* d_workspace, size_t ws_bytes,
+                              double* makespan_out, double* clock_out, int64_t* peak_out,
+                              double* op_start_out, double* op_end_out);
+
 /* Thread-local description of the last error ("" if none). */
 const char* distir_last_error(void);
 

@@ -95,6 +95,22 @@ class distir_stats(ctypes.Structure):
         "n_buckets", "n_items", "h2d_bytes", "d2h_bytes")]
 
 
+class distir_raw_op(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "n_dev", "dev_off", "n_in", "in_off", "n_out", "out_off")] + [
+        ("cost", ctypes.c_double)]
+
+
+class distir_raw_value(ctypes.Structure):
+    _fields_ = [("dev", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("bytes", ctypes.c_int64)]
+
+
+class distir_raw_program(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "n_dev", "n_ops", "op_base", "n_values", "value_base", "out_base")]
+
+
 TOPK_DTYPE = np.dtype([("index", "<i8"), ("makespan_s", "<f8"),
                        ("throughput", "<f8"), ("peak_bytes", "<i8")])
 
@@ -108,7 +124,8 @@ EXPORTS = ("distir_sim_create", "distir_sim_destroy", "distir_grid_size",
            "distir_grid_launch", "distir_last_stats", "distir_profile",
            "distir_grid_eval_sharded", "distir_nccl_unique_id",
            "distir_nccl_comm_init", "distir_nccl_comm_destroy",
-           "distir_shard_indices", "distir_last_error", "distir_version")
+           "distir_shard_indices", "distir_raw_workspace_size",
+           "distir_raw_eval", "distir_last_error", "distir_version")
 
 
 class DistirError(RuntimeError):
@@ -148,6 +165,10 @@ def _load():
     L.distir_nccl_comm_init.argtypes = [ctypes.c_char_p, i32, i32, i32, P(vp)]
     L.distir_nccl_comm_destroy.argtypes = [vp]
     L.distir_shard_indices.argtypes = [i64, i32, i32, P(i64), i64]
+    L.distir_raw_workspace_size.argtypes = [i32, i64, i64, i64, i64, P(ctypes.c_size_t)]
+    L.distir_raw_eval.argtypes = [vp, P(distir_raw_program), i32, P(distir_raw_op), i64,
+                                  P(i32), i64, P(distir_raw_value), i64, i64, vp,
+                                  ctypes.c_size_t, vp, vp, vp, vp, vp]
     L.distir_shard_indices.restype = i64
     for f in EXPORTS:
         if f not in ("distir_sim_destroy", "distir_last_error", "distir_version",
@@ -360,6 +381,58 @@ class Simulator:
             _ptr(outs["peak"]) if per_config else None,
             _ptr(outs["reason"]) if per_config else None,
             _ptr(outs["topk"]), _ptr(outs["ntopk"])))
+
+    # -- raw-program mode (f3)
+    def eval_raw(self, programs, per_op=True):
+        """Simulate explicit programs on the GPU.  programs: list of
+        (n_dev, ops, values) with ops = [(devs, cost, ins, outs), ...] and
+        values = [(dev, bytes, is_param, is_returned), ...] (ids local to the
+        program).  Returns a list of dicts (makespan, clocks, peak, start,
+        end)."""
+        progs = (distir_raw_program * max(len(programs), 1))()
+        ops_l, idx, vals = [], [], []
+        out_base = 0
+        for p, (n_dev, ops, values) in enumerate(programs):
+            progs[p] = distir_raw_program(n_dev, len(ops), len(ops_l), len(values),
+                                          len(vals), out_base)
+            out_base += n_dev
+            for op in ops:
+                devs, cost = op[0], op[1]
+                ins = op[2] if len(op) > 2 else []
+                outs = op[3] if len(op) > 3 else []
+                rec = (len(devs), len(idx), len(ins), len(idx) + len(devs), len(outs),
+                       len(idx) + len(devs) + len(ins), float(cost))
+                idx.extend(list(devs) + list(ins) + list(outs))
+                ops_l.append(rec)
+            for v in values:
+                vals.append((int(v[0]), (1 if v[2] else 0) | (2 if v[3] else 0), int(v[1])))
+        n_ops, n_idx, n_vals = len(ops_l), len(idx), len(vals)
+        ops_a = (distir_raw_op * max(n_ops, 1))(*[distir_raw_op(*r) for r in ops_l])
+        idx_a = (ctypes.c_int32 * max(n_idx, 1))(*idx)
+        vals_a = (distir_raw_value * max(n_vals, 1))(*[distir_raw_value(*v) for v in vals])
+        b = ctypes.c_size_t()
+        _check(lib.distir_raw_workspace_size(len(programs), n_ops, n_idx, n_vals, out_base,
+                                             ctypes.byref(b)))
+        ws = self.torch.empty(b.value, dtype=self.torch.uint8, device=self.device)
+        ms = np.zeros(max(len(programs), 1))
+        clk = np.zeros(max(out_base, 1))
+        pk = np.zeros(max(out_base, 1), dtype=np.int64)
+        st = np.zeros(max(n_ops, 1))
+        en = np.zeros(max(n_ops, 1))
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        _check(lib.distir_raw_eval(self.handle, progs, len(programs), ops_a, n_ops, idx_a,
+                                   n_idx, vals_a, n_vals, out_base,
+                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(), vp(ms), vp(clk),
+                                   vp(pk), vp(st) if per_op else None,
+                                   vp(en) if per_op else None))
+        res = []
+        for p, (n_dev, ops, values) in enumerate(programs):
+            o, ob = progs[p].op_base, progs[p].out_base
+            res.append(dict(makespan=ms[p], clocks=clk[ob:ob + n_dev].copy(),
+                            peak=pk[ob:ob + n_dev].copy(),
+                            start=st[o:o + len(ops)].copy() if per_op else None,
+                            end=en[o:o + len(ops)].copy() if per_op else None))
+        return res
 
     def profile(self, enable=True):
         """Kernel times (ms) accumulated since the previous call; then turn

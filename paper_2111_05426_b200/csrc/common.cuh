@@ -113,3 +113,19 @@ struct TopkRec {         // == distir_topk_entry
 };
 
 }  // namespace distir
+
+namespace distir {
+// ----------------------------------------------------- raw programs (f3) ----
+struct RawOp {           // == distir_raw_op (32 bytes)
+  int32_t n_dev, dev_off, n_in, in_off, n_out, out_off;
+  double cost;
+};
+struct RawValue {        // == distir_raw_value (16 bytes)
+  int32_t dev, flags;    // flags: bit0 parameter, bit1 returned
+  int64_t bytes;
+};
+struct RawProgram {      // == distir_raw_program (24 bytes)
+  int32_t n_dev, n_ops, op_base, n_values, value_base, out_base;
+};
+constexpr int kRawMaxDev = 64;
+}  // namespace distir

@@ -20,11 +20,15 @@
 
 #include "../../include/distir.h"
 #include "kernels.cuh"
+#include "raw.cuh"
 
 using namespace distir;
 
 static_assert(sizeof(distir_topk_entry) == sizeof(TopkRec), "top-k record layout");
 static_assert(sizeof(distir_config) == sizeof(DExplicit), "config layout");
+static_assert(sizeof(distir_raw_op) == sizeof(RawOp), "raw op layout");
+static_assert(sizeof(distir_raw_value) == sizeof(RawValue), "raw value layout");
+static_assert(sizeof(distir_raw_program) == sizeof(RawProgram), "raw program layout");
 
 namespace {
 
@@ -854,6 +858,117 @@ int distir_debug_counters(unsigned long long* out, int n) {
   return 0;
 }
 #endif
+
+// ---------------------------------------------------------- raw programs --
+namespace {
+struct RawLayout {
+  size_t progs, ops, idx, vals, lu, ms, clk, pk, st, en, total;
+};
+RawLayout raw_layout(int64_t np, int64_t no, int64_t ni, int64_t nv, int64_t nout) {
+  RawLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~size_t(255); return o; };
+  auto n1 = [](int64_t x) { return (size_t)(x > 0 ? x : 1); };
+  L.progs = take(n1(np) * sizeof(RawProgram));
+  L.ops = take(n1(no) * sizeof(RawOp));
+  L.idx = take(n1(ni) * 4);
+  L.vals = take(n1(nv) * sizeof(RawValue));
+  L.lu = take(n1(nv) * 4);
+  L.ms = take(n1(np) * 8);
+  L.clk = take(n1(nout) * 8);
+  L.pk = take(n1(nout) * 8);
+  L.st = take(n1(no) * 8);
+  L.en = take(n1(no) * 8);
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+distir_status distir_raw_workspace_size(int32_t n_programs, int64_t n_ops, int64_t n_idx,
+                                        int64_t n_values, int64_t n_out, size_t* bytes) {
+  g_err.clear();
+  if (!bytes || n_programs < 0 || n_ops < 0 || n_idx < 0 || n_values < 0 || n_out < 0)
+    return fail(DISTIR_E_INVALID_ARG, "sizes / bytes");
+  *bytes = raw_layout(n_programs, n_ops, n_idx, n_values, n_out).total;
+  return DISTIR_OK;
+}
+
+distir_status distir_raw_eval(distir_sim* sim, const distir_raw_program* programs,
+                              int32_t n_programs, const distir_raw_op* ops, int64_t n_ops,
+                              const int32_t* idx, int64_t n_idx, const distir_raw_value* values,
+                              int64_t n_values, int64_t n_out, void* d_workspace, size_t ws_bytes,
+                              double* makespan_out, double* clock_out, int64_t* peak_out,
+                              double* op_start_out, double* op_end_out) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (n_programs < 0 || (n_programs > 0 && (!programs || !makespan_out)))
+    return fail(DISTIR_E_INVALID_ARG, "programs / makespan_out");
+  if ((op_start_out == nullptr) != (op_end_out == nullptr))
+    return fail(DISTIR_E_INVALID_ARG, "op_start_out and op_end_out go together");
+  // validate every id and offset (host)
+  for (int32_t p = 0; p < n_programs; p++) {
+    const distir_raw_program& pr = programs[p];
+    auto bad = [&](const char* w) {
+      return fail(DISTIR_E_INVALID_ARG, "program " + std::to_string(p) + ": " + w);
+    };
+    if (pr.n_dev < 1 || pr.n_dev > kRawMaxDev) return bad("n_dev in [1, 64]");
+    if (pr.n_ops < 0 || pr.op_base < 0 || (int64_t)pr.op_base + pr.n_ops > n_ops) return bad("op range");
+    if (pr.n_values < 0 || pr.value_base < 0 || (int64_t)pr.value_base + pr.n_values > n_values)
+      return bad("value range");
+    if (pr.out_base < 0 || (int64_t)pr.out_base + pr.n_dev > n_out) return bad("out range");
+    for (int32_t v = 0; v < pr.n_values; v++) {
+      const distir_raw_value& x = values[pr.value_base + v];
+      if (x.dev < 0 || x.dev >= pr.n_dev || x.bytes < 0) return bad("value device / bytes");
+    }
+    for (int32_t i = 0; i < pr.n_ops; i++) {
+      const distir_raw_op& o = ops[pr.op_base + i];
+      if (!(o.cost >= 0.0) || std::isinf(o.cost)) return bad("op cost must be finite and >= 0");
+      if (o.n_dev < 1 || o.n_in < 0 || o.n_out < 0) return bad("op counts");
+      if (o.dev_off < 0 || (int64_t)o.dev_off + o.n_dev > n_idx || o.in_off < 0 ||
+          (int64_t)o.in_off + o.n_in > n_idx || o.out_off < 0 || (int64_t)o.out_off + o.n_out > n_idx)
+        return bad("op index range");
+      for (int j = 0; j < o.n_dev; j++)
+        if (idx[o.dev_off + j] < 0 || idx[o.dev_off + j] >= pr.n_dev) return bad("op device id");
+      for (int j = 0; j < o.n_in; j++)
+        if (idx[o.in_off + j] < 0 || idx[o.in_off + j] >= pr.n_values) return bad("op input id");
+      for (int j = 0; j < o.n_out; j++)
+        if (idx[o.out_off + j] < 0 || idx[o.out_off + j] >= pr.n_values) return bad("op output id");
+    }
+  }
+  const RawLayout L = raw_layout(n_programs, n_ops, n_idx, n_values, n_out);
+  if ((s = check_ws(d_workspace, ws_bytes, L.total)) != DISTIR_OK) return s;
+  if (n_programs == 0) return DISTIR_OK;
+  CUDA_TRY(cudaSetDevice(sim->device));
+  cudaStream_t st = sim->stream;
+  void* ws = d_workspace;
+  CUDA_TRY(cudaMemcpyAsync(at<void>(ws, L.progs), programs, n_programs * sizeof(RawProgram),
+                           cudaMemcpyHostToDevice, st));
+  if (n_ops)
+    CUDA_TRY(cudaMemcpyAsync(at<void>(ws, L.ops), ops, n_ops * sizeof(RawOp), cudaMemcpyHostToDevice, st));
+  if (n_idx)
+    CUDA_TRY(cudaMemcpyAsync(at<void>(ws, L.idx), idx, n_idx * 4, cudaMemcpyHostToDevice, st));
+  if (n_values)
+    CUDA_TRY(cudaMemcpyAsync(at<void>(ws, L.vals), values, n_values * sizeof(RawValue),
+                             cudaMemcpyHostToDevice, st));
+  k_raw_eval<<<(n_programs + 127) / 128, 128, 0, st>>>(
+      at<RawProgram>(ws, L.progs), n_programs, at<RawOp>(ws, L.ops), at<int32_t>(ws, L.idx),
+      at<RawValue>(ws, L.vals), at<int32_t>(ws, L.lu), at<double>(ws, L.ms),
+      clock_out ? at<double>(ws, L.clk) : nullptr, peak_out ? at<int64_t>(ws, L.pk) : nullptr,
+      op_start_out ? at<double>(ws, L.st) : nullptr, op_end_out ? at<double>(ws, L.en) : nullptr);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(makespan_out, at<double>(ws, L.ms), n_programs * 8, cudaMemcpyDeviceToHost, st));
+  if (clock_out && n_out)
+    CUDA_TRY(cudaMemcpyAsync(clock_out, at<double>(ws, L.clk), n_out * 8, cudaMemcpyDeviceToHost, st));
+  if (peak_out && n_out)
+    CUDA_TRY(cudaMemcpyAsync(peak_out, at<int64_t>(ws, L.pk), n_out * 8, cudaMemcpyDeviceToHost, st));
+  if (op_start_out && n_ops) {
+    CUDA_TRY(cudaMemcpyAsync(op_start_out, at<double>(ws, L.st), n_ops * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(op_end_out, at<double>(ws, L.en), n_ops * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DISTIR_OK;
+}
 
 int64_t distir_shard_indices(int64_t n_configs, int32_t rank, int32_t n_ranks, int64_t* out,
                              int64_t cap) {
