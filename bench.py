@@ -64,6 +64,14 @@ def bench_grid(name, n_gpus):
     return g
 
 
+def bench_config(name, grid, n_total, k, n_gpus):
+    return {"workload": "%s: %s x %s, %d configs" % (
+        name, "+".join(grid["models"]) or "synthetic", "+".join(grid["topos"]), n_total),
+        "configs": n_total, "k": k, "l2_flush": "256 MiB memset between steps",
+        "parallelism": ("round-robin config shards x %d GPUs, NCCL all-gather of top-k"
+                        % n_gpus) if n_gpus > 1 else "1 GPU"}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -188,7 +196,7 @@ def run_reference(args):
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": args.workload + " (oracle: %d seeded configs per step)" % per},
+           "config": bench_config(args.workload, grid, n, args.k, args.gpus),
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                             "sample": "%d configs/step x %d steps of %s, 1 thread"
                                       % (per, args.steps, args.workload)},
@@ -314,12 +322,7 @@ def main():
             "steps": K, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "%s: %s x %s, %d configs" % (
-                args.workload, "+".join(grid["models"]) or "synthetic",
-                "+".join(grid["topos"]), n_total),
-                "configs": n_total, "k": k, "l2_flush": "256 MiB memset between steps",
-                "parallelism": "round-robin config shards x %d GPUs, NCCL all-gather "
-                               "of top-k" % n_gpus if n_gpus > 1 else "1 GPU"},
+            "config": bench_config(args.workload, grid, n_total, k, n_gpus),
             "configs_per_s": n_total / (ms_step / 1e3),
             "time_to_best_ms": e2e_ms,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": issue_peak,
