@@ -43,6 +43,7 @@ struct Model {          // workloads/ model dict, in this order
   int64_t kind;         // 0 MLP training, 1 GPT-2 inference
   int64_t n_layer, d_model, n_head, seq_len, vocab_pad, n_ctx;
   int64_t dtype_bytes, id_bytes, lm_head;
+  int64_t schedule;     // MLP training pipeline schedule: 0 GPipe, 1 1F1B
 };
 struct Topo {
   int64_t world_max, node_size, capacity;
@@ -53,7 +54,7 @@ Model model_from(const int64_t* f) {
   Model m;
   m.kind = f[0]; m.n_layer = f[1]; m.d_model = f[2]; m.n_head = f[3];
   m.seq_len = f[4]; m.vocab_pad = f[5]; m.n_ctx = f[6]; m.dtype_bytes = f[7];
-  m.id_bytes = f[8]; m.lm_head = f[9];
+  m.id_bytes = f[8]; m.lm_head = f[9]; m.schedule = f[10];
   return m;
 }
 Topo topo_from(const int64_t* i, const double* d) {
@@ -170,97 +171,166 @@ Program build_mlp(const Model& M, const Cfg& c) {
   auto act = [&](int64_t k, int r, int64_t l) -> int& { return acts[(k * W + r) * (L + 1) + l]; };
   std::vector<int> fwd_recv(K * W, -1), bwd_recv(K * W, -1);
 
-  // Forward: for k, for s ascending (GPipe, microbatch-major; C.3).
-  for (int64_t k = 0; k < K; k++) {
-    for (int64_t s = 0; s < P; s++) {
-      std::vector<int> R = stage_ranks(s);
-      for (int r : R) act(k, r, lo(s)) = (s == 0) ? X[r * K + k] : fwd_recv[k * W + r];
-      for (int64_t l = lo(s); l < lo(s + 1); l++) {
-        std::vector<int> Z(W, -1);
-        for (int r : R) {
-          Z[r] = pr.new_val(r, m * n_out(l) * e);
-          emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l]}, {Z[r]}, 2 * m * k_in(l) * n_out(l));
-        }
-        if (mode(l) == ROW) {  // partial sums -> TP AllReduce over (i, *, s)
-          for (int64_t i = 0; i < D; i++) {
-            std::vector<int> g, in, out;
-            for (int64_t j = 0; j < T; j++) {
-              int r = (int)rank_of(c, i, j, s);
-              int z2 = pr.new_val(r, m * d * e);
-              g.push_back(r); in.push_back(Z[r]); out.push_back(z2); Z[r] = z2;
-            }
-            emit(ALLREDUCE, g, in, out, m * d * e);
+  // ---- the four kinds of pipeline events of one microbatch k on stage s
+  auto fwd_task = [&](int64_t k, int64_t s) {        // MatMul, [TP AllReduce], Relu
+    std::vector<int> R = stage_ranks(s);
+    for (int r : R) act(k, r, lo(s)) = (s == 0) ? X[r * K + k] : fwd_recv[k * W + r];
+    for (int64_t l = lo(s); l < lo(s + 1); l++) {
+      std::vector<int> Z(W, -1);
+      for (int r : R) {
+        Z[r] = pr.new_val(r, m * n_out(l) * e);
+        emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l]}, {Z[r]}, 2 * m * k_in(l) * n_out(l));
+      }
+      if (mode(l) == ROW) {  // partial sums -> TP AllReduce over (i, *, s)
+        for (int64_t i = 0; i < D; i++) {
+          std::vector<int> g, in, out;
+          for (int64_t j = 0; j < T; j++) {
+            int r = (int)rank_of(c, i, j, s);
+            int z2 = pr.new_val(r, m * d * e);
+            g.push_back(r); in.push_back(Z[r]); out.push_back(z2); Z[r] = z2;
           }
-        }
-        for (int r : R) {
-          int a = pr.new_val(r, m * d_out(l) * e);
-          emit(COMPUTE, {r}, {Z[r]}, {a}, m * d_out(l));  // Relu
-          act(k, r, l + 1) = a;
+          emit(ALLREDUCE, g, in, out, m * d * e);
         }
       }
-      if (s < P - 1) {
-        for (int r : R) {
-          int dst = r + (int)(T * D);
-          int64_t bytes = m * d_out(lo(s + 1) - 1) * e;
-          int v = pr.new_val(dst, bytes);
-          emit(SEND, {r, dst}, {act(k, r, lo(s + 1))}, {v}, bytes);
-          fwd_recv[k * W + dst] = v;
+      for (int r : R) {
+        int a = pr.new_val(r, m * d_out(l) * e);
+        emit(COMPUTE, {r}, {Z[r]}, {a}, m * d_out(l));  // Relu
+        act(k, r, l + 1) = a;
+      }
+    }
+  };
+  auto fwd_send = [&](int64_t k, int64_t s) {        // stage s -> s+1
+    for (int r : stage_ranks(s)) {
+      int dst = r + (int)(T * D);
+      int64_t bytes = m * d_out(lo(s + 1) - 1) * e;
+      int v = pr.new_val(dst, bytes);
+      emit(SEND, {r, dst}, {act(k, r, lo(s + 1))}, {v}, bytes);
+      fwd_recv[k * W + dst] = v;
+    }
+  };
+  std::vector<int> Gcur = Gv;
+  std::vector<int> bwd_out(K * W, -1);                // dA leaving stage s (first layer)
+  auto bwd_task = [&](int64_t k, int64_t s) {        // [LossGrad], per layer desc
+    std::vector<int> R = stage_ranks(s);
+    std::vector<int> dA(W, -1);
+    for (int r : R) {
+      if (s == P - 1) {  // LossGrad (MSE gradient, C.9 A22)
+        dA[r] = pr.new_val(r, m * d_out(L - 1) * e);
+        emit(COMPUTE, {r}, {act(k, r, L), Y[r * K + k]}, {dA[r]}, 3 * m * d_out(L - 1));
+      } else {
+        dA[r] = bwd_recv[k * W + r];
+      }
+    }
+    for (int64_t l = lo(s + 1) - 1; l >= lo(s); l--) {
+      std::vector<int> dZ(W, -1), dW(W, -1);
+      for (int r : R) {  // ReluGrad
+        dZ[r] = pr.new_val(r, m * d_out(l) * e);
+        emit(COMPUTE, {r}, {act(k, r, l + 1), dA[r]}, {dZ[r]}, m * d_out(l));
+      }
+      for (int r : R) {  // MatMulGrad -> (dA_l, dW_l)
+        int da = pr.new_val(r, m * k_in(l) * e);
+        dW[r] = pr.new_val(r, k_in(l) * n_out(l) * e);
+        emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l], dZ[r]}, {da, dW[r]},
+             4 * m * k_in(l) * n_out(l));
+        dA[r] = da;
+      }
+      if (mode(l) == COL) {  // partial dA_l (m x d) -> TP AllReduce
+        for (int64_t i = 0; i < D; i++) {
+          std::vector<int> g, in, out;
+          for (int64_t j = 0; j < T; j++) {
+            int r = (int)rank_of(c, i, j, s);
+            int v = pr.new_val(r, m * d * e);
+            g.push_back(r); in.push_back(dA[r]); out.push_back(v); dA[r] = v;
+          }
+          emit(ALLREDUCE, g, in, out, m * d * e);
+        }
+      }
+      for (int r : R) {  // gradient accumulation (C.9 A20)
+        int gn = pr.new_val(r, k_in(l) * n_out(l) * e);
+        emit(COMPUTE, {r}, {Gcur[r * L + l], dW[r]}, {gn}, k_in(l) * n_out(l));
+        Gcur[r * L + l] = gn;
+      }
+    }
+    for (int r : R) bwd_out[k * W + r] = dA[r];
+  };
+  auto bwd_send = [&](int64_t k, int64_t s) {        // stage s -> s-1
+    for (int r : stage_ranks(s)) {
+      int dst = r - (int)(T * D);
+      int64_t bytes = m * k_in(lo(s)) * e;
+      int v = pr.new_val(dst, bytes);
+      emit(SEND, {r, dst}, {bwd_out[k * W + r]}, {v}, bytes);
+      bwd_recv[k * W + dst] = v;
+    }
+  };
+
+  if (M.schedule == 0) {
+    // GPipe (north_star; C.3): all forwards microbatch-major, then all
+    // backwards.
+    for (int64_t k = 0; k < K; k++)
+      for (int64_t s = 0; s < P; s++) {
+        fwd_task(k, s);
+        if (s < P - 1) fwd_send(k, s);
+      }
+    for (int64_t k = 0; k < K; k++)
+      for (int64_t s = P - 1; s >= 0; s--) {
+        bwd_task(k, s);
+        if (s > 0) bwd_send(k, s);
+      }
+  } else {
+    // Synchronous 1F1B (PipeDream-flush): stage s runs w_s =
+    // min(P-1-s, K) warm-up forwards, then alternates F(w_s + i), B(i), then
+    // the remaining backwards.  The global program order (DESIGN reading R6)
+    // is the order of the unit-time schedule of these per-stage sequences
+    // (F and B take one unit, a task waits for its stage and for its
+    // producer on the neighbour stage): ops sorted by time, each Send at the
+    // time its producer finishes, Sends before tasks at equal times, Sends by
+    // lower stage of the pair then forward-before-backward, tasks by stage.
+    // For P = K = 2 this is exactly the program of Fig. 2/3.
+    struct Ev { int64_t t; int cls; int64_t key, kind, k, s; };
+    std::vector<std::vector<std::pair<int, int64_t>>> seq(P);   // (0 = F / 1 = B, k)
+    for (int64_t s = 0; s < P; s++) {
+      const int64_t w = std::min<int64_t>(P - 1 - s, K);
+      for (int64_t k = 0; k < w; k++) seq[s].push_back({0, k});
+      for (int64_t i = 0; i < K - w; i++) { seq[s].push_back({0, w + i}); seq[s].push_back({1, i}); }
+      for (int64_t k = K - w; k < K; k++) seq[s].push_back({1, k});
+    }
+    // unit-time schedule by relaxation over the per-stage sequences
+    std::vector<int64_t> endF(K * P, -1), endB(K * P, -1);
+    std::vector<Ev> ev;
+    std::vector<size_t> ptr(P, 0);
+    std::vector<int64_t> freeT(P, 0);
+    bool progress = true;
+    while (progress) {
+      progress = false;
+      for (int64_t s = 0; s < P; s++) {
+        while (ptr[s] < seq[s].size()) {
+          const int kind = seq[s][ptr[s]].first;
+          const int64_t k = seq[s][ptr[s]].second;
+          int64_t dep = 0;
+          if (kind == 0 && s > 0) { if (endF[k * P + s - 1] < 0) break; dep = endF[k * P + s - 1]; }
+          if (kind == 1 && s < P - 1) { if (endB[k * P + s + 1] < 0) break; dep = endB[k * P + s + 1]; }
+          const int64_t st = std::max(freeT[s], dep);
+          (kind == 0 ? endF : endB)[k * P + s] = st + 1;
+          freeT[s] = st + 1;
+          ev.push_back(Ev{st, 1, s, kind, k, s});                       // the task
+          if (kind == 0 && s < P - 1) ev.push_back(Ev{st + 1, 0, s, 0, k, s});      // F send
+          if (kind == 1 && s > 0) ev.push_back(Ev{st + 1, 0, s - 1, 1, k, s});      // B send
+          ptr[s]++;
+          progress = true;
         }
       }
     }
-  }
-  // Backward: for k, for s descending.
-  std::vector<int> Gcur = Gv;
-  for (int64_t k = 0; k < K; k++) {
-    for (int64_t s = P - 1; s >= 0; s--) {
-      std::vector<int> R = stage_ranks(s);
-      std::vector<int> dA(W, -1);
-      for (int r : R) {
-        if (s == P - 1) {  // LossGrad (MSE gradient, C.9 A22)
-          dA[r] = pr.new_val(r, m * d_out(L - 1) * e);
-          emit(COMPUTE, {r}, {act(k, r, L), Y[r * K + k]}, {dA[r]}, 3 * m * d_out(L - 1));
-        } else {
-          dA[r] = bwd_recv[k * W + r];
-        }
-      }
-      for (int64_t l = lo(s + 1) - 1; l >= lo(s); l--) {
-        std::vector<int> dZ(W, -1), dW(W, -1);
-        for (int r : R) {  // ReluGrad
-          dZ[r] = pr.new_val(r, m * d_out(l) * e);
-          emit(COMPUTE, {r}, {act(k, r, l + 1), dA[r]}, {dZ[r]}, m * d_out(l));
-        }
-        for (int r : R) {  // MatMulGrad -> (dA_l, dW_l)
-          int da = pr.new_val(r, m * k_in(l) * e);
-          dW[r] = pr.new_val(r, k_in(l) * n_out(l) * e);
-          emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l], dZ[r]}, {da, dW[r]},
-               4 * m * k_in(l) * n_out(l));
-          dA[r] = da;
-        }
-        if (mode(l) == COL) {  // partial dA_l (m x d) -> TP AllReduce
-          for (int64_t i = 0; i < D; i++) {
-            std::vector<int> g, in, out;
-            for (int64_t j = 0; j < T; j++) {
-              int r = (int)rank_of(c, i, j, s);
-              int v = pr.new_val(r, m * d * e);
-              g.push_back(r); in.push_back(dA[r]); out.push_back(v); dA[r] = v;
-            }
-            emit(ALLREDUCE, g, in, out, m * d * e);
-          }
-        }
-        for (int r : R) {  // gradient accumulation (C.9 A20)
-          int gn = pr.new_val(r, k_in(l) * n_out(l) * e);
-          emit(COMPUTE, {r}, {Gcur[r * L + l], dW[r]}, {gn}, k_in(l) * n_out(l));
-          Gcur[r * L + l] = gn;
-        }
-      }
-      if (s > 0) {
-        for (int r : R) {
-          int dst = r - (int)(T * D);
-          int64_t bytes = m * k_in(lo(s)) * e;
-          int v = pr.new_val(dst, bytes);
-          emit(SEND, {r, dst}, {dA[r]}, {v}, bytes);
-          bwd_recv[k * W + dst] = v;
-        }
+    std::stable_sort(ev.begin(), ev.end(), [](const Ev& x, const Ev& y) {
+      if (x.t != y.t) return x.t < y.t;
+      if (x.cls != y.cls) return x.cls < y.cls;
+      if (x.key != y.key) return x.key < y.key;
+      return x.kind < y.kind;
+    });
+    for (const Ev& v : ev) {
+      if (v.cls == 1) {
+        if (v.kind == 0) fwd_task(v.k, v.s); else bwd_task(v.k, v.s);
+      } else {
+        if (v.kind == 0) fwd_send(v.k, v.s); else bwd_send(v.k, v.s);
       }
     }
   }
@@ -621,10 +691,10 @@ Decoded synth(const Spec& sp, int64_t index) {
   Model M;
   static const int64_t HF[4][3] = {{12, 768, 12}, {24, 1024, 16}, {36, 1280, 20}, {48, 1600, 25}};
   if (kind == 0) {
-    M = Model{0, int64_t(1) << (1 + r[5] % 6), int64_t(1) << (8 + r[6] % 7), 1, 1, 0, 0, 2, 8, 0};
+    M = Model{0, int64_t(1) << (1 + r[5] % 6), int64_t(1) << (8 + r[6] % 7), 1, 1, 0, 0, 2, 8, 0, 0};
   } else {
     const int64_t* hf = HF[r[5] % 4];
-    M = Model{1, hf[0], hf[1], hf[2], 8, 50304, 1024, 2, 8, 1};
+    M = Model{1, hf[0], hf[1], hf[2], 8, 50304, 1024, 2, 8, 1, 0};
   }
   dc.M = M;
   dc.model_slot = -1;
@@ -666,7 +736,7 @@ Spec spec_from(int32_t n_model_table, const int64_t* model_table,
   // hdr: n_models, n_topos, n_world, n_batch, n_k, k_mode, dp_mask, tp_mask,
   //      pp_mask, synth_seed, synth_count; lists: the lists concatenated.
   Spec sp;
-  for (int i = 0; i < n_model_table; i++) sp.models.push_back(model_from(model_table + 10 * i));
+  for (int i = 0; i < n_model_table; i++) sp.models.push_back(model_from(model_table + 11 * i));
   for (int i = 0; i < n_topo_table; i++) sp.topos.push_back(topo_from(topo_i + 3 * i, topo_d + 6 * i));
   const int64_t* p = lists;
   sp.model_ids.assign(p, p + hdr[0]); p += hdr[0];
@@ -807,7 +877,7 @@ int64_t oracle_enumerate(int32_t n_model_table, const int64_t* model_table,
                          int32_t n_topo_table, const int64_t* topo_i, const double* topo_d,
                          const int64_t* hdr, const int64_t* lists, int64_t cap,
                          int64_t* fields /* [cap][9]: model_slot, topo_slot, W, D, T, P, K, B, kind */,
-                         int64_t* model_out /* [cap][10] or NULL */) {
+                         int64_t* model_out /* [cap][11] or NULL */) {
   Spec sp = spec_from(n_model_table, model_table, n_topo_table, topo_i, topo_d, hdr, lists);
   std::vector<Decoded> all = enumerate(sp);
   for (int64_t i = 0; i < (int64_t)all.size() && i < cap; i++) {
@@ -817,9 +887,10 @@ int64_t oracle_enumerate(int32_t n_model_table, const int64_t* model_table,
     f[3] = dc.c.D; f[4] = dc.c.T; f[5] = dc.c.P; f[6] = dc.c.K; f[7] = dc.c.B; f[8] = dc.M.kind;
     if (model_out) {
       const Model& M = dc.M;
-      int64_t* mo = model_out + 10 * i;
+      int64_t* mo = model_out + 11 * i;
       mo[0] = M.kind; mo[1] = M.n_layer; mo[2] = M.d_model; mo[3] = M.n_head; mo[4] = M.seq_len;
       mo[5] = M.vocab_pad; mo[6] = M.n_ctx; mo[7] = M.dtype_bytes; mo[8] = M.id_bytes; mo[9] = M.lm_head;
+      mo[10] = M.schedule;
     }
   }
   return (int64_t)all.size();

@@ -32,10 +32,16 @@ GPT2_INFER = 1
 # bytes, lm_head flag.
 # ----------------------------------------------------------------------------
 
-def mlp(n_layer, d_model, dtype_bytes=2):
+GPIPE = 0
+ONE_F_ONE_B = 1
+
+
+def mlp(n_layer, d_model, dtype_bytes=2, schedule=GPIPE):
+    """schedule: the pipeline schedule of the training transform -- GPipe
+    (north_star) or the paper's synchronous 1F1B (NEXT row f1)."""
     return dict(kind=MLP_TRAIN, n_layer=n_layer, d_model=d_model, n_head=1,
                 seq_len=1, vocab_pad=0, n_ctx=0, dtype_bytes=dtype_bytes,
-                id_bytes=8, lm_head=0)
+                id_bytes=8, lm_head=0, schedule=schedule)
 
 
 def gpt2(n_layer, d_model, n_head, seq_len=8, vocab_pad=50304, n_ctx=1024,
@@ -43,7 +49,7 @@ def gpt2(n_layer, d_model, n_head, seq_len=8, vocab_pad=50304, n_ctx=1024,
     return dict(kind=GPT2_INFER, n_layer=n_layer, d_model=d_model,
                 n_head=n_head, seq_len=seq_len, vocab_pad=vocab_pad,
                 n_ctx=n_ctx, dtype_bytes=dtype_bytes, id_bytes=8,
-                lm_head=lm_head)
+                lm_head=lm_head, schedule=GPIPE)
 
 
 MODELS = {
@@ -55,6 +61,10 @@ MODELS = {
     "mlp_103b": mlp(96, 32768),
     # W4 deep-pipeline stress (BASELINE configs[3]).
     "mlp_w4": mlp(64, 8192),
+    # the paper's own pipeline schedule (1F1B; NEXT row f1)
+    "mlp_w1_1f1b": mlp(2, 64, schedule=1),
+    "mlp_1b_1f1b": mlp(16, 8192, schedule=1),
+    "mlp_w4_1f1b": mlp(64, 8192, schedule=1),
     # HF GPT-2 family (W3, BASELINE configs[2]).
     "gpt2_small": gpt2(12, 768, 12),
     "gpt2_medium": gpt2(24, 1024, 16),
