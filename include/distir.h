@@ -79,11 +79,16 @@ enum {
 /* A model (Table 1).  MLP: n_layer square bias-free layers of
  * width d_model; GPT-2: HF shapes with seq_len tokens per sample, a
  * padded vocabulary and an optional LM head.  dtype_bytes = 2 (16-bit values,
- * P:543); id_bytes = bytes per token id.  Unused fields are ignored. */
+ * P:543); id_bytes = bytes per token id.  schedule (MLP training only): the
+ * pipeline schedule of the D/T/P transform, DISTIR_SCHED_GPIPE (north_star)
+ * or DISTIR_SCHED_1F1B (the paper's synchronous 1F1B; P <= 32).
+ * Unused fields are ignored. */
+enum { DISTIR_SCHED_GPIPE = 0, DISTIR_SCHED_1F1B = 1 };
 typedef struct {
   int32_t kind;
   int32_t n_layer, d_model, n_head, seq_len, vocab_pad, n_ctx;
   int32_t dtype_bytes, id_bytes, lm_head;
+  int32_t schedule;
 } distir_model;
 
 /* Hardware description ("GPU DRAM bandwidth, kernel launch overhead,

@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 class distir_model(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
-        "n_ctx", "dtype_bytes", "id_bytes", "lm_head")]
+        "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule")]
 
 
 class distir_topology(ctypes.Structure):
@@ -188,9 +188,9 @@ def _check(status):
 # ------------------------------------------------------ marshalling ---------
 
 def model_struct(m) -> distir_model:
-    return distir_model(*[int(m[k]) for k in (
+    return distir_model(*[int(m.get(k, 0)) for k in (
         "kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
-        "n_ctx", "dtype_bytes", "id_bytes", "lm_head")])
+        "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule")])
 
 
 def topo_struct(t) -> distir_topology:

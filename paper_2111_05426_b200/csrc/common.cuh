@@ -17,12 +17,13 @@ constexpr int kMaxK = 64;           // top-k width
 constexpr int kMaxRanks = 8;        // GPUs merged by the all-gather
 constexpr int kNumBuckets = 4096;   // hash slots for warp-shape buckets
 constexpr int kOverflowBucket = kNumBuckets;  // catch-alls: + kind (1 config / warp)
-constexpr int kBucketSlots = kNumBuckets + 2;
+constexpr int kBucketSlots = kNumBuckets + 3;   // + MLP, GPT-2, MLP-1F1B catch-alls
 // Simulate kernels ("groups"): model kind x schedule mode.  Modes 0-2: one
 // lane walks a whole configuration in program order, P <= 1 / 2 / 4 stages;
 // modes 3-4: wavefront, one lane per stage (mode 4: two stages per lane,
-// 32 < P <= 64, and the catch-all buckets).
-constexpr int kModes = 5;
+// 32 < P <= 64, and the catch-all buckets); mode 5 (MLP only): the 1F1B
+// co-simulation, one lane per stage, P <= 32.
+constexpr int kModes = 6;
 constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
@@ -34,7 +35,7 @@ constexpr int kTopkIPT = 8;         // candidates per thread held in registers
 enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };
 
 struct DModel {          // distir_model, int32
-  int32_t kind, L, d, h, S, V, nctx, e, ide, lm;
+  int32_t kind, L, d, h, S, V, nctx, e, ide, lm, sched;
 };
 
 struct DTopo {           // distir_topology
@@ -69,6 +70,7 @@ struct SpecBlock {
   int64_t n_total;                    // configs of the whole grid
   int32_t rank, n_ranks;              // shard: global i = rank + q * n_ranks
   int64_t n_local;
+  int32_t f1b;                        // any 1F1B model in use (launch mode 5)
   DModel models[kMaxModels];          // handle tables
   DTopo topos[kMaxTopos];
 };

@@ -143,6 +143,7 @@ struct GraphCache {
   void* comm = nullptr;
   int64_t n_local = -1, n_total = -1;
   int32_t mode = -1;
+  int32_t f1b = -1;
 };
 
 struct distir_sim {
@@ -189,6 +190,9 @@ distir_status validate_model(const distir_model& m, int i) {
   if (m.kind != DISTIR_MODEL_MLP_TRAIN && m.kind != DISTIR_MODEL_GPT2_INFER) return bad("kind");
   if (m.n_layer < 1 || m.d_model < 1 || m.dtype_bytes < 1) return bad("n_layer/d_model/dtype_bytes");
   if (m.n_layer > 1024) return fail(DISTIR_E_UNSUPPORTED, "n_layer > 1024");
+  if (m.kind == DISTIR_MODEL_MLP_TRAIN && m.schedule != DISTIR_SCHED_GPIPE &&
+      m.schedule != DISTIR_SCHED_1F1B)
+    return bad("schedule");
   if (m.d_model > (1 << 20)) return fail(DISTIR_E_UNSUPPORTED, "d_model > 2^20");
   if (m.kind == DISTIR_MODEL_GPT2_INFER) {
     if (m.n_head < 1 || m.seq_len < 1 || m.vocab_pad < 1 || m.n_ctx < 0 || m.id_bytes < 1)
@@ -256,10 +260,13 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
   if (g->n_batch < 1 || g->n_batch > 32) return fail(DISTIR_E_INVALID_ARG, "spec.n_batch");
   if (g->n_k < 0 || g->n_k > 16) return fail(DISTIR_E_INVALID_ARG, "spec.n_k");
   if (g->k_mode != 0 && g->k_mode != 1) return fail(DISTIR_E_INVALID_ARG, "spec.k_mode");
+  bool any_1f1b = false;
+  for (int mi = 0; mi < g->n_models; mi++) any_1f1b |= sim->models[g->models[mi]].sched == 1;
   for (int i = 0; i < g->n_world; i++) {
     if (!is_pow2(g->world[i]) || (i && g->world[i] <= g->world[i - 1]))
       return fail(DISTIR_E_INVALID_ARG, "spec.world: ascending powers of two");
     if (g->world[i] > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
+    if (any_1f1b && g->world[i] > 32) return fail(DISTIR_E_UNSUPPORTED, "1F1B with world size > 32");
   }
   for (int i = 0; i < g->n_batch; i++) {
     if (g->batch[i] < 1 || (i && g->batch[i] <= g->batch[i - 1]))
@@ -275,6 +282,7 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     if (g->k_set[i] > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
   }
   sp.k_mode = g->k_mode;
+  sp.f1b = any_1f1b ? 1 : 0;
   sp.n_k = g->n_k;
   for (int i = 0; i < g->n_k; i++) sp.k_set[i] = g->k_set[i];
   sp.n_batch = g->n_batch;
@@ -314,6 +322,8 @@ distir_status validate_configs(const distir_sim* sim, const distir_config* cf, i
     if (!is_pow2(c.dp) || !is_pow2(c.tp))
       return fail(DISTIR_E_UNSUPPORTED, "config dp/tp must be powers of two (stage symmetry)");
     if ((int64_t)c.dp * c.tp * c.pp > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
+    if (sim->models[c.model].sched == 1 && c.pp > 32)
+      return fail(DISTIR_E_UNSUPPORTED, "1F1B with more than 32 stages");
     if (c.microbatches > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
     if (!work_fits(sim->models[c.model], c.batch))
       return fail(DISTIR_E_UNSUPPORTED, "per-op work overflows int64");
@@ -418,8 +428,9 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     kernels += 2;
 #endif
     DISTIR_SIM(0, 3); DISTIR_SIM(0, 4); DISTIR_SIM(1, 3); DISTIR_SIM(1, 4);
-#undef DISTIR_SIM
     kernels += 4;
+    if (sp.f1b) { DISTIR_SIM(0, 5); kernels++; }
+#undef DISTIR_SIM
   }
   CUDA_TRY(mark(2));
   TopkRec* fin = at<TopkRec>(ws, L.fin);
@@ -471,7 +482,7 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
   const bool key_ok = G.exec && G.ws == ws && G.ms == ms && G.pk == pk && G.rs == rs &&
                       G.topk == topk && G.ntopk == ntopk && G.k == k && G.comm == comm &&
                       G.n_local == sim->spec.n_local && G.n_total == sim->spec.n_total &&
-                      G.mode == sim->spec.mode;
+                      G.mode == sim->spec.mode && G.f1b == sim->spec.f1b;
   if (sim->use_graph && !key_ok) {
     if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
     if (G.graph) { cudaGraphDestroy(G.graph); G.graph = nullptr; }
@@ -508,7 +519,7 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
       CUDA_TRY(e);
       G.ws = ws; G.ms = ms; G.pk = pk; G.rs = rs; G.topk = topk; G.ntopk = ntopk; G.k = k;
       G.comm = comm; G.n_local = sim->spec.n_local; G.n_total = sim->spec.n_total;
-      G.mode = sim->spec.mode; G.kernels = kern; G.ev_ring = false;
+      G.mode = sim->spec.mode; G.f1b = sim->spec.f1b; G.kernels = kern; G.ev_ring = false;
     }
   }
   if (sim->use_graph && G.exec) {
@@ -563,6 +574,7 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
     for (size_t i = 0; i < sim->topos.size(); i++) sp.topos[i] = sim->topos[i];
     sp.mode = MODE_EXPLICIT;
     n_total = n_configs;
+    for (int64_t i = 0; i < n_configs && !sp.f1b; i++) sp.f1b = sim->models[configs[i].model].sched;
   }
   sp.n_total = n_total;
   sp.rank = rank;
@@ -632,7 +644,8 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   for (int i = 0; i < n_models; i++) {
     const distir_model& m = models[i];
     sim->models.push_back(DModel{m.kind, m.n_layer, m.d_model, m.n_head, m.seq_len, m.vocab_pad,
-                                 m.n_ctx, m.dtype_bytes, m.id_bytes, m.lm_head});
+                                 m.n_ctx, m.dtype_bytes, m.id_bytes, m.lm_head,
+                                 m.kind == DISTIR_MODEL_MLP_TRAIN ? m.schedule : 0});
   }
   for (int i = 0; i < n_topos; i++) {
     const distir_topology& t = topos[i];
@@ -647,11 +660,11 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   int per_sm[kGroups] = {};
   const void* fns[kGroups] = {
       (const void*)k_simulate<0, 0>, (const void*)k_simulate<0, 1>, (const void*)k_simulate<0, 2>,
-      (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<1, 0>,
-      (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>, (const void*)k_simulate<1, 3>,
-      (const void*)k_simulate<1, 4>};
+      (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<0, 5>,
+      (const void*)k_simulate<1, 0>, (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>,
+      (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr};
   for (int g = 0; g < kGroups && e == cudaSuccess; g++)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], fns[g], sim_tpb(g / kModes, g % kModes), 0);
+    if (fns[g]) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], fns[g], sim_tpb(g / kModes, g % kModes), 0);
   if (e != cudaSuccess) {
     delete sim;
     return fail(DISTIR_E_CUDA, std::string("device setup: ") + cudaGetErrorString(e));

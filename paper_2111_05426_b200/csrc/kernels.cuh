@@ -77,13 +77,13 @@ __device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t 
     c.K = (c.P == 1) ? 1 : (1ll << (1 + r[3] % 5));
     c.B = 1ll << (7 + r[4] % 12);
     if ((r[0] & 1) == 0) {
-      c.M = DModel{0, (int32_t)(1 << (1 + r[5] % 6)), (int32_t)(1 << (8 + r[6] % 7)), 1, 1, 0, 0, 2, 8, 0};
+      c.M = DModel{0, (int32_t)(1 << (1 + r[5] % 6)), (int32_t)(1 << (8 + r[6] % 7)), 1, 1, 0, 0, 2, 8, 0, 0};
     } else {
       const int q = (int)(r[5] % 4);
       const int32_t L = q == 0 ? 12 : q == 1 ? 24 : q == 2 ? 36 : 48;
       const int32_t d = q == 0 ? 768 : q == 1 ? 1024 : q == 2 ? 1280 : 1600;
       const int32_t h = q == 0 ? 12 : q == 1 ? 16 : q == 2 ? 20 : 25;
-      c.M = DModel{1, L, d, h, 8, 50304, 1024, 2, 8, 1};
+      c.M = DModel{1, L, d, h, 8, 50304, 1024, 2, 8, 1, 0};
     }
     c.topo = sp.topo_ids[r[7] % (uint64_t)sp.n_topos];
     return;
@@ -135,7 +135,8 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
 
 __device__ __forceinline__ uint32_t bucket_key(const Cfg& c) {
   const uint32_t K = (uint32_t)(c.K < 255 ? c.K : 255);
-  return (uint32_t)c.M.kind | (uint32_t)(c.P - 1) << 1 | (uint32_t)(c.M.L - 1) << 7 | K << 17;
+  return (uint32_t)c.M.kind | (uint32_t)(c.P - 1) << 1 | (uint32_t)(c.M.L - 1) << 7 | K << 17 |
+         (uint32_t)(c.M.sched & 1) << 25;
 }
 
 // ------------------------------------------------------------ costs (C.5) ---
@@ -248,7 +249,7 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
     ev += events; st += steps; nv += 1;
     const uint32_t key = bucket_key(c);
     uint32_t slot = (key * 2654435761u) >> 20;                 // 12-bit hash
-    uint32_t found = kOverflowBucket + (uint32_t)c.M.kind;
+    uint32_t found = kOverflowBucket + (c.M.sched ? 2u : (uint32_t)c.M.kind);
     for (int probe = 0; probe < kNumBuckets; probe++) {
       const uint32_t sl = (slot + probe) & (kNumBuckets - 1);
       uint32_t cur = *(volatile uint32_t*)&bk[sl].key;
@@ -304,7 +305,9 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
     if (b >= kOverflowBucket) {        // mixed shapes: one config per warp
       lanes = 32;
       cls = kNumClasses - 1;
-      group = (uint32_t)(b - kOverflowBucket) * kModes + 4;
+      // MLP / GPT-2 catch-alls run two stages per lane (any P <= 64); the
+      // 1F1B catch-all (P <= 32 by validation) one stage per lane
+      group = b == kOverflowBucket + 2 ? 5 : (uint32_t)(b - kOverflowBucket) * kModes + 4;
     } else {
       const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, K = (B.key >> 17) & 255;
       uint32_t mode;
@@ -315,7 +318,7 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
         est = (unsigned long long)K * P * (kind ? 1ull : 2ull);
       } else {
         lanes = P < 32 ? pow2ceil32(P) : 32;
-        mode = P > 32 ? 4 : 3;
+        mode = (B.key >> 25) & 1 ? 5 : P > 32 ? 4 : 3;
         est = (2ull * K + P) * (kind ? 1ull : 2ull) * 2;
       }
       cls = 63 - __clzll(est + 1);
@@ -379,7 +382,7 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
 // Persistent simulate kernel for one group (model kind x stages per lane):
 // each warp pulls work items of its group, heaviest weight class first.
 __host__ __device__ constexpr int sim_v(int mode) {
-  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : mode == 3 ? 1 : 2;
+  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : mode == 4 ? 2 : 1;
 }
 __host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per lane row
   return kind == 1 ? 19 + 6 * sim_v(mode) : 15 + 14 * sim_v(mode);
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE)) k_simulate(const SpecBloc
     if (has) {
       decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);
     } else {
-      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0};
+      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0};
       c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
     }
     const DTopo& tp = sp.topos[c.topo];
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE)) k_simulate(const SpecBloc
     const long long t0 = clock64();
 #endif
     if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, ms, pk);
-    else run_mlp<V, SEQ>(c, tp, has, sl, S, lane, row, ms, pk);
+    else run_mlp<V, SEQ, MODE == 5>(c, tp, has, sl, S, lane, row, ms, pk);
 #ifdef DISTIR_INSTR
     if (lane == 0) {
       const unsigned long long dt = (unsigned long long)(clock64() - t0);

@@ -33,7 +33,7 @@ __device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, in
   a = Seg{row + oa, na, n1 & 1};
 }
 
-template <int V, bool SEQ>
+template <int V, bool SEQ, bool F1B>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                         double* row, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
@@ -131,7 +131,91 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       add_task(clk[q], sg, cb[q]);
     }
   };
-  if constexpr (SEQ) {
+  if constexpr (F1B) {
+    static_assert(V == 1 && !SEQ, "1F1B: one stage per lane");
+    // (validation keeps 1F1B configurations at P <= 32)
+    // ---- synchronous 1F1B (NEXT row f1).  Stage s's ops are the
+    // PipeDream-flush sequence (w = min(P-1-s, K) warm-up forwards, then
+    // F(w+i), B(i) pairs, then the remaining backwards) interleaved with its
+    // Sends in the order of the unit-time schedule (DESIGN reading R6): in
+    // that schedule F(k, s) starts at s + k (k <= w) or 2k + s, B(k, s) at
+    // 2P - 1 - s + 2k, and a Send happens when its producer finishes; Sends
+    // precede tasks at equal times, then by lower stage, forward first.  The
+    // warp co-simulates the stages (lane = stage): a lane whose next event is
+    // a task runs it; a Send runs when both ends have it next (rendezvous,
+    // P:119).  This is exactly the per-device order of the oracle's program.
+    const int st = s[0];
+    const int Pi = (int)P, Ki = (int)K;
+    const int w = Pi - 1 - st < Ki ? Pi - 1 - st : Ki;
+    auto fstart = [&](int k, int ss) {
+      const int ww = Pi - 1 - ss < Ki ? Pi - 1 - ss : Ki;
+      return k <= ww ? ss + k : 2 * k + ss;
+    };
+    // event key: ((t * 2 + cls) * 64 + lower) * 2 + kind; cls 0 = Send
+    auto key = [](int t, int cls, int lower, int kind) -> int64_t {
+      return (((int64_t)t * 2 + cls) * 64 + lower) * 2 + kind;
+    };
+    constexpr int64_t kDone = INT64_MAX;
+    int jt = 0, ka_in = 0, ka_out = 0, kg_out = 0, kg_in = 0;
+    const int n_tasks = ok[0] ? 2 * Ki : 0;
+    // every iteration runs >= 1 event of each configuration (its globally
+    // first one); the guard only bounds a broken schedule
+    const int max_iter = warp_max_int(has ? 4 * Pi * Ki + 64 : 0);
+    for (int iter = 0; iter < max_iter; iter++) {
+      // next event of each stream of this stage
+      int64_t best = kDone;
+      int which = -1;                  // 0 task, 1 recvA, 2 sendA, 3 sendG, 4 recvG
+      int tkind = 0, tk = 0;
+      if (jt < n_tasks) {
+        if (jt < w) { tkind = 0; tk = jt; }
+        else if (jt < 2 * Ki - w) { const int jj = jt - w; tkind = jj & 1; tk = (jj >> 1) + (tkind ? 0 : w); }
+        else { tkind = 1; tk = jt - Ki; }
+        const int t = tkind ? 2 * Pi - 1 - st + 2 * tk : fstart(tk, st);
+        best = key(t, 1, st, tkind);
+        which = 0;
+      }
+      if (ok[0] && st > 0 && ka_in < Ki) {
+        const int64_t k2 = key(fstart(ka_in, st - 1) + 1, 0, st - 1, 0);
+        if (k2 < best) { best = k2; which = 1; }
+      }
+      if (ok[0] && st < Pi - 1 && ka_out < Ki) {
+        const int64_t k2 = key(fstart(ka_out, st) + 1, 0, st, 0);
+        if (k2 < best) { best = k2; which = 2; }
+      }
+      if (ok[0] && st > 0 && kg_out < Ki) {
+        const int64_t k2 = key(2 * Pi - st + 2 * kg_out, 0, st - 1, 1);
+        if (k2 < best) { best = k2; which = 3; }
+      }
+      if (ok[0] && st < Pi - 1 && kg_in < Ki) {
+        const int64_t k2 = key(2 * Pi - (st + 1) + 2 * kg_in, 0, st, 1);
+        if (k2 < best) { best = k2; which = 4; }
+      }
+      if (!__any_sync(0xffffffffu, which >= 0)) break;
+      // rendezvous identity (lower stage, direction, microbatch); -1 = none
+      const int my_id = which == 1 ? ((st - 1) << 14 | ka_in)
+                      : which == 2 ? (st << 14 | ka_out)
+                      : which == 3 ? ((st - 1) << 14 | 1 << 13 | kg_out)
+                      : which == 4 ? (st << 14 | 1 << 13 | kg_in) : -1;
+      const int up_id = __shfl_down_sync(0xffffffffu, my_id, 1);
+      const int dn_id = __shfl_up_sync(0xffffffffu, my_id, 1);
+      const double up_c = __shfl_down_sync(0xffffffffu, clk[0], 1);
+      const double dn_c = __shfl_up_sync(0xffffffffu, clk[0], 1);
+      fwd_task(0, which == 0 && tkind == 0);                   // all lanes call both:
+      bwd_task(0, which == 0 && tkind == 1);                   // warp-uniform votes
+      if (which == 0) jt++;
+      const bool down_link = which == 1 || which == 3;         // partner s - 1
+      const bool ready = which > 0 && (down_link ? (sl > 0 && dn_id == my_id)
+                                                 : (sl < S - 1 && up_id == my_id));
+      if (ready) {
+        const double other = down_link ? dn_c : up_c;
+        clk[0] = dadd(fmax(clk[0], other), down_link ? sendb[0] : sendf[0]);
+        if (which == 1) { MEM(0, m * kin[lo[0] & 1] * e, 0); ka_in++; }        // recv act
+        else if (which == 2) { ka_out++; }                                    // send act
+        else if (which == 3) { live[0] -= m * kin[lo[0] & 1] * e; kg_out++; } // send grad
+        else { MEM(0, m * dout[(hi[0] - 1) & 1] * e, 0); kg_in++; }           // recv grad
+      }
+    }
+  } else if constexpr (SEQ) {
     // ---- program order (one lane owns all P <= V stages)
     const int K_ = warp_max_int(has ? (int)K : 0);
     for (int k = 0; k < K_; k++) {
