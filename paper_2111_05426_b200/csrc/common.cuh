@@ -26,6 +26,10 @@ constexpr int kBucketSlots = kNumBuckets + 3;   // + MLP, GPT-2, MLP-1F1B catch-
 constexpr int kModes = 6;
 constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
+constexpr int kMaxSplit = 5;        // configs per item divided by up to 2^5
+struct PlanBudget {                 // resident warps of each simulate kernel
+  uint32_t warps[kGroups];
+};
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
 constexpr int kTopkBlocks = 1024;   // max partial top-k blocks
@@ -94,7 +98,8 @@ struct Bucket {          // per hash slot (plus one overflow slot)
   uint32_t cfg_base;     // first position in perm
   uint32_t item_base;    // first work item
   uint32_t cursor;       // scatter cursor
-  uint32_t lanes;        // lanes per config S (power of two <= 32)
+  uint16_t lanes;        // lanes per config S (power of two <= 32)
+  uint16_t cpw;          // configs per work item (<= 32 / lanes)
   uint16_t cls;          // weight class
   uint16_t group;        // simulate kernel: kind * kModes + mode
   uint32_t item_off;     // offset within (group, class)

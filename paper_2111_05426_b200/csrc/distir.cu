@@ -407,7 +407,9 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   if (n > 0) {
     const int eg = (int)std::min<int64_t>((n + 255) / 256, sim->enum_grid);
     k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, hdr);
-    k_plan<<<1, 1024, 0, st>>>(bk, hdr);
+    PlanBudget pb;
+    for (int g = 0; g < kGroups; g++) pb.warps[g] = (uint32_t)sim->sim_grid[g] * (sim_tpb(g / kModes, g % kModes) / 32);
+    k_plan<<<1, 1024, 0, st>>>(bk, hdr, pb);
     k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, perm, items);
     kernels += 3;
   }

@@ -35,6 +35,16 @@ __device__ __forceinline__ void distir_count(int i) {
   if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));
 }
 #define DISTIR_COUNT(i) NV_IF_TARGET(NV_IS_DEVICE, (distir_count(i);))
+// warp-level timing of the divergent slow path: [9] cycles, [10] entries
+#define DISTIR_SLOW_T0 const long long slow_t0_ = clock64();
+#define DISTIR_SLOW_T1(any)                                                   \
+  if ((any) && (threadIdx.x & 31) == 0) {                                    \
+    atomicAdd(&g_distir_instr[9], (unsigned long long)(clock64() - slow_t0_)); \
+    atomicAdd(&g_distir_instr[10], 1ull);                                     \
+  }
+#else
+#define DISTIR_SLOW_T0
+#define DISTIR_SLOW_T1(any)
 #endif
 #include "common.cuh"
 #include "exact_add.cuh"
@@ -289,13 +299,22 @@ __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
 
 // One block: lanes per config, simulate kernel (group), work items numbered
 // group-major and heaviest weight class first within a group (LPT order for
-// the persistent simulate kernels), config ranges.
-__global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
+// the persistent simulate kernels), config ranges.  Configurations of one
+// warp diverge whenever one of them crosses a binade (exact_add.cuh), so a
+// warp's time grows with the configs it holds: while a simulate kernel has
+// more resident warps than items, the heaviest classes are split into items
+// of fewer configurations (cpw halved per step, heaviest class first).
+__global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, PlanBudget budget) {
   __shared__ unsigned int s_items[kGroups][kNumClasses];
+  __shared__ unsigned int s_alt[kGroups][kNumClasses][kMaxSplit + 1];   // items at split j
+  __shared__ unsigned char s_shift[kGroups][kNumClasses];
   __shared__ unsigned int s_base[kGroups][kNumClasses];
   __shared__ unsigned int s_cfg, s_nb;
-  for (int c = threadIdx.x; c < kGroups * kNumClasses; c += blockDim.x)
+  for (int c = threadIdx.x; c < kGroups * kNumClasses; c += blockDim.x) {
     s_items[c / kNumClasses][c % kNumClasses] = 0;
+    s_shift[c / kNumClasses][c % kNumClasses] = 0;
+    for (int j = 0; j <= kMaxSplit; j++) s_alt[c / kNumClasses][c % kNumClasses][j] = 0;
+  }
   if (threadIdx.x == 0) { s_cfg = 0; s_nb = 0; }
   __syncthreads();
   for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
@@ -325,15 +344,41 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr) {
       if (cls >= kNumClasses) cls = kNumClasses - 1;
       group = kind * kModes + mode;
     }
-    const uint32_t cpw = 32 / lanes;
-    const uint32_t items = (B.count + cpw - 1) / cpw;
-    B.lanes = lanes;
+    B.lanes = (uint16_t)lanes;
     B.cls = (uint16_t)cls;
     B.group = (uint16_t)group;
-    B.item_off = atomicAdd(&s_items[group][cls], items);
+    const uint32_t cpw = 32 / lanes;
+    for (int j = 0; j <= kMaxSplit; j++) {
+      const uint32_t cj = (cpw >> j) ? (cpw >> j) : 1u;
+      atomicAdd(&s_alt[group][cls][j], (B.count + cj - 1) / cj);
+    }
     B.cfg_base = atomicAdd(&s_cfg, B.count);
     B.cursor = 0;
     atomicAdd(&s_nb, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kGroups) {         // split heavy classes while warps are idle
+    const int g = threadIdx.x;
+    unsigned int total = 0;
+    for (int c = 0; c < kNumClasses; c++) total += s_alt[g][c][0];
+    for (int c = kNumClasses - 1; c >= 0; c--) {
+      int j = 0;
+      while (j < kMaxSplit && total - s_alt[g][c][j] + s_alt[g][c][j + 1] <= budget.warps[g]) {
+        total = total - s_alt[g][c][j] + s_alt[g][c][j + 1];
+        j++;
+      }
+      s_shift[g][c] = (unsigned char)j;
+      if (j < kMaxSplit && s_alt[g][c][j] != s_alt[g][c][j + 1]) break;   // budget reached
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
+    Bucket& B = bk[b];
+    if (B.count == 0) continue;
+    const uint32_t cpw0 = 32u / B.lanes, sh = s_shift[B.group][B.cls];
+    const uint32_t cpw = (cpw0 >> sh) ? (cpw0 >> sh) : 1u;
+    B.cpw = (uint16_t)cpw;
+    B.item_off = atomicAdd(&s_items[B.group][B.cls], (B.count + cpw - 1) / cpw);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -365,7 +410,7 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
     const uint32_t b = cfg_bucket[q];
     if (b == kEmptyKey) continue;
     const uint32_t pos = atomicAdd(&bk[b].cursor, 1u);
-    const uint32_t cpw = 32 / bk[b].lanes;
+    const uint32_t cpw = bk[b].cpw;
     perm[bk[b].cfg_base + pos] = (uint32_t)q;
     if (pos % cpw == 0) {
       const uint32_t cnt = bk[b].count;

@@ -115,21 +115,27 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   auto fwd_task = [&](int q, bool act) {
     if (act) mem_apply(live[q], peak[q], pf[q]);
     const bool slow = act && !task_fast(clk[q], cf[q]);
-    if (__any_sync(0xffffffffu, slow) && slow) {
+    DISTIR_SLOW_T0
+    const bool any = __any_sync(0xffffffffu, slow);
+    if (any && slow) {
       Seg sg[3];
       alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
       add_task(clk[q], sg, cf[q]);
     }
+    DISTIR_SLOW_T1(any)
   };
   auto bwd_task = [&](int q, bool act) {
     if (act) mem_apply(live[q], peak[q], pb[q]);
     const bool slow = act && !task_fast(clk[q], cb[q]);
-    if (__any_sync(0xffffffffu, slow) && slow) {
+    DISTIR_SLOW_T0
+    const bool any = __any_sync(0xffffffffu, slow);
+    if (any && slow) {
       Seg sg[4];                                               // LossGrad, layers desc
       sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
       alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
       add_task(clk[q], sg, cb[q]);
     }
+    DISTIR_SLOW_T1(any)
   };
   if constexpr (F1B) {
     static_assert(V == 1 && !SEQ, "1F1B: one stage per lane");
@@ -445,12 +451,15 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   auto task = [&](int q, bool act, bool last) {
     if (act) mem_apply(live[q], peak[q], last ? ptask1[q] : ptask0[q]);
     const bool slow = act && !task_fast(clk[q], tc[q]);
-    if (__any_sync(0xffffffffu, slow) && slow) {
+    DISTIR_SLOW_T0
+    const bool any = __any_sync(0xffffffffu, slow);
+    if (any && slow) {
       const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
                          Seg{row + 2, 14, nb[q]},                   // blocks
                          Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
       add_task(clk[q], sg, tc[q]);
     }
+    DISTIR_SLOW_T1(any)
   };
   if constexpr (SEQ) {
     // ---- program order (one lane owns all P <= V stages)

@@ -11,7 +11,8 @@ import workloads as W
 import paper_2111_05426_b200 as pkg
 from paper_2111_05426_b200 import Simulator
 
-NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles"]
+NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles",
+         "slow_cycles", "slow_entries"]
 
 
 def counters():
@@ -26,6 +27,8 @@ def main():
     mi = {n: i for i, n in enumerate(names)}
     tb = list(W.TOPOLOGIES).index("TB200")
     cases = [("xl P2 K128", None, [(mi["gpt2_xl"], tb, 8, 1, 2, 128, 1 << 20)]),
+             ("xl P16 K128", None, [(mi["gpt2_xl"], tb, 1, 1, 16, 128, 1 << 20)]),
+             ("mlp1b P2 K128", None, [(mi["mlp_1b"], tb, 8, 1, 2, 128, 1 << 18)]),
              ("16x xl P2 K128", None, [(mi["gpt2_xl"], tb, 8, 1, 2, 128, 1 << e) for e in range(7, 21)])]
     cases += [(g, W.GRIDS[g], None) for g in ["W3", "W2", "W5"]]
     for name, grid, cfgs in cases:
@@ -40,10 +43,11 @@ def main():
         c = counters()
         d = dict(zip(NAMES, c))
         print("%-16s sim %.3f ms  tasks %d fast %.3f refresh/task %.3f plain/task %.3f steps %d "
-              "items %d avg_item_cyc %.0f max_item_cyc %d" % (
+              "items %d avg_item_cyc %.0f max_item_cyc %d slow_cyc/item %.0f slow_entries/item %.1f" % (
                   name, p["ms_simulate"], d["tasks"], d["fast"] / max(d["tasks"], 1),
                   d["refresh"] / max(d["tasks"], 1), d["plain"] / max(d["tasks"], 1), d["steps"],
-                  d["items"], d["item_cycles"] / max(d["items"], 1), d["max_item_cycles"]))
+                  d["items"], d["item_cycles"] / max(d["items"], 1), d["max_item_cycles"],
+                  d["slow_cycles"] / max(d["items"], 1), d["slow_entries"] / max(d["items"], 1)))
 
 
 if __name__ == "__main__":
