@@ -101,7 +101,20 @@ typedef struct {
   double alpha_intra_s, bw_intra_Bps;
   double alpha_inter_s, bw_inter_Bps;
   int64_t capacity_bytes; /* per-GPU memory limit                   */
+  /* Compute-op cost model.  DISTIR_COST_ANALYTIC:
+   * flops / F + o.  DISTIR_COST_REGRESSION: the paper's linear-regression
+   * cost functions, t = (c0 + s_per_flop * flops) + s_per_byte *
+   * bytes, evaluated left to right in binary64 without contraction, where
+   * bytes = the sizes of every tensor the op reads or writes (DESIGN R7);
+   * the mm_* set applies to MatMul-type ops (Gemm, MatMul, MatMulGrad), the
+   * ew_* set to every other compute op.  Coefficients must be finite and
+   * >= 0 (ignored under ANALYTIC).  Communication keeps the alpha-beta forms. */
+  int32_t cost_model;
+  int32_t reserved;       /* must be 0                                      */
+  double mm_c0_s, mm_s_per_flop, mm_s_per_byte;
+  double ew_c0_s, ew_s_per_flop, ew_s_per_byte;
 } distir_topology;
+enum { DISTIR_COST_ANALYTIC = 0, DISTIR_COST_REGRESSION = 1 };
 
 /* One explicit configuration (D, T, P, K; P:567 batch).  model and
  * topo index the arrays given to distir_sim_create. */

@@ -67,12 +67,18 @@ def model_fields(m) -> np.ndarray:
     return np.array([int(m.get(k, 0)) for k in MODEL_KEYS], dtype=np.int64)
 
 
+REGRESSION_KEYS = ("mm_c0_s", "mm_s_per_flop", "mm_s_per_byte",
+                   "ew_c0_s", "ew_s_per_flop", "ew_s_per_byte")
+
+
 def topo_arrays(t):
-    ti = np.array([t["world_max"], t["node_size"], t["capacity_bytes"]],
-                  dtype=np.int64)
+    """Topology -> (int64[4], float64[12]); cost_model 1 selects the paper's
+    regression cost functions (NEXT row f2)."""
+    ti = np.array([t["world_max"], t["node_size"], t["capacity_bytes"],
+                   int(t.get("cost_model", 0))], dtype=np.int64)
     td = np.array([t["flops_per_s"], t["op_overhead_s"], t["alpha_intra_s"],
-                   t["bw_intra_Bps"], t["alpha_inter_s"], t["bw_inter_Bps"]],
-                  dtype=np.float64)
+                   t["bw_intra_Bps"], t["alpha_inter_s"], t["bw_inter_Bps"]] +
+                  [float(t.get(k, 0.0)) for k in REGRESSION_KEYS], dtype=np.float64)
     return ti, td
 
 

@@ -48,6 +48,11 @@ struct Model {          // workloads/ model dict, in this order
 struct Topo {
   int64_t world_max, node_size, capacity;
   double F, o, a_intra, bw_intra, a_inter, bw_inter;
+  // cost model (C.5; NEXT row f2): 0 analytic flops/F + o; 1 the paper's
+  // linear-regression cost functions, t = c0 + c_flop * flops +
+  // c_byte * bytes, one coefficient set for MatMul-type ops, one for the rest
+  int64_t cost_model;
+  double mm_c0, mm_flop, mm_byte, ew_c0, ew_flop, ew_byte;
 };
 
 Model model_from(const int64_t* f) {
@@ -62,6 +67,9 @@ Topo topo_from(const int64_t* i, const double* d) {
   t.world_max = i[0]; t.node_size = i[1]; t.capacity = i[2];
   t.F = d[0]; t.o = d[1]; t.a_intra = d[2]; t.bw_intra = d[3];
   t.a_inter = d[4]; t.bw_inter = d[5];
+  t.cost_model = i[3];
+  t.mm_c0 = d[6]; t.mm_flop = d[7]; t.mm_byte = d[8];
+  t.ew_c0 = d[9]; t.ew_flop = d[10]; t.ew_byte = d[11];
   return t;
 }
 
@@ -82,6 +90,7 @@ struct Op {
   std::vector<int> in, out;
   int64_t work;            // FLOPs (compute) or bytes (communication)
   double cost;             // seconds (C.5)
+  bool mm = false;         // MatMul-type compute op (Gemm / MatMul / MatMulGrad)
 };
 
 struct Program {
@@ -103,7 +112,20 @@ bool intra(const Topo& t, const std::vector<int>& devs) {
   return true;
 }
 
-double op_cost(const Topo& t, const Op& op) {
+double op_cost(const Topo& t, const Program& pr, const Op& op) {
+  if (op.cls == COMPUTE && t.cost_model == 1) {
+    // "linear regression models in terms of the sizes of the
+    // input tensors" for MatMul, analytic-style ones for the rest; the
+    // features are the op's FLOPs and the bytes of every tensor it reads or
+    // writes (its typed inputs and outputs), evaluated left to right.
+    int64_t bytes = 0;
+    for (int v : op.in) bytes += pr.vals[v].bytes;
+    for (int v : op.out) bytes += pr.vals[v].bytes;
+    const double c0 = op.mm ? t.mm_c0 : t.ew_c0;
+    const double cf = op.mm ? t.mm_flop : t.ew_flop;
+    const double cb = op.mm ? t.mm_byte : t.ew_byte;
+    return (c0 + cf * (double)op.work) + cb * (double)bytes;
+  }
   if (op.cls == COMPUTE)  // P:487 "N / f", plus the fixed overhead o
     return ((double)op.work) / t.F + t.o;
   const bool in_node = intra(t, op.devs);
@@ -148,8 +170,8 @@ Program build_mlp(const Model& M, const Cfg& c) {
   };
   auto stage_of = [&](int r) { return (int64_t)r / (D * T); };
   auto emit = [&](Cls cls, std::vector<int> devs, std::vector<int> in,
-                  std::vector<int> out, int64_t work) {
-    pr.ops.push_back(Op{cls, std::move(devs), std::move(in), std::move(out), work, 0.0});
+                  std::vector<int> out, int64_t work, bool mm = false) {
+    pr.ops.push_back(Op{cls, std::move(devs), std::move(in), std::move(out), work, 0.0, mm});
   };
 
   // Parameters (C.3): W_l and a zero gradient buffer G_l per local layer;
@@ -179,7 +201,7 @@ Program build_mlp(const Model& M, const Cfg& c) {
       std::vector<int> Z(W, -1);
       for (int r : R) {
         Z[r] = pr.new_val(r, m * n_out(l) * e);
-        emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l]}, {Z[r]}, 2 * m * k_in(l) * n_out(l));
+        emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l]}, {Z[r]}, 2 * m * k_in(l) * n_out(l), true);
       }
       if (mode(l) == ROW) {  // partial sums -> TP AllReduce over (i, *, s)
         for (int64_t i = 0; i < D; i++) {
@@ -231,7 +253,7 @@ Program build_mlp(const Model& M, const Cfg& c) {
         int da = pr.new_val(r, m * k_in(l) * e);
         dW[r] = pr.new_val(r, k_in(l) * n_out(l) * e);
         emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l], dZ[r]}, {da, dW[r]},
-             4 * m * k_in(l) * n_out(l));
+             4 * m * k_in(l) * n_out(l), true);
         dA[r] = da;
       }
       if (mode(l) == COL) {  // partial dA_l (m x d) -> TP AllReduce
@@ -381,8 +403,8 @@ Program build_gpt2(const Model& M, const Cfg& c) {
   };
   auto stage_of = [&](int r) { return (int64_t)r / (D * T); };
   auto emit = [&](Cls cls, std::vector<int> devs, std::vector<int> in,
-                  std::vector<int> out, int64_t work) {
-    pr.ops.push_back(Op{cls, std::move(devs), std::move(in), std::move(out), work, 0.0});
+                  std::vector<int> out, int64_t work, bool mm = false) {
+    pr.ops.push_back(Op{cls, std::move(devs), std::move(in), std::move(out), work, 0.0, mm});
   };
   // Per-block parameters (Megatron shards; C.4), one value per tensor.
   enum { LN1 = 0, WQKV, BQKV, WPROJ, BPROJ, LN2, WFC1, BFC1, WFC2, BFC2, NPB };
@@ -439,11 +461,11 @@ Program build_gpt2(const Model& M, const Cfg& c) {
         for (int r : R) {  // 2 Gemm QKV (column parallel)
           qkv[r] = pr.new_val(r, n * 3 * dT * e);
           emit(COMPUTE, {r}, {h1[r], bpar(r, l, WQKV), bpar(r, l, BQKV)}, {qkv[r]},
-               2 * n * d * (3 * dT) + n * (3 * dT));
+               2 * n * d * (3 * dT) + n * (3 * dT), true);
         }
         for (int r : R) {  // 3 attention scores
           sc[r] = pr.new_val(r, m * hT * S * S * e);
-          emit(COMPUTE, {r}, {qkv[r]}, {sc[r]}, 2 * m * S * S * dT);
+          emit(COMPUTE, {r}, {qkv[r]}, {sc[r]}, 2 * m * S * S * dT, true);
         }
         for (int r : R) {  // 4 softmax
           pb[r] = pr.new_val(r, m * hT * S * S * e);
@@ -451,12 +473,12 @@ Program build_gpt2(const Model& M, const Cfg& c) {
         }
         for (int r : R) {  // 5 attention context
           ctx[r] = pr.new_val(r, n * dT * e);
-          emit(COMPUTE, {r}, {pb[r], qkv[r]}, {ctx[r]}, 2 * m * S * S * dT);
+          emit(COMPUTE, {r}, {pb[r], qkv[r]}, {ctx[r]}, 2 * m * S * S * dT, true);
         }
         for (int r : R) {  // 6 Gemm proj (row parallel) -> partial
           o[r] = pr.new_val(r, n * d * e);
           emit(COMPUTE, {r}, {ctx[r], bpar(r, l, WPROJ), bpar(r, l, BPROJ)}, {o[r]},
-               2 * n * dT * d + n * d);
+               2 * n * dT * d + n * d, true);
         }
         if (T > 1) tp_allreduce(s, o, n * d * e);  // 7
         for (int r : R) {  // 8 residual add
@@ -470,7 +492,7 @@ Program build_gpt2(const Model& M, const Cfg& c) {
         for (int r : R) {  // 10 Gemm FC1 (column parallel)
           f[r] = pr.new_val(r, n * 4 * dT * e);
           emit(COMPUTE, {r}, {h2[r], bpar(r, l, WFC1), bpar(r, l, BFC1)}, {f[r]},
-               2 * n * d * (4 * dT) + n * (4 * dT));
+               2 * n * d * (4 * dT) + n * (4 * dT), true);
         }
         for (int r : R) {  // 11 GeLU
           g[r] = pr.new_val(r, n * 4 * dT * e);
@@ -479,7 +501,7 @@ Program build_gpt2(const Model& M, const Cfg& c) {
         for (int r : R) {  // 12 Gemm FC2 (row parallel) -> partial
           f2[r] = pr.new_val(r, n * d * e);
           emit(COMPUTE, {r}, {g[r], bpar(r, l, WFC2), bpar(r, l, BFC2)}, {f2[r]},
-               2 * n * (4 * dT) * d + n * d);
+               2 * n * (4 * dT) * d + n * d, true);
         }
         if (T > 1) tp_allreduce(s, f2, n * d * e);  // 13
         for (int r : R) {  // 14 residual add
@@ -497,7 +519,7 @@ Program build_gpt2(const Model& M, const Cfg& c) {
         if (M.lm_head) {
           for (int r : R) {  // vocab-parallel LM head (tied wte shard)
             int lg = pr.new_val(r, n * VT * e, false, T == 1);
-            emit(COMPUTE, {r}, {x[r], wte_last[r]}, {lg}, 2 * n * d * VT);
+            emit(COMPUTE, {r}, {x[r], wte_last[r]}, {lg}, 2 * n * d * VT, true);
             x[r] = lg;
           }
           if (T > 1) {  // gather the logits on every TP rank
@@ -621,7 +643,7 @@ Result eval_config(const Model& M, const Topo& t, const Cfg& c,
   Result res{std::numeric_limits<double>::infinity(), -1, validity(M, t, c), 0};
   if (res.reason) return res;
   Program pr = (M.kind == 0) ? build_mlp(M, c) : build_gpt2(M, c);
-  for (Op& op : pr.ops) op.cost = op_cost(t, op);
+  for (Op& op : pr.ops) op.cost = op_cost(t, pr, op);
   SimOut so = simulate(pr);
   if (err && (!so.ready_ok || !so.placement_ok)) *err = 1;
   res.makespan = so.makespan;
@@ -737,7 +759,7 @@ Spec spec_from(int32_t n_model_table, const int64_t* model_table,
   //      pp_mask, synth_seed, synth_count; lists: the lists concatenated.
   Spec sp;
   for (int i = 0; i < n_model_table; i++) sp.models.push_back(model_from(model_table + 11 * i));
-  for (int i = 0; i < n_topo_table; i++) sp.topos.push_back(topo_from(topo_i + 3 * i, topo_d + 6 * i));
+  for (int i = 0; i < n_topo_table; i++) sp.topos.push_back(topo_from(topo_i + 4 * i, topo_d + 12 * i));
   const int64_t* p = lists;
   sp.model_ids.assign(p, p + hdr[0]); p += hdr[0];
   sp.topo_ids.assign(p, p + hdr[1]); p += hdr[1];
@@ -821,7 +843,7 @@ int64_t oracle_program_ops(const int64_t* model, const int64_t* topo_i, const do
   Cfg c{D, T, P, K, B};
   if (validity(M, t, c) & ~(uint32_t)R_CAPACITY) return -1;
   Program pr = (M.kind == 0) ? build_mlp(M, c) : build_gpt2(M, c);
-  for (Op& op : pr.ops) op.cost = op_cost(t, op);
+  for (Op& op : pr.ops) op.cost = op_cost(t, pr, op);
   std::vector<double> st, en;
   simulate(pr, &st, &en);
   int64_t n = (int64_t)pr.ops.size();
@@ -848,7 +870,7 @@ int oracle_export_program(const int64_t* model, const int64_t* topo_i, const dou
   Cfg c{D, T, P, K, B};
   if (validity(M, t, c) & ~(uint32_t)R_CAPACITY) return -1;
   Program pr = (M.kind == 0) ? build_mlp(M, c) : build_gpt2(M, c);
-  for (Op& op : pr.ops) op.cost = op_cost(t, op);
+  for (Op& op : pr.ops) op.cost = op_cost(t, pr, op);
   int64_t nd = 0, ni = 0, no = 0;
   for (const Op& op : pr.ops) { nd += op.devs.size(); ni += op.in.size(); no += op.out.size(); }
   const bool fill = value_dev != nullptr;

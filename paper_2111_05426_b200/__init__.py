@@ -55,7 +55,11 @@ class distir_topology(ctypes.Structure):
                 ("bw_intra_Bps", ctypes.c_double),
                 ("alpha_inter_s", ctypes.c_double),
                 ("bw_inter_Bps", ctypes.c_double),
-                ("capacity_bytes", ctypes.c_int64)]
+                ("capacity_bytes", ctypes.c_int64),
+                ("cost_model", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("mm_c0_s", ctypes.c_double), ("mm_s_per_flop", ctypes.c_double),
+                ("mm_s_per_byte", ctypes.c_double), ("ew_c0_s", ctypes.c_double),
+                ("ew_s_per_flop", ctypes.c_double), ("ew_s_per_byte", ctypes.c_double)]
 
 
 class distir_config(ctypes.Structure):
@@ -198,7 +202,10 @@ def topo_struct(t) -> distir_topology:
                            float(t["flops_per_s"]), float(t["op_overhead_s"]),
                            float(t["alpha_intra_s"]), float(t["bw_intra_Bps"]),
                            float(t["alpha_inter_s"]), float(t["bw_inter_Bps"]),
-                           int(t["capacity_bytes"]))
+                           int(t["capacity_bytes"]), int(t.get("cost_model", 0)), 0,
+                           *[float(t.get(k, 0.0)) for k in (
+                               "mm_c0_s", "mm_s_per_flop", "mm_s_per_byte",
+                               "ew_c0_s", "ew_s_per_flop", "ew_s_per_byte")])
 
 
 def spec_struct(grid, model_index, topo_index) -> distir_grid_spec:

@@ -46,6 +46,8 @@ struct DTopo {           // distir_topology
   int32_t world_max, node_size;
   double F, o, a_intra, bw_intra, a_inter, bw_inter;
   int64_t capacity;
+  int32_t cost_model;    // 0 analytic, 1 regression
+  double mm_c0, mm_flop, mm_byte, ew_c0, ew_flop, ew_byte;
 };
 
 struct DEntry {          // one (D, T, P) triple of the grid, canonical order

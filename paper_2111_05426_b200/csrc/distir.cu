@@ -211,6 +211,15 @@ distir_status validate_topo(const distir_topology& t, int i) {
   if (!(t.op_overhead_s >= 0) || !(t.alpha_intra_s >= 0) || !(t.alpha_inter_s >= 0))
     return bad("overheads");
   if (t.capacity_bytes < 0) return bad("capacity");
+  if (t.cost_model != DISTIR_COST_ANALYTIC && t.cost_model != DISTIR_COST_REGRESSION)
+    return bad("cost_model");
+  if (t.reserved != 0) return bad("reserved");
+  if (t.cost_model == DISTIR_COST_REGRESSION) {
+    const double cs[6] = {t.mm_c0_s, t.mm_s_per_flop, t.mm_s_per_byte,
+                          t.ew_c0_s, t.ew_s_per_flop, t.ew_s_per_byte};
+    for (double v : cs)
+      if (!(v >= 0) || !(v < INFINITY)) return bad("regression coefficients");
+  }
   return DISTIR_OK;
 }
 
@@ -653,7 +662,8 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
     const distir_topology& t = topos[i];
     sim->topos.push_back(DTopo{t.world_max, t.node_size, t.flops_per_s, t.op_overhead_s,
                                t.alpha_intra_s, t.bw_intra_Bps, t.alpha_inter_s, t.bw_inter_Bps,
-                               t.capacity_bytes});
+                               t.capacity_bytes, t.cost_model, t.mm_c0_s, t.mm_s_per_flop,
+                               t.mm_s_per_byte, t.ew_c0_s, t.ew_s_per_flop, t.ew_s_per_byte});
   }
   sim->device = cuda_device;
   sim->stream = static_cast<cudaStream_t>(cuda_stream);

@@ -154,6 +154,19 @@ __device__ __forceinline__ uint32_t bucket_key(const Cfg& c) {
 __device__ __forceinline__ double cost_compute(int64_t flops, const DTopo& t) {
   return __dadd_rn(__ddiv_rn(__ll2double_rn(flops), t.F), t.o);
 }
+// Compute op with `flops` FLOPs touching `bytes` of tensors (C.5; row f2:
+// the regression form of P:518-520 when the topology selects it).
+__device__ __noinline__ double cost_regression(int64_t flops, int64_t bytes, bool mm, const DTopo& t) {
+  const double c0 = mm ? t.mm_c0 : t.ew_c0, cf = mm ? t.mm_flop : t.ew_flop,
+               cb = mm ? t.mm_byte : t.ew_byte;
+  return __dadd_rn(__dadd_rn(c0, __dmul_rn(cf, __ll2double_rn(flops))),
+                   __dmul_rn(cb, __ll2double_rn(bytes)));
+}
+__device__ __forceinline__ double cost_op(int64_t flops, int64_t bytes, bool mm, const DTopo& t) {
+  // (out of line: keeps the setup's register pressure off the simulate loop)
+  if (t.cost_model == 1) return cost_regression(flops, bytes, mm, t);
+  return cost_compute(flops, t);
+}
 __device__ __forceinline__ bool group_intra(int64_t first, int64_t last, int32_t ns) {
   return first / ns == last / ns;
 }
@@ -437,7 +450,7 @@ __host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per
 }
 
 template <int KIND, int MODE>
-__global__ void __launch_bounds__(sim_tpb(KIND, MODE)) k_simulate(const SpecBlock* __restrict__ spp,
+__global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecBlock* __restrict__ spp,
                                                   const DExplicit* __restrict__ ex,
                                                   const Bucket* __restrict__ bk,
                                                   const Item* __restrict__ items,

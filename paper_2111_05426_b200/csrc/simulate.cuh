@@ -50,17 +50,30 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   const double ar_tp = T > 1 ? cost_allreduce(T, mde, tp_intra, tp) : 0.0;
   const int64_t ar_b = T > 1 ? mde : 0;
   const int64_t dlast = dout[(L - 1) & 1];
-  const double loss = cost_compute(3 * m * dlast, tp);
+  // LossGrad reads act_L and Y_k and writes dA (3 tensors of m x d_last)
+  const double loss = cost_op(3 * m * dlast, 3 * m * dlast * e, false, tp);
   // forward / backward layer op costs (absent collectives are +0.0), in the
-  // lane's row: fwd A [0,3) B [3,6), bwd A [6,10) B [10,14), LossGrad [14]
+  // lane's row: fwd A [0,3) B [3,6), bwd A [6,10) B [10,14), LossGrad [14].
+  // Bytes (regression model, DESIGN R7) = every tensor the op reads/writes:
+  // MatMul act + W + Z; Relu Z + act; ReluGrad act + dA + dZ; MatMulGrad
+  // act + W + dZ + dA + dW; Add G + dW + G'.
   {
-    const double relu_a = cost_compute(m * dout.a, tp), relu_b = cost_compute(m * dout.b, tp);
-    row[0] = cost_compute(2 * m * w0, tp); row[1] = 0.0; row[2] = relu_a;
-    row[3] = cost_compute(2 * m * w1, tp); row[4] = ar_tp; row[5] = relu_b;
-    row[6] = relu_a; row[7] = cost_compute(4 * m * w0, tp); row[8] = ar_tp;
-    row[9] = cost_compute(w0, tp);
-    row[10] = relu_b; row[11] = cost_compute(4 * m * w1, tp); row[12] = 0.0;
-    row[13] = cost_compute(w1, tp);
+    auto mm_f = [&](int64_t ki, int64_t no, int64_t w) {
+      return cost_op(2 * m * w, (m * ki + w + m * no) * e, true, tp);
+    };
+    auto mm_b = [&](int64_t ki, int64_t no, int64_t w) {
+      return cost_op(4 * m * w, (2 * m * ki + 2 * w + m * no) * e, true, tp);
+    };
+    row[0] = mm_f(kin.a, nout.a, w0); row[1] = 0.0;
+    row[2] = cost_op(m * dout.a, 2 * m * dout.a * e, false, tp);
+    row[3] = mm_f(kin.b, nout.b, w1); row[4] = ar_tp;
+    row[5] = cost_op(m * dout.b, 2 * m * dout.b * e, false, tp);
+    row[6] = cost_op(m * dout.a, 3 * m * dout.a * e, false, tp);
+    row[7] = mm_b(kin.a, nout.a, w0); row[8] = ar_tp;
+    row[9] = cost_op(w0, 3 * w0 * e, false, tp);
+    row[10] = cost_op(m * dout.b, 3 * m * dout.b * e, false, tp);
+    row[11] = mm_b(kin.b, nout.b, w1); row[12] = 0.0;
+    row[13] = cost_op(w1, 3 * w1 * e, false, tp);
     row[14] = loss;
   }
   // live-memory profiles of one forward / backward layer (C.7)
@@ -321,7 +334,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   // stage: plain op-by-op walk)
   const Par<double> ardp{D > 1 ? cost_allreduce(D, Wb.a, dp_intra, tp) : 0.0,
                          D > 1 ? cost_allreduce(D, Wb.b, dp_intra, tp) : 0.0};
-  const Par<double> sgd{cost_compute(2 * w0, tp), cost_compute(2 * w1, tp)};
+  const Par<double> sgd{cost_op(2 * w0, 3 * w0 * e, false, tp),     // SGD: W + G -> W'
+                        cost_op(2 * w1, 3 * w1 * e, false, tp)};
 #pragma unroll
   for (int q = 0; q < V; q++) {
     if (!ok[q]) continue;
@@ -361,28 +375,33 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   const int64_t nde = n * d * e;
   // op costs (C.4 work per op); absent collectives are +0.0
   const double c_ar = T > 1 ? cost_allreduce(T, nde, tp_intra, tp) : 0.0;
-  const double c_ln = cost_compute(5 * n * d, tp);
-  const double c_att = cost_compute(2 * m * Sq * Sq * dT, tp);
-  const double c_add = cost_compute(n * d, tp);
+  // Bytes (regression model, DESIGN R7) = every tensor the op reads/writes
+  // (C.4 program: activations, parameters and outputs).
+  const int64_t sc_b = m * hT * Sq * Sq * e, qkv_b = n * 3 * dT * e;
+  const double c_ln = cost_op(5 * n * d, 2 * nde + 2 * d * e, false, tp);
+  const double c_add = cost_op(n * d, 3 * nde, false, tp);
   // the lane's row: prologue [0,2), block [2,16), epilogue [16,19)
-  row[0] = cost_compute(2 * n * d, tp);                                  // Embed
-  row[1] = c_ar;                                                         // TP AllReduce
-  row[2] = c_ln;                                                         // ln_1
-  row[3] = cost_compute(2 * n * d * (3 * dT) + n * (3 * dT), tp);        // QKV
-  row[4] = c_att;                                                        // scores
-  row[5] = cost_compute(5 * m * hT * Sq * Sq, tp);                       // softmax
-  row[6] = c_att;                                                        // context
-  row[7] = cost_compute(2 * n * dT * d + n * d, tp);                     // proj
-  row[8] = c_ar;                                                         // TP AllReduce
-  row[9] = c_add;                                                        // residual
-  row[10] = c_ln;                                                        // ln_2
-  row[11] = cost_compute(2 * n * d * (4 * dT) + n * (4 * dT), tp);       // FC1
-  row[12] = cost_compute(8 * n * (4 * dT), tp);                          // GeLU
-  row[13] = cost_compute(2 * n * (4 * dT) * d + n * d, tp);              // FC2
-  row[14] = c_ar;                                                        // TP AllReduce
-  row[15] = c_add;                                                       // residual
-  row[16] = c_ln;                                                        // ln_f
-  row[17] = lm ? cost_compute(2 * n * d * VT, tp) : 0.0;                 // LM head
+  row[0] = cost_op(2 * n * d, n * ide + VT * d * e + nctx * d * e + nde, false, tp);  // Embed
+  row[1] = c_ar;                                                                     // TP AllReduce
+  row[2] = c_ln;                                                                     // ln_1
+  row[3] = cost_op(2 * n * d * (3 * dT) + n * (3 * dT),
+                   nde + (d * 3 * dT + 3 * dT) * e + qkv_b, true, tp);              // QKV
+  row[4] = cost_op(2 * m * Sq * Sq * dT, qkv_b + sc_b, true, tp);                  // scores
+  row[5] = cost_op(5 * m * hT * Sq * Sq, 2 * sc_b, false, tp);                     // softmax
+  row[6] = cost_op(2 * m * Sq * Sq * dT, sc_b + qkv_b + n * dT * e, true, tp);     // context
+  row[7] = cost_op(2 * n * dT * d + n * d, n * dT * e + (dT * d + d) * e + nde, true, tp);  // proj
+  row[8] = c_ar;                                                                     // TP AllReduce
+  row[9] = c_add;                                                                    // residual
+  row[10] = c_ln;                                                                    // ln_2
+  row[11] = cost_op(2 * n * d * (4 * dT) + n * (4 * dT),
+                    nde + (d * 4 * dT + 4 * dT) * e + n * 4 * dT * e, true, tp);    // FC1
+  row[12] = cost_op(8 * n * (4 * dT), 2 * n * 4 * dT * e, false, tp);              // GeLU
+  row[13] = cost_op(2 * n * (4 * dT) * d + n * d,
+                    n * 4 * dT * e + (4 * dT * d + d) * e + nde, true, tp);         // FC2
+  row[14] = c_ar;                                                                    // TP AllReduce
+  row[15] = c_add;                                                                   // residual
+  row[16] = c_ln;                                                                    // ln_f
+  row[17] = lm ? cost_op(2 * n * d * VT, nde + VT * d * e + n * VT * e, true, tp) : 0.0;  // LM head
   row[18] = (lm && T > 1) ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0;  // AllGather
   // live-memory profiles (C.7), for a normal and for the last microbatch
   // (whose ops free the parameters at their last use)

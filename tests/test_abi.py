@@ -41,7 +41,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(pkg.distir_config) == 32
     assert ctypes.sizeof(pkg.distir_topk_entry) == 32
     assert ctypes.sizeof(pkg.distir_model) == 44
-    assert ctypes.sizeof(pkg.distir_topology) == 64
+    assert ctypes.sizeof(pkg.distir_topology) == 120
     assert pkg.TOPK_DTYPE.itemsize == 32
 
 

@@ -83,11 +83,36 @@ HF_GPT2 = ["gpt2_small", "gpt2_medium", "gpt2_large", "gpt2_xl"]
 # ----------------------------------------------------------------------------
 
 def topo(world_max, node_size, flops, overhead, a_intra, bw_intra, a_inter,
-         bw_inter, capacity):
-    return dict(world_max=world_max, node_size=node_size, flops_per_s=flops,
-                op_overhead_s=overhead, alpha_intra_s=a_intra,
-                bw_intra_Bps=bw_intra, alpha_inter_s=a_inter,
-                bw_inter_Bps=bw_inter, capacity_bytes=capacity)
+         bw_inter, capacity, regression=None):
+    """regression: None (analytic flops/F + o) or the six coefficients of the
+    paper's regression cost functions (NEXT row f2) as a dict
+    with keys mm_c0_s, mm_s_per_flop, mm_s_per_byte, ew_c0_s, ew_s_per_flop,
+    ew_s_per_byte."""
+    t = dict(world_max=world_max, node_size=node_size, flops_per_s=flops,
+             op_overhead_s=overhead, alpha_intra_s=a_intra,
+             bw_intra_Bps=bw_intra, alpha_inter_s=a_inter,
+             bw_inter_Bps=bw_inter, capacity_bytes=capacity, cost_model=0)
+    if regression is not None:
+        t["cost_model"] = 1
+        for k in REGRESSION_KEYS:
+            t[k] = float(regression[k])
+    return t
+
+
+REGRESSION_KEYS = ("mm_c0_s", "mm_s_per_flop", "mm_s_per_byte",
+                   "ew_c0_s", "ew_s_per_flop", "ew_s_per_byte")
+
+
+def _load_calibration():
+    """The B200 coefficients fitted by `python -m
+    paper_2111_05426_b200.calibrate` (data file, committed)."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "calib_b200.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
 
 
 TOPOLOGIES = {
@@ -107,6 +132,18 @@ for _i in range(8):
                                    5e-6, _bwx, 180000000000)
 
 TM = ["TM%d" % i for i in range(8)]
+
+# TB200 with the regression cost functions calibrated on a B200 (row f2).
+_CAL = _load_calibration()
+if _CAL is not None:
+    TOPOLOGIES["TB200R"] = topo(64, 8, 1.355e15, 5e-6, 2e-6, 900e9, 5e-6, 50e9,
+                                180000000000, regression=_CAL)
+# A regression topology with dyadic coefficients (exact sums; parity tests).
+TOPOLOGIES["TRD"] = topo(64, 8, 2.0 ** 50, 2.0 ** -18, 2.0 ** -19, 2.0 ** 39,
+                         2.0 ** -17, 2.0 ** 35, 180000000000,
+                         regression=dict(mm_c0_s=2.0 ** -18, mm_s_per_flop=2.0 ** -50,
+                                         mm_s_per_byte=2.0 ** -43, ew_c0_s=2.0 ** -19,
+                                         ew_s_per_flop=2.0 ** -46, ew_s_per_byte=2.0 ** -42))
 
 # ----------------------------------------------------------------------------
 # Grid specifications (SURVEY C.1 enumeration, §8d D.1 workloads).
