@@ -32,9 +32,9 @@ struct PlanBudget {                 // resident warps of each simulate kernel
 };
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
-constexpr int kTopkBlocks = 1024;   // max partial top-k blocks
-constexpr int kTopkThreads = 512;   // threads per partial top-k block
-constexpr int kTopkIPT = 8;         // candidates per thread held in registers
+constexpr int kTopkBlocks = 1024;   // max partial top-k blocks (<= 4 lists per merge thread)
+constexpr int kTopkThreads = 256;   // threads per partial top-k block
+constexpr int kTopkIPT = 2;         // candidates per thread held in registers
 
 enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };
 
@@ -91,7 +91,7 @@ struct WsHeader {
   unsigned long long n_valid;
   unsigned long long n_feasible;
   unsigned int cfg_total;
-  unsigned int pad;
+  unsigned int topk_ticket;           // partial top-k blocks done (last one merges)
 };
 
 struct Bucket {          // per hash slot (plus one overflow slot)

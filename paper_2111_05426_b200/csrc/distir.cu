@@ -452,13 +452,12 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     TopkRec* part = at<TopkRec>(ws, L.part);
     int* part_n = at<int>(ws, L.part_n);
     if (n > 0) {
-      const int64_t per = (int64_t)kTopkThreads * kTopkIPT - kMaxK;
+      const int64_t per = (int64_t)kTopkThreads * kTopkIPT;
       const int nblk = (int)std::min<int64_t>(kTopkBlocks, (n + per - 1) / per);
-      k_topk_partial<<<nblk, kTopkThreads, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n);
-      k_topk_merge<<<1, kTopkThreads, 0, st>>>(part, part_n, nblk, k, k, loc, loc_n);
-      kernels += 2;
+      k_topk<<<nblk, kTopkThreads, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n, hdr, loc, loc_n);
+      kernels++;
     } else {
-      k_topk_merge<<<1, kTopkThreads, 0, st>>>(part, part_n, 0, k, k, loc, loc_n);
+      k_topk_merge<<<1, 32, 0, st>>>(part, part_n, 0, k, k, loc, loc_n);
       kernels++;
     }
   }
@@ -472,7 +471,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     if (r != ncclSuccess)
       return fail(DISTIR_E_NCCL, std::string("ncclAllGather: ") +
                                      (api.getErrorString ? api.getErrorString(r) : "error"));
-    k_topk_merge<<<1, kTopkThreads, 0, st>>>(gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
+    k_topk_merge<<<1, 32, 0, st>>>(gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
     kernels++;
   }
   CUDA_TRY(mark(4));

@@ -562,148 +562,184 @@ __device__ __forceinline__ void cswap(Key& x, Key& y) {                    // x 
   y = sw ? t : y;
 }
 
-// Warp-wide best key (all lanes get it), comparing (a, b, c) only.
-__device__ __forceinline__ Key warp_best(Key k) {
-  for (int o = 16; o > 0; o >>= 1) {
-    Key x;
-    x.a = __shfl_xor_sync(0xffffffffu, k.a, o);
-    x.b = __shfl_xor_sync(0xffffffffu, k.b, o);
-    x.c = __shfl_xor_sync(0xffffffffu, k.c, o);
-    if (better(x, k)) { k.a = x.a; k.b = x.b; k.c = x.c; }
+// Lane holding the warp's best key by (a, b, c), or -1 when no lane holds a
+// candidate (a == 0).  Lexicographic max over the six 32-bit words with
+// warp reductions (REDUX) and ballots; stops at the first word that leaves
+// a single lane (keys are unique: c holds the index).
+__device__ __forceinline__ int warp_best_lane(const Key& k) {
+  const uint32_t wd[6] = {(uint32_t)(k.a >> 32), (uint32_t)k.a, (uint32_t)(k.b >> 32),
+                          (uint32_t)k.b, (uint32_t)(k.c >> 32), (uint32_t)k.c};
+  const int lane = threadIdx.x & 31;
+  unsigned m = 0xffffffffu;
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    const bool in = (m >> lane) & 1u;
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, in ? wd[i] : 0u);
+    if (i < 2) any |= mx != 0u;
+    m = __ballot_sync(0xffffffffu, in && wd[i] == mx);
+    if (i >= 1 && __popc(m) == 1) break;
   }
-  return k;
+  return any ? __ffs(m) - 1 : -1;
 }
 
-// Top k of a candidate set held in registers (n <= kTopkIPT * blockDim.x).
-// Each thread sorts its <= 8 candidates (sorting network), each warp then
-// extracts its top k by k rounds of warp-best over the lanes' heads (the
-// winning lane pops its head), and warp 0 merges the per-warp lists the same
-// way.  No block barrier inside the rounds.  Result valid in warp 0.
-template <typename Fetch>
-__device__ int select_topk(int64_t n, int k, Fetch fetch, TopkRec* out) {
-  __shared__ Key s_cand[kTopkThreads / 32][kMaxK];
-  __shared__ int s_cnt[kTopkThreads / 32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  Key it[kTopkIPT];
+// Merge n_lists sorted lists of up to k_in records (counts in list_n, or,
+// when list_n == NULL, records with index >= 0 are valid) into the first k
+// by the C.8 order, with the whole block: thread t owns lists t, t + B, ...
+// and offers the best of their heads; k rounds of a block-wide best (warp
+// winners in shared memory, then warp 0); the owner of the winner advances.
+// Pads `out` to k.
+__device__ void merge_lists(const TopkRec* __restrict__ lists, const int* __restrict__ list_n,
+                            int n_lists, int k_in, int k, TopkRec* __restrict__ out,
+                            int* __restrict__ out_n) {
+  constexpr int kLPT = 4;                                      // lists per thread
+  __shared__ Key s_w[32];
+  __shared__ int s_win;                                        // winning thread, -1 none
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+  int cnt[kLPT], ptr[kLPT];
+  Key hd[kLPT];
+  auto head = [&](int j) -> Key {
+    const int l = t + j * (int)blockDim.x;
+    if (ptr[j] >= cnt[j]) return no_key();
+    const TopkRec x = lists[(int64_t)l * k_in + ptr[j]];
+    return make_key(x.throughput, x.peak, x.index, x.makespan);
+  };
 #pragma unroll
-  for (int i = 0; i < kTopkIPT; i++) {
-    const int64_t j = threadIdx.x + (int64_t)i * blockDim.x;
-    if (!(j < n && fetch(j, it[i]))) it[i] = no_key();
+  for (int j = 0; j < kLPT; j++) {
+    const int l = t + j * (int)blockDim.x;
+    cnt[j] = 0;
+    ptr[j] = 0;
+    if (l < n_lists) {
+      if (list_n) cnt[j] = list_n[l] < k_in ? list_n[l] : k_in;
+      else
+        while (cnt[j] < k_in && lists[(int64_t)l * k_in + cnt[j]].index >= 0) cnt[j]++;
+    }
+    hd[j] = head(j);
   }
-  // Batcher odd-even merge sort of 8 (19 comparators), descending
-  cswap(it[0], it[1]); cswap(it[2], it[3]); cswap(it[4], it[5]); cswap(it[6], it[7]);
-  cswap(it[0], it[2]); cswap(it[1], it[3]); cswap(it[4], it[6]); cswap(it[5], it[7]);
-  cswap(it[1], it[2]); cswap(it[5], it[6]);
-  cswap(it[0], it[4]); cswap(it[1], it[5]); cswap(it[2], it[6]); cswap(it[3], it[7]);
-  cswap(it[2], it[4]); cswap(it[3], it[5]);
-  cswap(it[1], it[2]); cswap(it[3], it[4]); cswap(it[5], it[6]);
-  int head = 0, got = 0;
+  int got = 0;
   for (int r = 0; r < k; r++) {
-    Key mine = no_key();
+    int bj = 0;                                                // best own head
+    Key mine = hd[0];
 #pragma unroll
-    for (int i = 0; i < kTopkIPT; i++)
-      if (i == head) mine = it[i];
-    const Key best = warp_best(mine);
-    if (best.a == 0) break;
-    if (mine.a != 0 && mine.c == best.c) {         // this lane's head won
-      s_cand[w][r] = mine;
-      head++;
+    for (int j = 1; j < kLPT; j++)
+      if (better(hd[j], mine)) { bj = j; mine = hd[j]; }
+    const int wl = warp_best_lane(mine);
+    bool win;
+    if (nw == 1) {
+      if (wl < 0) break;
+      win = lane == wl;
+    } else {
+      if (lane == 0) s_w[w] = no_key();
+      __syncwarp();
+      if (lane == wl) s_w[w] = mine;
+      __syncthreads();
+      if (w == 0) {
+        const int b = warp_best_lane(lane < nw ? s_w[lane] : no_key());
+        if (lane == 0) s_win = b < 0 ? -1 : b * 32;            // warp index * 32, resolved below
+      }
+      __syncthreads();
+      const int bw = s_win;
+      __syncthreads();
+      if (bw < 0) break;
+      win = (w == bw / 32) && lane == wl;
+    }
+    if (win) {
+      out[r] = key_rec(mine);
+#pragma unroll
+      for (int j = 0; j < kLPT; j++)
+        if (j == bj) { ptr[j]++; hd[j] = head(j); }
     }
     got++;
   }
-  if (lane == 0) s_cnt[w] = got;
-  __syncthreads();
-  got = 0;
-  if (w == 0) {
-    int ptr = 0;
-    const int cnt = lane < nw ? s_cnt[lane] : 0;
-    for (int r = 0; r < k; r++) {
-      const Key mine = ptr < cnt ? s_cand[lane][ptr] : no_key();
-      const Key best = warp_best(mine);
-      if (best.a == 0) break;
-      if (mine.a != 0 && mine.c == best.c) {
-        out[r] = key_rec(mine);
-        ptr++;
-      }
-      got++;
-    }
-  }
-  return got;    // valid in warp 0
+  for (int r = got + t; r < k; r += blockDim.x) out[r] = TopkRec{-1, 0.0, -1.0, -1};
+  if (t == 0) *out_n = got;
 }
 
-// Stream candidates [0, n) of `fetch` through select_topk in chunks of
-// kTopkIPT*kTopkThreads - kMaxK, carrying the best-so-far list (in shared
-// memory) into every chunk.  Chunks c = first, first + step, ...  Returns the
-// list length (all threads); the list is in s_acc.
-template <typename Fetch>
-__device__ int topk_stream(int64_t n, int64_t first, int64_t step, int k, Fetch fetch,
-                           TopkRec* s_acc, int* s_acc_n) {
-  const int64_t per = (int64_t)kTopkIPT * kTopkThreads - kMaxK;
-  if (threadIdx.x == 0) *s_acc_n = 0;
-  __syncthreads();
-  for (int64_t c = first; c * per < n || (c == first && n == 0); c += step) {
-    const int64_t base = c * per;
-    const int64_t len = n - base < per ? (n - base > 0 ? n - base : 0) : per;
-    const int acc_n = *s_acc_n;
-    auto f2 = [&](int64_t j, Key& key) -> bool {
-      if (j < acc_n) {
-        const TopkRec x = s_acc[j];
-        key = make_key(x.throughput, x.peak, x.index, x.makespan);
-        return true;
-      }
-      return fetch(base + (j - acc_n), key);
-    };
-    const int got = select_topk(acc_n + len, k, f2, s_acc);
-    __syncthreads();
-    if (threadIdx.x == 0) *s_acc_n = got;
-    __syncthreads();
-  }
-  return *s_acc_n;
-}
-
-// Partial top-k of the shard: grid-strided chunks per block.
-__global__ void __launch_bounds__(kTopkThreads) k_topk_partial(
+// Partial top-k of the shard, then the merge.  Block b takes chunks b, b +
+// gridDim, ... of kTopkThreads * kTopkIPT candidates; per chunk each thread
+// holds kTopkIPT candidates sorted in registers, each warp extracts its top
+// k by rounds of warp-best over the lanes' heads (the winning lane pops its
+// head; rounds stop when the warp runs out), and warp 0 merges the per-warp
+// lists with the best-so-far list carried from the previous chunk.  Each
+// block writes one sorted list; the last block to finish (ticket) merges
+// all of them.
+__global__ void __launch_bounds__(kTopkThreads) k_topk(
     const SpecBlock* __restrict__ spp, const double* __restrict__ ms,
     const int64_t* __restrict__ pk, const uint32_t* __restrict__ rs,
-    const double* __restrict__ tpv, int k, TopkRec* __restrict__ part, int* __restrict__ part_n) {
-  __shared__ TopkRec s_acc[kMaxK];
+    const double* __restrict__ tpv, int k, TopkRec* __restrict__ part, int* __restrict__ part_n,
+    WsHeader* __restrict__ hdr, TopkRec* __restrict__ out, int* __restrict__ out_n) {
+  constexpr int NW = kTopkThreads / 32;
+  static_assert(NW + 1 <= 32, "warp 0 merges the warps' lists and the carried list");
+  __shared__ Key s_cand[NW][kMaxK];
+  __shared__ int s_cnt[NW];
+  __shared__ Key s_acc[2][kMaxK];
   __shared__ int s_acc_n;
+  __shared__ bool s_last;
   const SpecBlock& sp = *spp;
   const int64_t n = sp.n_local;
   const int64_t rank = sp.rank, nr = sp.n_ranks;
-  auto fetch = [&](int64_t q, Key& c) -> bool {
-    if (rs[q] != 0) return false;
-    c = make_key(tpv[q], pk[q], rank + q * nr, ms[q]);
-    return true;
-  };
-  const int got = topk_stream(n, blockIdx.x, gridDim.x, k, fetch, s_acc, &s_acc_n);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int64_t per = (int64_t)kTopkThreads * kTopkIPT;
+  int cur = 0;
+  if (threadIdx.x == 0) s_acc_n = 0;
+  __syncthreads();
+  for (int64_t c = blockIdx.x; c * per < n; c += gridDim.x) {
+    Key it[kTopkIPT];
+#pragma unroll
+    for (int i = 0; i < kTopkIPT; i++) {
+      const int64_t q = c * per + threadIdx.x + (int64_t)i * kTopkThreads;
+      it[i] = (q < n && rs[q] == 0) ? make_key(tpv[q], pk[q], rank + q * nr, ms[q]) : no_key();
+    }
+    static_assert(kTopkIPT == 2, "one compare-exchange sorts a thread's candidates");
+    cswap(it[0], it[1]);
+    int head = 0, got = 0;
+    for (int r = 0; r < k; r++) {
+      const Key mine = head == 0 ? it[0] : (head == 1 ? it[1] : no_key());
+      const int wl = warp_best_lane(mine);
+      if (wl < 0) break;
+      if (lane == wl) { s_cand[w][r] = mine; head++; }
+      got++;
+    }
+    if (lane == 0) s_cnt[w] = got;
+    __syncthreads();
+    if (w == 0) {
+      const int acc_n = s_acc_n;
+      const int cnt = lane < NW ? s_cnt[lane] : (lane == NW ? acc_n : 0);
+      int ptr = 0, o = 0;
+      for (int r = 0; r < k; r++) {
+        Key mine = no_key();
+        if (ptr < cnt) mine = lane < NW ? s_cand[lane][ptr] : s_acc[cur][ptr];
+        const int wl = warp_best_lane(mine);
+        if (wl < 0) break;
+        if (lane == wl) { s_acc[cur ^ 1][r] = mine; ptr++; }
+        o++;
+      }
+      if (lane == 0) s_acc_n = o;
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  const int got = s_acc_n;
   TopkRec* o = part + (int64_t)blockIdx.x * k;
-  for (int r = threadIdx.x; r < got; r += blockDim.x) o[r] = s_acc[r];
+  for (int r = threadIdx.x; r < got; r += blockDim.x) o[r] = key_rec(s_acc[cur][r]);
   if (threadIdx.x == 0) part_n[blockIdx.x] = got;
+  // last block merges (threadfence reduction)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&hdr->topk_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  merge_lists(part, part_n, gridDim.x, k, k, out, out_n);
 }
 
-// Merge lists of up to k_in records: `n_lists` lists with counts in list_n,
-// or, when list_n == NULL, records with index >= 0 are valid.  One block;
-// pads `out` to k.
+// Merge of gathered per-rank lists (and the empty-shard case).
 __global__ void __launch_bounds__(kTopkThreads) k_topk_merge(const TopkRec* __restrict__ lists,
                                                             const int* __restrict__ list_n,
                                                             int n_lists, int k_in, int k,
                                                             TopkRec* __restrict__ out,
                                                             int* __restrict__ out_n) {
-  __shared__ TopkRec s_acc[kMaxK];
-  __shared__ int s_acc_n;
-  auto fetch = [&](int64_t j, Key& c) -> bool {
-    const int jj = (int)j;
-    const int l = jj / k_in, r = jj - l * k_in;
-    if (list_n ? r >= list_n[l] : lists[jj].index < 0) return false;
-    const TopkRec x = lists[jj];
-    c = make_key(x.throughput, x.peak, x.index, x.makespan);
-    return true;
-  };
-  const int got = topk_stream((int64_t)n_lists * k_in, 0, 1, k, fetch, s_acc, &s_acc_n);
-  for (int r = threadIdx.x; r < k; r += blockDim.x)
-    out[r] = r < got ? s_acc[r] : TopkRec{-1, 0.0, -1.0, -1};
-  if (threadIdx.x == 0) *out_n = got;
+  merge_lists(lists, list_n, n_lists, k_in, k, out, out_n);
 }
 
 }  // namespace distir
