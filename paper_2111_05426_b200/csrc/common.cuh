@@ -30,6 +30,11 @@ constexpr int kMaxSplit = 5;        // configs per item divided by up to 2^5
 struct PlanBudget {                 // resident warps of each simulate kernel
   uint32_t warps[kGroups];
 };
+// Binade tables (exact_add.cuh BinTab) of the wavefront simulate kernels:
+// the first kTabCfgs configurations of a warp get one.
+constexpr int kTabCfgs = 4;
+constexpr int kTabBinadesGpt2 = 32;   // 3 task segments
+constexpr int kTabBinadesMlp = 24;    // 3 forward + 4 backward task segments
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
 constexpr int kTopkBlocks = 1024;   // max partial top-k blocks (<= 4 lists per merge thread)

@@ -425,7 +425,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   CUDA_TRY(mark(1));
   if (n > 0) {
 #define DISTIR_SIM(KD, MD) \
-  k_simulate<KD, MD><<<sim->sim_grid[KD * kModes + MD], sim_tpb(KD, MD), 0, st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv)
+  k_simulate<KD, MD><<<sim->sim_grid[KD * kModes + MD], sim_tpb(KD, MD), sim_smem(KD, MD), st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv)
 #if DISTIR_SEQ_MAXP >= 1
     DISTIR_SIM(0, 0); DISTIR_SIM(1, 0);
     kernels += 2;
@@ -674,8 +674,13 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
       (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<0, 5>,
       (const void*)k_simulate<1, 0>, (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>,
       (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr};
-  for (int g = 0; g < kGroups && e == cudaSuccess; g++)
-    if (fns[g]) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], fns[g], sim_tpb(g / kModes, g % kModes), 0);
+  for (int g = 0; g < kGroups && e == cudaSuccess; g++) {
+    if (!fns[g]) continue;
+    const int smem = sim_smem(g / kModes, g % kModes);
+    e = cudaFuncSetAttribute(fns[g], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], fns[g], sim_tpb(g / kModes, g % kModes), smem);
+  }
   if (e != cudaSuccess) {
     delete sim;
     return fail(DISTIR_E_CUDA, std::string("device setup: ") + cudaGetErrorString(e));

@@ -77,6 +77,7 @@ constexpr int64_t kHidden = int64_t(1) << 52;
 constexpr int64_t kTwo53 = int64_t(1) << 53;
 constexpr double kTwo53d = 9007199254740992.0;
 constexpr double kNever = 1.152921504606846976e18;   // 2^60: never fits a binade
+DISTIR_HD double kInf() { return bits2d(0x7FF0000000000000ll); }
 
 #ifdef __CUDA_ARCH__
 DISTIR_HD double xmul(double a, double b) { return __dmul_rn(a, b); }
@@ -172,29 +173,72 @@ struct Seg {
 };
 
 // Per-task cache for one binade: the x increment of the whole task from an
-// even / odd significand (-1: the task never fits this binade), and each
-// segment's per-pass ulp increments (R[2i], R[2i+1]; kNever if a pass never
-// fits) in caller-provided storage (shared memory).
+// even / odd significand (+inf: the task never fits this binade), the
+// binade's bounds [lo, hi) = [2^E, 2^(E+1)) (lo = +inf: no binade cached),
+// and each segment's per-pass ulp increments (R[2i], R[2i+1]; kNever if a
+// pass never fits), either in caller-provided per-lane storage or in a
+// per-configuration binade table (BinTab) shared by the configuration's lanes.
 struct TaskCache {
   int32_t ef;
   double Su0, Su1;
+  double lo, hi;
   double* R;
+  double* own;          // per-lane storage for binades outside the table
 };
 
-DISTIR_HD TaskCache task_cache_make(double* store) { return TaskCache{-1, -1.0, -1.0, store}; }
+// Per-pass increments of NS segments for the binades [e0, e0 + nb), filled
+// cooperatively by a configuration's lanes before its walk (binade b at
+// tab + b * 2 * NS); nb = 0 disables the table.
+struct BinTab {
+  double* tab;
+  int32_t e0, nb;
+};
 
+DISTIR_HD TaskCache task_cache_make(double* store) {
+  return TaskCache{-1, kInf(), kInf(), kInf(), kInf(), store, store};
+}
+
+// Fill binades e0 + first, e0 + first + stride, ... of a table of NS
+// segments (the segments' op lists; reps are ignored).
 template <int NS>
-DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
+DISTIR_HD void bintab_fill(const BinTab& t, const Seg (&sg)[NS], int first, int stride) {
+  for (int b = first; b < t.nb; b += stride) {
+    const int32_t ef = t.e0 + b;
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      double R0 = kNever, R1 = kNever;
+      if (!(ef >= 53 && ef <= 1993) || !seg_pass(sg[i].a, sg[i].n, ef, R0, R1)) R0 = R1 = kNever;
+      t.tab[(int64_t)b * 2 * NS + 2 * i] = R0;
+      t.tab[(int64_t)b * 2 * NS + 2 * i + 1] = R1;
+    }
+  }
+}
+
+// Move the cache to binade field ef: per-pass increments from the table when
+// it covers ef, else computed into the lane's own storage; then the task's
+// total increments from each parity (closed forms of reps_total).
+template <int NS>
+DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS], const BinTab& t) {
   DISTIR_COUNT(2);
+  if (ef - t.e0 >= 0 && ef - t.e0 < t.nb) {
+    c.R = t.tab + (int64_t)(ef - t.e0) * 2 * NS;
+  } else {
+    c.R = c.own;
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      double R0 = kNever, R1 = kNever;
+      if (sg[i].reps > 0 && !seg_pass(sg[i].a, sg[i].n, ef, R0, R1)) R0 = R1 = kNever;
+      c.R[2 * i] = R0;
+      c.R[2 * i + 1] = R1;
+    }
+  }
   double T[2] = {0.0, 0.0};
   bool ok = true;
 #pragma unroll
   for (int i = 0; i < NS; i++) {
-    double R0 = kNever, R1 = kNever;
-    if (sg[i].reps > 0 && !seg_pass(sg[i].a, sg[i].n, ef, R0, R1)) { R0 = R1 = kNever; ok = false; }
-    c.R[2 * i] = R0;
-    c.R[2 * i + 1] = R1;
-    if (sg[i].reps <= 0 || !ok) continue;
+    if (sg[i].reps <= 0) continue;
+    const double R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
+    if (!(R0 < kNever)) { ok = false; continue; }
 #pragma unroll
     for (int p = 0; p < 2; p++) {
       const int pe = p ^ odd(T[p]);                 // parity entering segment i
@@ -204,20 +248,25 @@ DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
   }
   const double u = bits2d((int64_t)(ef - 52) << 52);
   c.ef = ef;
-  c.Su0 = (ok && T[0] < kTwo53d) ? xmul(T[0], u) : -1.0;     // exact
-  c.Su1 = (ok && T[1] < kTwo53d) ? xmul(T[1], u) : -1.0;
+  c.lo = bits2d((int64_t)ef << 52);
+  c.hi = bits2d((int64_t)(ef + 1) << 52);
+  c.Su0 = (ok && T[0] < kTwo53d) ? xmul(T[0], u) : kInf();     // exact
+  c.Su1 = (ok && T[1] < kTwo53d) ? xmul(T[1], u) : kInf();
+}
+template <int NS>
+DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
+  task_refresh(c, ef, sg, BinTab{nullptr, 0, 0});
 }
 
 // Fast path of a task: when x lies in the cached binade and the whole task
 // stays inside it, x <- x + Su (exact) and true; otherwise x is untouched
-// and false.  Branch-free (the caller branches once, warp-uniformly, on the
-// rare misses).
+// and false.  x >= 2^E and x + Su < 2^(E+1) is exactly "x in binade E and
+// the rounded sum keeps x's exponent" (Su >= 0; +inf never fits).
+// Branch-free (the caller branches once, warp-uniformly, on the rare misses).
 DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
-  const int64_t xb = d2bits(x);
-  const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
-  const double Su = (xb & 1) ? c.Su1 : c.Su0;
+  const double Su = (d2bits(x) & 1) ? c.Su1 : c.Su0;
   const double y = xadd(x, Su);
-  const bool ok = x > 0.0 && ef == c.ef && Su >= 0.0 && exp_field(y) == ef;
+  const bool ok = x >= c.lo && y < c.hi;
   x = ok ? y : x;
   return ok;
 }
@@ -228,12 +277,12 @@ DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
 // walk when the binade has ties), the pass that leaves the binade is done op
 // by op, and the cache follows x into the new binade.
 template <int NS>
-DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
+DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t) {
   DISTIR_COUNT(0);
   {
     const int32_t ef = exp_field(x);
     if (x > 0.0 && ef >= 53 && ef <= 1993) {
-      if (ef != c.ef) task_refresh(c, ef, sg);
+      if (ef != c.ef) task_refresh(c, ef, sg, t);
       if (task_fast(x, c)) { DISTIR_COUNT(1); return; }
     }
   }
@@ -244,7 +293,7 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
       const int64_t xb = d2bits(x);
       const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
       if (x > 0.0 && ef >= 53 && ef <= 1993) {
-        if (ef != c.ef) task_refresh(c, ef, sg);
+        if (ef != c.ef) task_refresh(c, ef, sg, t);
         const double R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
         if (R0 < kNever) {
           int64_t M = (xb & kMant) | kHidden;
@@ -252,8 +301,12 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
           const int64_t before = reps;
           if (r0 == r1) {                            // no tie: closed form
             const int64_t avail = kTwo53 - 1 - M;
-            int64_t fit = r0 > 0 ? (int64_t)((double)avail / (double)r0) : reps;
-            if (fit > reps) fit = reps;
+            int64_t fit = reps;                      // min(reps, avail / r0)
+            if (r0 > 0 && (double)reps * (double)r0 > (double)avail) {   // reps <= 2^10
+              fit = (int64_t)((float)avail / (float)r0);
+              if (fit > reps) fit = reps;
+              if (fit < 0) fit = 0;
+            }
             while (fit > 0 && fit * r0 > avail) fit--;
             while (fit < reps && (fit + 1) * r0 <= avail) fit++;
             M += fit * r0;
@@ -278,6 +331,11 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
       }
     }
   }
+}
+
+template <int NS>
+DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
+  add_task(x, sg, c, BinTab{nullptr, 0, 0});
 }
 
 // ------------------------------------------------------------------ memory --

@@ -448,6 +448,16 @@ __host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per
 __host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per block
   return sim_row(kind, mode) * 8 * 128 <= 48 * 1024 ? 128 : 64;
 }
+// Binade tables (exact_add.cuh BinTab) of the wavefront kernels: the first
+// kTabCfgs configurations of a warp (S >= 2 lanes each) get one, filled by
+// their lanes before the walk: binades x 2 parities x segments doubles.
+__host__ __device__ constexpr int sim_tab(int kind, int mode) {   // doubles per config
+  return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3 : kTabBinadesMlp * 2 * 7;
+}
+__host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic smem bytes
+  return 8 * (sim_tpb(kind, mode) * sim_row(kind, mode) +
+              (sim_tpb(kind, mode) / 32) * kTabCfgs * sim_tab(kind, mode));
+}
 
 template <int KIND, int MODE>
 __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecBlock* __restrict__ spp,
@@ -471,10 +481,13 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
   const unsigned int n_warps = gridDim.x * (blockDim.x >> 5);
   const unsigned int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   bool first_item = true;
-  // per-lane rows: op costs, then per-slot task-cache increments
+  // per-lane rows (op costs, then per-slot task-cache increments), then
+  // the warps' binade tables
   constexpr int ROW = sim_row(KIND, MODE);
-  __shared__ double s_row[sim_tpb(KIND, MODE)][ROW];
-  double* row = s_row[threadIdx.x];
+  constexpr int TAB = sim_tab(KIND, MODE);
+  extern __shared__ double s_dyn[];
+  double* row = s_dyn + threadIdx.x * ROW;
+  double* wtab = s_dyn + sim_tpb(KIND, MODE) * ROW + (threadIdx.x >> 5) * kTabCfgs * TAB;
   unsigned long long feas = 0;
   while (true) {
     unsigned int id;
@@ -501,13 +514,14 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
       c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
     }
     const DTopo& tp = sp.topos[c.topo];
+    double* tab = (TAB > 0 && S >= 2 && seg < kTabCfgs) ? wtab + seg * TAB : nullptr;
     double ms;
     int64_t pk;
 #ifdef DISTIR_INSTR
     const long long t0 = clock64();
 #endif
-    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, ms, pk);
-    else run_mlp<V, SEQ, MODE == 5>(c, tp, has, sl, S, lane, row, ms, pk);
+    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+    else run_mlp<V, SEQ, MODE == 5>(c, tp, has, sl, S, lane, row, tab, ms, pk);
 #ifdef DISTIR_INSTR
     if (lane == 0) {
       const unsigned long long dt = (unsigned long long)(clock64() - t0);
@@ -596,7 +610,7 @@ __device__ void merge_lists(const TopkRec* __restrict__ lists, const int* __rest
   __shared__ Key s_w[32];
   __shared__ int s_win;                                        // winning thread, -1 none
   const int t = threadIdx.x, w = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
-  int cnt[kLPT], ptr[kLPT];
+  int cnt[kLPT] = {}, ptr[kLPT] = {};
   Key hd[kLPT];
   auto head = [&](int j) -> Key {
     const int l = t + j * (int)blockDim.x;

@@ -12,6 +12,29 @@
 // shared memory (`row`), read only when a task's binade cache is refreshed
 // or a task crosses a binade.
 
+// Binade range of a configuration's clocks (for its BinTab): from the
+// smallest positive op cost (every positive clock is at least one op's cost)
+// to an upper bound of the makespan (P stages x the busiest stage's total
+// work, doubled for rounding slack), capped at nb_max binades.  `work` is
+// this lane's total work; the max runs over the configuration's S lanes.
+__device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, double cmin, double work,
+                                               int64_t P, int S) {
+  for (int o = S >> 1; o > 0; o >>= 1) {
+    work = fmax(work, __shfl_xor_sync(0xffffffffu, work, o));
+    cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+  }
+  BinTab t{tab, 0, 0};
+  if (tab != nullptr && cmin > 0.0 && cmin < kInf()) {
+    const int32_t e0 = exp_field(cmin);
+    const int32_t e1 = exp_field(__dmul_rn(work, 2.0 * (double)P)) + 1;
+    t.e0 = e0 < 53 ? 53 : e0;
+    const int32_t nb = e1 - t.e0 + 1;
+    t.nb = nb < 0 ? 0 : (nb > nb_max ? nb_max : nb);
+  }
+  return t;
+}
+__device__ __forceinline__ double min_pos(double m, double x) { return x > 0.0 && x < m ? x : m; }
+
 __device__ __forceinline__ MemProf mem_alt(MemProf A, MemProf B, int p0, int n) {
   if (n <= 0) return mem_id();
   MemProf r = mem_id();
@@ -35,7 +58,7 @@ __device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, in
 
 template <int V, bool SEQ, bool F1B>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                        double* row, double& ms_out, int64_t& peak_out) {
+                        double* row, double* tab, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
   const int64_t m = has ? c.B / (D * K) : 0;
   const int32_t ns = tp.node_size;
@@ -125,28 +148,65 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     cb[q] = task_cache_make(row + 15 + 14 * q + 6);  // 4 bwd segments
   }
 
+  // task segments; the op lists are the same on every lane of the
+  // configuration (only the repetition counts depend on the stage)
+  auto fsegs = [&](int q, Seg (&sg)[3]) {
+    alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
+  };
+  auto bsegs = [&](int q, Seg (&sg)[4]) {                      // LossGrad, layers desc
+    sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
+    alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
+  };
+  BinTab btf{nullptr, 0, 0}, btb{nullptr, 0, 0};
+  if constexpr (!SEQ) {
+    // binade tables of the forward / backward task segments, filled by the
+    // configuration's lanes (forward at tab, backward after it)
+    double cmin = kInf(), work = 0.0;
+    for (int j = 0; j < 15; j++) cmin = min_pos(cmin, row[j]);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (!ok[q]) continue;
+      cmin = min_pos(min_pos(cmin, sendf[q]), sendb[q]);
+      double lay = 0.0;
+      for (int j = 0; j < 14; j++) lay = lay + row[j];
+      const double w = (double)(hi[q] - lo[q]) * lay + row[14] + sendf[q] + sendb[q];
+      work = fmax(work, w * (double)K);
+    }
+    btf = bintab_range(has ? tab : nullptr, kTabBinadesMlp, cmin, work, P, S);
+    btb = btf;
+    btb.tab = btf.tab ? btf.tab + kTabBinadesMlp * 6 : nullptr;
+    Seg f[3], g[4];
+    fsegs(0, f);
+    bsegs(0, g);
+    bintab_fill(btf, f, sl, S);
+    bintab_fill(btb, g, sl, S);
+    __syncwarp();
+  }
   auto fwd_task = [&](int q, bool act) {
-    if (act) mem_apply(live[q], peak[q], pf[q]);
+    if constexpr (SEQ || F1B) {
+      if (act) mem_apply(live[q], peak[q], pf[q]);
+    }
     const bool slow = act && !task_fast(clk[q], cf[q]);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
       Seg sg[3];
-      alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
-      add_task(clk[q], sg, cf[q]);
+      fsegs(q, sg);
+      add_task(clk[q], sg, cf[q], btf);
     }
     DISTIR_SLOW_T1(any)
   };
   auto bwd_task = [&](int q, bool act) {
-    if (act) mem_apply(live[q], peak[q], pb[q]);
+    if constexpr (SEQ || F1B) {
+      if (act) mem_apply(live[q], peak[q], pb[q]);
+    }
     const bool slow = act && !task_fast(clk[q], cb[q]);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
-      Seg sg[4];                                               // LossGrad, layers desc
-      sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
-      alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
-      add_task(clk[q], sg, cb[q]);
+      Seg sg[4];
+      bsegs(q, sg);
+      add_task(clk[q], sg, cb[q], btb);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -264,68 +324,83 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       }
     }
   } else {
-  // ---- forward wavefront: task (k, s) at step 2k + s
+  // Memory is time-independent (SURVEY C.7 Theorem 4): stage s's events
+  // are recv act(k), fwd(k) [the Send keeps the activation for backward]
+  // for every k, then recv grad(k), bwd(k), send grad(k) (the sent
+  // gradient dies), composed exactly before the walk.
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (!ok[q]) continue;
+    const MemProf ra = s[q] > 0 ? mem_op(m * kin[lo[q] & 1] * e, 0) : mem_id();
+    const MemProf rg = s[q] < P - 1 ? mem_op(m * dout[(hi[q] - 1) & 1] * e, 0) : mem_id();
+    const MemProf sg = s[q] > 0 ? mem_op(0, m * kin[lo[q] & 1] * e) : mem_id();
+    mem_apply(live[q], peak[q], mem_then(mem_rep(mem_then(ra, pf[q]), K),
+                                         mem_rep(mem_then(mem_then(rg, pb[q]), sg), K)));
+  }
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
-  for (int w = 0; w < nsteps; w++) {
-    bool act[V];
+  const unsigned int K2 = (unsigned int)(2 * K);
+  bool up[V], dn[V];
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      const int kk = w - s[q];
-      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      fwd_task(q, act[q]);
-    }
-    // Send s -> s+1: both ends wait for each other (P:119, P:303); the end
-    // time travels back to the receiver (-1 = nothing sent)
-    double nb[V], t[V];
-    Nbr<V>::up_stage(clk, nb, lane);
+  for (int q = 0; q < V; q++) {
+    up[q] = ok[q] && s[q] < P - 1;
+    dn[q] = ok[q] && s[q] > 0;
+  }
+  // ---- forward wavefront: task (k, s) at step 2k + s, then Send s -> s+1
+  {
+    int kk[V];
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      const bool snd = act[q] && s[q] < P - 1;
-      const double end = dadd(fmax(clk[q], nb[q]), sendf[q]);
-      if (snd) clk[q] = end;
-      t[q] = snd ? end : -1.0;
-    }
-    double tin[V];
-    Nbr<V>::down_stage(t, tin, lane);
+    for (int q = 0; q < V; q++) kk[q] = -s[q];
+    for (int w = 0; w < nsteps; w++) {
+      bool act[V];
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] > 0 && tin[q] >= 0.0) {
-        clk[q] = tin[q];
-        MEM(q, m * kin[lo[q] & 1] * e, 0);                    // received activation
+      for (int q = 0; q < V; q++) {
+        act[q] = ok[q] && (unsigned int)kk[q] < K2 && !(kk[q] & 1);
+        kk[q]++;
+        fwd_task(q, act[q]);
       }
+      // Send s -> s+1: both ends wait for each other; the end
+      // time travels back to the receiver (-1 = nothing sent)
+      double nb[V], t[V];
+      Nbr<V>::up_stage(clk, nb, lane);
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        const bool snd = act[q] && up[q];
+        const double end = dadd(fmax(clk[q], nb[q]), sendf[q]);
+        clk[q] = snd ? end : clk[q];
+        t[q] = snd ? end : -1.0;
+      }
+      double tin[V];
+      Nbr<V>::down_stage(t, tin, lane);
+#pragma unroll
+      for (int q = 0; q < V; q++) clk[q] = (dn[q] && tin[q] >= 0.0) ? tin[q] : clk[q];
     }
   }
-
-  // ---- backward wavefront: task (k, s) at step 2k + (P-1-s)
-  for (int w = 0; w < nsteps; w++) {
-    bool act[V];
+  // ---- backward wavefront: task (k, s) at step 2k + (P-1-s), then Send s -> s-1
+  {
+    int kk[V];
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      const int kk = w - (int)(P - 1 - s[q]);
-      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      bwd_task(q, act[q]);
-    }
-    // Send s -> s-1
-    double nb[V], t[V];
-    Nbr<V>::down_stage(clk, nb, lane);
+    for (int q = 0; q < V; q++) kk[q] = -(int)(P - 1 - s[q]);
+    for (int w = 0; w < nsteps; w++) {
+      bool act[V];
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      const bool snd = act[q] && s[q] > 0;
-      const double end = dadd(fmax(clk[q], nb[q]), sendb[q]);
-      if (snd) {
-        clk[q] = end;
-        live[q] -= m * kin[lo[q] & 1] * e;                    // sent gradient dies
+      for (int q = 0; q < V; q++) {
+        act[q] = ok[q] && (unsigned int)kk[q] < K2 && !(kk[q] & 1);
+        kk[q]++;
+        bwd_task(q, act[q]);
       }
-      t[q] = snd ? end : -1.0;
-    }
-    double tin[V];
-    Nbr<V>::up_stage(t, tin, lane);
+      double nb[V], t[V];
+      Nbr<V>::down_stage(clk, nb, lane);
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] < P - 1 && tin[q] >= 0.0) {
-        clk[q] = tin[q];
-        MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);             // received gradient
+      for (int q = 0; q < V; q++) {
+        const bool snd = act[q] && dn[q];
+        const double end = dadd(fmax(clk[q], nb[q]), sendb[q]);
+        clk[q] = snd ? end : clk[q];
+        t[q] = snd ? end : -1.0;
       }
+      double tin[V];
+      Nbr<V>::up_stage(t, tin, lane);
+#pragma unroll
+      for (int q = 0; q < V; q++) clk[q] = (up[q] && tin[q] >= 0.0) ? tin[q] : clk[q];
     }
   }
   }  // wavefront
@@ -363,7 +438,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 // ------------------------------------------------ GPT-2 inference (C.4) -----
 template <int V, bool SEQ>
 __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                         double* row, double& ms_out, int64_t& peak_out) {
+                         double* row, double* tab, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
                 ide = c.M.ide, nctx = c.M.nctx;
   const bool lm = c.M.lm != 0;
@@ -467,16 +542,44 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     tc[q] = task_cache_make(row + 19 + 6 * q);       // 3 segments
   }
 
+  // the task's segments: prologue (stage 0), blocks, epilogue (stage P-1);
+  // the op lists are the same on every lane of the configuration
+  auto segs = [&](int q, Seg (&sg)[3]) {
+    sg[0] = Seg{row, 2, s[q] == 0 ? 1 : 0};
+    sg[1] = Seg{row + 2, 14, nb[q]};
+    sg[2] = Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0};
+  };
+  BinTab bt{nullptr, 0, 0};
+  if constexpr (!SEQ) {
+    // binade table of the task segments, filled by the configuration's lanes
+    double cmin = kInf(), work = 0.0;
+    for (int j = 0; j < 19; j++) cmin = min_pos(cmin, row[j]);
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      if (!ok[q]) continue;
+      cmin = min_pos(cmin, sendf[q]);
+      double w = nb[q] * (row[2] + row[3] + row[4] + row[5] + row[6] + row[7] + row[8] + row[9] +
+                          row[10] + row[11] + row[12] + row[13] + row[14] + row[15]);
+      w = w + row[0] + row[1] + row[16] + row[17] + row[18] + sendf[q];
+      work = fmax(work, w * (double)K);
+    }
+    bt = bintab_range(has ? tab : nullptr, kTabBinadesGpt2, cmin, work, P, S);
+    Seg sg[3];
+    segs(0, sg);
+    bintab_fill(bt, sg, sl, S);
+    __syncwarp();
+  }
   auto task = [&](int q, bool act, bool last) {
-    if (act) mem_apply(live[q], peak[q], last ? ptask1[q] : ptask0[q]);
+    if constexpr (SEQ) {
+      if (act) mem_apply(live[q], peak[q], last ? ptask1[q] : ptask0[q]);
+    }
     const bool slow = act && !task_fast(clk[q], tc[q]);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
-      const Seg sg[3] = {Seg{row, 2, s[q] == 0 ? 1 : 0},           // prologue
-                         Seg{row + 2, 14, nb[q]},                   // blocks
-                         Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0}};  // epilogue
-      add_task(clk[q], sg, tc[q]);
+      Seg sg[3];
+      segs(q, sg);
+      add_task(clk[q], sg, tc[q], bt);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -498,31 +601,53 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       }
     }
   } else {
+  // Memory is time-independent (SURVEY C.7 Theorem 4): stage s's events
+  // are recv(k), task(k), send(k) for k = 0..K-1 (the last task frees the
+  // parameters), composed exactly before the walk.
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    if (!ok[q]) continue;
+    const MemProf rv = s[q] > 0 ? mem_op(nde, 0) : mem_id();          // received activation
+    const MemProf sd = s[q] < P - 1 ? mem_op(0, nde) : mem_id();      // sent activation dies
+    const MemProf p0 = mem_then(mem_then(rv, ptask0[q]), sd);
+    const MemProf p1 = mem_then(mem_then(rv, ptask1[q]), sd);
+    mem_apply(live[q], peak[q], mem_then(mem_rep(p0, K - 1), p1));
+  }
+  // wavefront: task (k, s) at step 2k + s, then Send s -> s+1
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  bool up[V], dn[V];
+  int kk[V];
+  const unsigned int K2 = (unsigned int)(2 * K);
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    up[q] = ok[q] && s[q] < P - 1;
+    dn[q] = ok[q] && s[q] > 0;
+    kk[q] = -s[q];
+  }
   for (int w = 0; w < nsteps; w++) {
     if (lane == 0) DISTIR_COUNT(4);
     bool act[V];
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      const int kk = w - s[q];
-      act[q] = ok[q] && kk >= 0 && !(kk & 1) && (kk >> 1) < K;
-      task(q, act[q], (kk >> 1) == K - 1);
+      act[q] = ok[q] && (unsigned int)kk[q] < K2 && !(kk[q] & 1);
+      kk[q]++;
+      task(q, act[q], false);
     }
+    // Send s -> s+1: both ends wait for each other (P:119, P:303); the end
+    // time travels back to the receiver (-1 = nothing sent)
     double nbv[V], t[V];
     Nbr<V>::up_stage(clk, nbv, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      const bool snd = act[q] && s[q] < P - 1;
+      const bool snd = act[q] && up[q];
       const double end = dadd(fmax(clk[q], nbv[q]), sendf[q]);
-      if (snd) { clk[q] = end; live[q] -= nde; }              // sent activation dies
+      clk[q] = snd ? end : clk[q];
       t[q] = snd ? end : -1.0;
     }
     double tin[V];
     Nbr<V>::down_stage(t, tin, lane);
 #pragma unroll
-    for (int q = 0; q < V; q++) {
-      if (ok[q] && s[q] > 0 && tin[q] >= 0.0) { clk[q] = tin[q]; MEM(q, nde, 0); }
-    }
+    for (int q = 0; q < V; q++) clk[q] = (dn[q] && tin[q] >= 0.0) ? tin[q] : clk[q];
   }
   }  // wavefront
   double msx = 0.0;

@@ -1,8 +1,8 @@
 // Host check of the product's exact aggregation (paper_2111_05426_b200/csrc/
 // exact_add.cuh): add_task(x, segments) must equal every plain IEEE addition
 // of the task, in order, bit for bit -- over random, tie-heavy dyadic and
-// zero costs, clocks starting at zero or anywhere, binade crossings, and a
-// cache reused across tasks -- and MemProf composition must equal the
+// zero costs, clocks starting at zero or anywhere, binade crossings, a
+// cache reused across tasks, with and without a precomputed binade table -- and MemProf composition must equal the
 // op-by-op live/peak walk.
 #include <cmath>
 #include <cstdio>
@@ -30,18 +30,27 @@ static long check(std::mt19937_64& g, int trials, int mode) {
     for (int i = 0; i < NS; i++) {
       const int n = 1 + (int)(g() % 14);
       for (int j = 0; j < n; j++) store[i][j] = draw_cost(g, mode);
-      sg[i] = Seg{store[i], n, (g() % 5 == 0) ? 0 : 1 + (int64_t)(g() % 200)};
+      sg[i] = Seg{store[i], n, (g() % 5 == 0) ? 0 : 1 + (int64_t)(g() % ((g() & 7) ? 200 : 1024))};
     }
     double x = (g() % 5 == 0) ? 0.0 : std::ldexp(U(g), -(int)(g() % 30));
     double y = x;
     double cstore[2 * NS];
     TaskCache c = task_cache_make(cstore);
+    // half of the trials use a binade table (BinTab) covering a random range
+    // around the clocks; binades outside it fall back to the lane's storage
+    static double tstore[64 * 2 * NS];
+    BinTab tb{tstore, 0, 0};
+    if (g() & 1) {
+      tb.e0 = 1023 - 45 + (int)(g() % 40);
+      tb.nb = 1 + (int)(g() % 64);
+      bintab_fill(tb, sg, 0, 1);
+    }
     const int tasks = 1 + (int)(g() % 40);
     for (int k = 0; k < tasks; k++) {
       for (int i = 0; i < NS; i++)
         for (int64_t r = 0; r < sg[i].reps; r++)
           for (int j = 0; j < sg[i].n; j++) x = x + sg[i].a[j];
-      if ((g() & 1) || !task_fast(y, c)) add_task(y, sg, c);   // as the kernels do
+      if ((g() & 1) || !task_fast(y, c)) add_task(y, sg, c, tb);   // as the kernels do
       if (std::memcmp(&x, &y, 8) != 0) {
         if (bad < 5) std::printf("mismatch NS=%d mode=%d task=%d plain=%a agg=%a\n", NS, mode, k, x, y);
         bad++;
