@@ -60,7 +60,8 @@ def _p(a, t):
 
 
 MODEL_KEYS = ("kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
-              "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule")
+              "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule",
+              "recompute", "zero")
 
 
 def model_fields(m) -> np.ndarray:
@@ -216,7 +217,7 @@ def spec_arrays(grid, models=None, topos=None):
     models = models or MODELS
     topos = topos or TOPOLOGIES
     mt = np.concatenate([model_fields(models[m]) for m in grid["models"]]) \
-        if grid["models"] else np.zeros(11, np.int64)
+        if grid["models"] else np.zeros(13, np.int64)
     tis, tds = zip(*[topo_arrays(topos[t]) for t in grid["topos"]])
     ti = np.concatenate(tis)
     td = np.concatenate(tds)
@@ -234,14 +235,14 @@ def spec_arrays(grid, models=None, topos=None):
 
 def enumerate_grid(grid, with_models=False):
     """Nested-loop enumeration (C.1).  Returns int64 [N, 9]:
-    model_slot, topo_slot, W, D, T, P, K, B, kind  (and [N, 11] models)."""
+    model_slot, topo_slot, W, D, T, P, K, B, kind  (and [N, 13] models)."""
     L = lib()
     nm, mt, nt, ti, td, hdr, lists = spec_arrays(grid)
     args = (ctypes.c_int32(nm), _p(mt, I64P), ctypes.c_int32(nt),
             _p(ti, I64P), _p(td, F64P), _p(hdr, I64P), _p(lists, I64P))
     n = L.oracle_enumerate(*args, ctypes.c_int64(0), None, None)
     f = np.zeros((max(n, 1), 9), np.int64)
-    mo = np.zeros((max(n, 1), 11), np.int64)
+    mo = np.zeros((max(n, 1), 13), np.int64)
     L.oracle_enumerate(*args, ctypes.c_int64(n), _p(f, I64P),
                        _p(mo, I64P) if with_models else None)
     return (f[:n], mo[:n]) if with_models else f[:n]

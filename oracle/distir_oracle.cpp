@@ -44,6 +44,10 @@ struct Model {          // workloads/ model dict, in this order
   int64_t n_layer, d_model, n_head, seq_len, vocab_pad, n_ctx;
   int64_t dtype_bytes, id_bytes, lm_head;
   int64_t schedule;     // MLP training pipeline schedule: 0 GPipe, 1 1F1B
+  // memory-saving variants of the training program (NEXT row f4; Appendix
+  // Figs. 8/9): gradient checkpointing and ZeRO-2/3 partitioning
+  int64_t recompute;    // 1: discard in-stage activations, recompute in backward
+  int64_t zero;         // 1: W_l and its gradient owned by replica l mod D
 };
 struct Topo {
   int64_t world_max, node_size, capacity;
@@ -60,6 +64,7 @@ Model model_from(const int64_t* f) {
   m.kind = f[0]; m.n_layer = f[1]; m.d_model = f[2]; m.n_head = f[3];
   m.seq_len = f[4]; m.vocab_pad = f[5]; m.n_ctx = f[6]; m.dtype_bytes = f[7];
   m.id_bytes = f[8]; m.lm_head = f[9]; m.schedule = f[10];
+  m.recompute = f[11]; m.zero = f[12];
   return m;
 }
 Topo topo_from(const int64_t* i, const double* d) {
@@ -75,7 +80,7 @@ Topo topo_from(const int64_t* i, const double* d) {
 
 // ---------------------------------------------------------- the program ----
 // a function is a list of ops over SSA values.
-enum Cls { COMPUTE = 0, SEND = 1, ALLREDUCE = 2, ALLGATHER = 3 };
+enum Cls { COMPUTE = 0, SEND = 1, ALLREDUCE = 2, ALLGATHER = 3, BROADCAST = 4, REDUCE = 5 };
 
 struct Value {
   int dev;          // the device the value lives on (P:410 type carries device)
@@ -137,9 +142,14 @@ double op_cost(const Topo& t, const Program& pr, const Op& op) {
   if (op.cls == ALLREDUCE)  // ring: 2(g-1) steps of bytes/g
     return ((double)(2 * (g - 1))) * a +
            (((double)(2 * (g - 1))) / ((double)g)) * (((double)op.work) / bw);
-  // ALLGATHER, ring: (g-1) steps; work = gathered bytes
-  return ((double)(g - 1)) * a +
-         (((double)(g - 1)) / ((double)g)) * (((double)op.work) / bw);
+  if (op.cls == ALLGATHER)  // ring: (g-1) steps; work = gathered bytes
+    return ((double)(g - 1)) * a +
+           (((double)(g - 1)) / ((double)g)) * (((double)op.work) / bw);
+  // BROADCAST from the owner / REDUCE to the owner (ZeRO, Fig. 9):
+  // a pipelined chain over the g members, (g-1) hops of latency and the
+  // whole tensor once over a link; g = 2 is exactly a Send (Fig. 9 sends
+  // w1, w2 between its two devices).  DESIGN reading R9.
+  return ((double)(g - 1)) * a + ((double)op.work) / bw;
 }
 
 // ------------------------------------------------ C.3 MLP training, GPipe ---
@@ -173,52 +183,105 @@ Program build_mlp(const Model& M, const Cfg& c) {
                   std::vector<int> out, int64_t work, bool mm = false) {
     pr.ops.push_back(Op{cls, std::move(devs), std::move(in), std::move(out), work, 0.0, mm});
   };
+  // NEXT row f4 (Appendix; DESIGN readings R8/R9).
+  // Gradient checkpointing (Fig. 8): a stage keeps its input and output
+  // activations; the activations inside the stage die after their forward
+  // use and are recomputed at the start of the stage's backward (after
+  // LossGrad, as as_b follows dp in Fig. 8).
+  const bool ckpt = M.recompute != 0;
+  // ZeRO-2/3 (Fig. 9): W_l and its gradient belong to replica l mod D of the
+  // layer's (j, s) group; the owner broadcasts W_l before each forward and
+  // backward use (w2_1_f, w2_1_b), the replicas' gradients are reduced to the
+  // owner after the stage's backward (MPIReduce dw1, dw2), which accumulates
+  // and updates them alone.  With D = 1 the owner is the only replica.
+  const bool zero = M.zero != 0 && D > 1;
+  auto owner = [&](int64_t l) { return l % D; };
+  auto replica_of = [&](int r) { return ((int64_t)r / T) % D; };
+  auto wbytes = [&](int64_t l) { return k_in(l) * n_out(l) * e; };
 
-  // Parameters (C.3): W_l and a zero gradient buffer G_l per local layer;
-  // X_k on stage 0, Y_k on stage P-1.
+  // Parameters (C.3): W_l and a zero gradient buffer G_l per local layer
+  // (ZeRO: on the owner only); X_k on stage 0, Y_k on stage P-1.
   std::vector<int> Wv(W * L, -1), Gv(W * L, -1), X(W * K, -1), Y(W * K, -1);
   for (int r = 0; r < W; r++) {
     int64_t s = stage_of(r);
     for (int64_t l = lo(s); l < lo(s + 1); l++) {
-      Wv[r * L + l] = pr.new_val(r, k_in(l) * n_out(l) * e, true);
-      Gv[r * L + l] = pr.new_val(r, k_in(l) * n_out(l) * e, true);
+      if (zero && replica_of(r) != owner(l)) continue;
+      Wv[r * L + l] = pr.new_val(r, wbytes(l), true);
+      Gv[r * L + l] = pr.new_val(r, wbytes(l), true);
     }
     for (int64_t k = 0; k < K; k++) {
       if (s == 0) X[r * K + k] = pr.new_val(r, m * d * e, true);
       if (s == P - 1) Y[r * K + k] = pr.new_val(r, m * d_out(L - 1) * e, true);
     }
   }
-  // acts[(k*W + r)*(L+1) + l] = input activation of layer l (output of l-1).
-  std::vector<int> acts(K * W * (L + 1), -1);
+  // the weight of layer l each rank of stage s reads: its own, or (ZeRO) a
+  // copy broadcast from the owner of its (*, j, s) group just before use
+  auto weights = [&](int64_t l, int64_t s) {
+    std::vector<int> Wu(W, -1);
+    if (!zero) {
+      for (int r : stage_ranks(s)) Wu[r] = Wv[r * L + l];
+      return Wu;
+    }
+    for (int64_t j = 0; j < T; j++) {
+      std::vector<int> g, out;
+      const int src = (int)rank_of(c, owner(l), j, s);
+      for (int64_t i = 0; i < D; i++) {
+        const int r = (int)rank_of(c, i, j, s);
+        g.push_back(r);
+        if (r == src) { Wu[r] = Wv[r * L + l]; continue; }
+        const int v = pr.new_val(r, wbytes(l));
+        out.push_back(v);
+        Wu[r] = v;
+      }
+      emit(BROADCAST, g, {Wv[src * L + l]}, out, wbytes(l));
+    }
+    return Wu;
+  };
+  // acts[(k*W + r)*(L+1) + l] = input activation of layer l (output of l-1);
+  // racts: the same for activations recomputed in backward (checkpointing).
+  std::vector<int> acts(K * W * (L + 1), -1), racts(K * W * (L + 1), -1);
   auto act = [&](int64_t k, int r, int64_t l) -> int& { return acts[(k * W + r) * (L + 1) + l]; };
+  auto ract = [&](int64_t k, int r, int64_t l) -> int& { return racts[(k * W + r) * (L + 1) + l]; };
   std::vector<int> fwd_recv(K * W, -1), bwd_recv(K * W, -1);
 
-  // ---- the four kinds of pipeline events of one microbatch k on stage s
-  auto fwd_task = [&](int64_t k, int64_t s) {        // MatMul, [TP AllReduce], Relu
+  // one forward layer on stage s: [ZeRO Broadcast], MatMul, [TP AllReduce
+  // if row], Relu; A[r] = input activation, replaced by the output
+  auto fwd_layer = [&](int64_t s, int64_t l, std::vector<int>& A) {
     std::vector<int> R = stage_ranks(s);
-    for (int r : R) act(k, r, lo(s)) = (s == 0) ? X[r * K + k] : fwd_recv[k * W + r];
-    for (int64_t l = lo(s); l < lo(s + 1); l++) {
-      std::vector<int> Z(W, -1);
-      for (int r : R) {
-        Z[r] = pr.new_val(r, m * n_out(l) * e);
-        emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l]}, {Z[r]}, 2 * m * k_in(l) * n_out(l), true);
-      }
-      if (mode(l) == ROW) {  // partial sums -> TP AllReduce over (i, *, s)
-        for (int64_t i = 0; i < D; i++) {
-          std::vector<int> g, in, out;
-          for (int64_t j = 0; j < T; j++) {
-            int r = (int)rank_of(c, i, j, s);
-            int z2 = pr.new_val(r, m * d * e);
-            g.push_back(r); in.push_back(Z[r]); out.push_back(z2); Z[r] = z2;
-          }
-          emit(ALLREDUCE, g, in, out, m * d * e);
+    std::vector<int> Wu = weights(l, s);
+    std::vector<int> Z(W, -1);
+    for (int r : R) {
+      Z[r] = pr.new_val(r, m * n_out(l) * e);
+      emit(COMPUTE, {r}, {A[r], Wu[r]}, {Z[r]}, 2 * m * k_in(l) * n_out(l), true);
+    }
+    if (mode(l) == ROW) {  // partial sums -> TP AllReduce over (i, *, s)
+      for (int64_t i = 0; i < D; i++) {
+        std::vector<int> g, in, out;
+        for (int64_t j = 0; j < T; j++) {
+          int r = (int)rank_of(c, i, j, s);
+          int z2 = pr.new_val(r, m * d * e);
+          g.push_back(r); in.push_back(Z[r]); out.push_back(z2); Z[r] = z2;
         }
+        emit(ALLREDUCE, g, in, out, m * d * e);
       }
-      for (int r : R) {
-        int a = pr.new_val(r, m * d_out(l) * e);
-        emit(COMPUTE, {r}, {Z[r]}, {a}, m * d_out(l));  // Relu
-        act(k, r, l + 1) = a;
-      }
+    }
+    for (int r : R) {
+      int a = pr.new_val(r, m * d_out(l) * e);
+      emit(COMPUTE, {r}, {Z[r]}, {a}, m * d_out(l));  // Relu
+      A[r] = a;
+    }
+  };
+
+  // ---- the four kinds of pipeline events of one microbatch k on stage s
+  auto fwd_task = [&](int64_t k, int64_t s) {        // per layer: MatMul, [TP AllReduce], Relu
+    std::vector<int> A(W, -1);
+    for (int r : stage_ranks(s)) {
+      A[r] = (s == 0) ? X[r * K + k] : fwd_recv[k * W + r];
+      act(k, r, lo(s)) = A[r];
+    }
+    for (int64_t l = lo(s); l < lo(s + 1); l++) {
+      fwd_layer(s, l, A);
+      for (int r : stage_ranks(s)) act(k, r, l + 1) = A[r];
     }
   };
   auto fwd_send = [&](int64_t k, int64_t s) {        // stage s -> s+1
@@ -232,7 +295,7 @@ Program build_mlp(const Model& M, const Cfg& c) {
   };
   std::vector<int> Gcur = Gv;
   std::vector<int> bwd_out(K * W, -1);                // dA leaving stage s (first layer)
-  auto bwd_task = [&](int64_t k, int64_t s) {        // [LossGrad], per layer desc
+  auto bwd_task = [&](int64_t k, int64_t s) {        // [LossGrad], [recompute], per layer desc
     std::vector<int> R = stage_ranks(s);
     std::vector<int> dA(W, -1);
     for (int r : R) {
@@ -243,16 +306,31 @@ Program build_mlp(const Model& M, const Cfg& c) {
         dA[r] = bwd_recv[k * W + r];
       }
     }
+    // checkpointing: recompute the activations inside the stage
+    auto a_in = [&](int r, int64_t l) { return (ckpt && l > lo(s)) ? ract(k, r, l) : act(k, r, l); };
+    auto a_out = [&](int r, int64_t l) {
+      return (ckpt && l + 1 < lo(s + 1)) ? ract(k, r, l + 1) : act(k, r, l + 1);
+    };
+    if (ckpt) {
+      std::vector<int> A(W, -1);
+      for (int r : R) A[r] = act(k, r, lo(s));
+      for (int64_t l = lo(s); l + 1 < lo(s + 1); l++) {
+        fwd_layer(s, l, A);
+        for (int r : R) ract(k, r, l + 1) = A[r];
+      }
+    }
+    std::vector<std::vector<int>> pend(L);            // ZeRO: gradients to reduce
     for (int64_t l = lo(s + 1) - 1; l >= lo(s); l--) {
+      std::vector<int> Wu = weights(l, s);
       std::vector<int> dZ(W, -1), dW(W, -1);
       for (int r : R) {  // ReluGrad
         dZ[r] = pr.new_val(r, m * d_out(l) * e);
-        emit(COMPUTE, {r}, {act(k, r, l + 1), dA[r]}, {dZ[r]}, m * d_out(l));
+        emit(COMPUTE, {r}, {a_out(r, l), dA[r]}, {dZ[r]}, m * d_out(l));
       }
       for (int r : R) {  // MatMulGrad -> (dA_l, dW_l)
         int da = pr.new_val(r, m * k_in(l) * e);
-        dW[r] = pr.new_val(r, k_in(l) * n_out(l) * e);
-        emit(COMPUTE, {r}, {act(k, r, l), Wv[r * L + l], dZ[r]}, {da, dW[r]},
+        dW[r] = pr.new_val(r, wbytes(l));
+        emit(COMPUTE, {r}, {a_in(r, l), Wu[r], dZ[r]}, {da, dW[r]},
              4 * m * k_in(l) * n_out(l), true);
         dA[r] = da;
       }
@@ -267,10 +345,32 @@ Program build_mlp(const Model& M, const Cfg& c) {
           emit(ALLREDUCE, g, in, out, m * d * e);
         }
       }
+      if (zero) { pend[l] = dW; continue; }
       for (int r : R) {  // gradient accumulation (C.9 A20)
-        int gn = pr.new_val(r, k_in(l) * n_out(l) * e);
+        int gn = pr.new_val(r, wbytes(l));
         emit(COMPUTE, {r}, {Gcur[r * L + l], dW[r]}, {gn}, k_in(l) * n_out(l));
         Gcur[r * L + l] = gn;
+      }
+    }
+    if (zero) {  // reduce each layer's gradient to its owner, who accumulates it
+      for (int64_t l = lo(s); l < lo(s + 1); l++) {
+        std::vector<int> red(W, -1);
+        for (int64_t j = 0; j < T; j++) {
+          std::vector<int> g, in;
+          const int dst = (int)rank_of(c, owner(l), j, s);
+          for (int64_t i = 0; i < D; i++) {
+            const int r = (int)rank_of(c, i, j, s);
+            g.push_back(r); in.push_back(pend[l][r]);
+          }
+          red[dst] = pr.new_val(dst, wbytes(l));
+          emit(REDUCE, g, in, {red[dst]}, wbytes(l));
+        }
+        for (int64_t j = 0; j < T; j++) {
+          const int o = (int)rank_of(c, owner(l), j, s);
+          int gn = pr.new_val(o, wbytes(l));
+          emit(COMPUTE, {o}, {Gcur[o * L + l], red[o]}, {gn}, k_in(l) * n_out(l));
+          Gcur[o * L + l] = gn;
+        }
       }
     }
     for (int r : R) bwd_out[k * W + r] = dA[r];
@@ -356,26 +456,28 @@ Program build_mlp(const Model& M, const Cfg& c) {
       }
     }
   }
-  // Tail: DP AllReduce of the accumulated gradients, then SGD (C.9 A23).
+  // Tail: DP AllReduce of the accumulated gradients, then SGD (C.9 A23);
+  // ZeRO: the owner updates its layers alone (w1_new, w2_new of Fig. 9).
   for (int64_t s = P - 1; s >= 0; s--) {
     std::vector<int> R = stage_ranks(s);
-    if (D > 1) {
+    if (D > 1 && !zero) {
       for (int64_t l = lo(s + 1) - 1; l >= lo(s); l--) {
         for (int64_t j = 0; j < T; j++) {
           std::vector<int> g, in, out;
           for (int64_t i = 0; i < D; i++) {
             int r = (int)rank_of(c, i, j, s);
-            int v = pr.new_val(r, k_in(l) * n_out(l) * e);
+            int v = pr.new_val(r, wbytes(l));
             g.push_back(r); in.push_back(Gcur[r * L + l]); out.push_back(v);
             Gcur[r * L + l] = v;
           }
-          emit(ALLREDUCE, g, in, out, k_in(l) * n_out(l) * e);
+          emit(ALLREDUCE, g, in, out, wbytes(l));
         }
       }
     }
     for (int64_t l = lo(s); l < lo(s + 1); l++) {
       for (int r : R) {
-        int wn = pr.new_val(r, k_in(l) * n_out(l) * e, false, true);  // returned
+        if (zero && replica_of(r) != owner(l)) continue;
+        int wn = pr.new_val(r, wbytes(l), false, true);  // returned
         emit(COMPUTE, {r}, {Wv[r * L + l], Gcur[r * L + l]}, {wn}, 2 * k_in(l) * n_out(l));
       }
     }
@@ -758,7 +860,7 @@ Spec spec_from(int32_t n_model_table, const int64_t* model_table,
   // hdr: n_models, n_topos, n_world, n_batch, n_k, k_mode, dp_mask, tp_mask,
   //      pp_mask, synth_seed, synth_count; lists: the lists concatenated.
   Spec sp;
-  for (int i = 0; i < n_model_table; i++) sp.models.push_back(model_from(model_table + 11 * i));
+  for (int i = 0; i < n_model_table; i++) sp.models.push_back(model_from(model_table + 13 * i));
   for (int i = 0; i < n_topo_table; i++) sp.topos.push_back(topo_from(topo_i + 4 * i, topo_d + 12 * i));
   const int64_t* p = lists;
   sp.model_ids.assign(p, p + hdr[0]); p += hdr[0];
@@ -899,7 +1001,7 @@ int64_t oracle_enumerate(int32_t n_model_table, const int64_t* model_table,
                          int32_t n_topo_table, const int64_t* topo_i, const double* topo_d,
                          const int64_t* hdr, const int64_t* lists, int64_t cap,
                          int64_t* fields /* [cap][9]: model_slot, topo_slot, W, D, T, P, K, B, kind */,
-                         int64_t* model_out /* [cap][11] or NULL */) {
+                         int64_t* model_out /* [cap][13] or NULL */) {
   Spec sp = spec_from(n_model_table, model_table, n_topo_table, topo_i, topo_d, hdr, lists);
   std::vector<Decoded> all = enumerate(sp);
   for (int64_t i = 0; i < (int64_t)all.size() && i < cap; i++) {
@@ -909,10 +1011,10 @@ int64_t oracle_enumerate(int32_t n_model_table, const int64_t* model_table,
     f[3] = dc.c.D; f[4] = dc.c.T; f[5] = dc.c.P; f[6] = dc.c.K; f[7] = dc.c.B; f[8] = dc.M.kind;
     if (model_out) {
       const Model& M = dc.M;
-      int64_t* mo = model_out + 11 * i;
+      int64_t* mo = model_out + 13 * i;
       mo[0] = M.kind; mo[1] = M.n_layer; mo[2] = M.d_model; mo[3] = M.n_head; mo[4] = M.seq_len;
       mo[5] = M.vocab_pad; mo[6] = M.n_ctx; mo[7] = M.dtype_bytes; mo[8] = M.id_bytes; mo[9] = M.lm_head;
-      mo[10] = M.schedule;
+      mo[10] = M.schedule; mo[11] = M.recompute; mo[12] = M.zero;
     }
   }
   return (int64_t)all.size();

@@ -36,12 +36,16 @@ GPIPE = 0
 ONE_F_ONE_B = 1
 
 
-def mlp(n_layer, d_model, dtype_bytes=2, schedule=GPIPE):
+def mlp(n_layer, d_model, dtype_bytes=2, schedule=GPIPE, recompute=0, zero=0):
     """schedule: the pipeline schedule of the training transform -- GPipe
-    (north_star) or the paper's synchronous 1F1B (NEXT row f1)."""
+    (north_star) or the paper's synchronous 1F1B (NEXT row f1).
+    recompute / zero: the memory-saving variants of the Appendix (NEXT row
+    f4): gradient checkpointing (Fig. 8) and ZeRO-2/3 parameter and
+    gradient partitioning over the data-parallel replicas (Fig. 9)."""
     return dict(kind=MLP_TRAIN, n_layer=n_layer, d_model=d_model, n_head=1,
                 seq_len=1, vocab_pad=0, n_ctx=0, dtype_bytes=dtype_bytes,
-                id_bytes=8, lm_head=0, schedule=schedule)
+                id_bytes=8, lm_head=0, schedule=schedule, recompute=recompute,
+                zero=zero)
 
 
 def gpt2(n_layer, d_model, n_head, seq_len=8, vocab_pad=50304, n_ctx=1024,
@@ -49,7 +53,7 @@ def gpt2(n_layer, d_model, n_head, seq_len=8, vocab_pad=50304, n_ctx=1024,
     return dict(kind=GPT2_INFER, n_layer=n_layer, d_model=d_model,
                 n_head=n_head, seq_len=seq_len, vocab_pad=vocab_pad,
                 n_ctx=n_ctx, dtype_bytes=dtype_bytes, id_bytes=8,
-                lm_head=lm_head, schedule=GPIPE)
+                lm_head=lm_head, schedule=GPIPE, recompute=0, zero=0)
 
 
 MODELS = {
@@ -65,6 +69,12 @@ MODELS = {
     "mlp_w1_1f1b": mlp(2, 64, schedule=1),
     "mlp_1b_1f1b": mlp(16, 8192, schedule=1),
     "mlp_w4_1f1b": mlp(64, 8192, schedule=1),
+    # memory-saving variants (Appendix Figs. 8/9; NEXT row f4)
+    "mlp_w1_ckpt": mlp(2, 64, recompute=1),
+    "mlp_w1_zero": mlp(2, 64, zero=1),
+    "mlp_1b_ckpt": mlp(16, 8192, recompute=1),
+    "mlp_1b_zero": mlp(16, 8192, zero=1),
+    "mlp_1b_zero_ckpt": mlp(16, 8192, recompute=1, zero=1),
     # HF GPT-2 family (W3, BASELINE configs[2]).
     "gpt2_small": gpt2(12, 768, 12),
     "gpt2_medium": gpt2(24, 1024, 16),
