@@ -82,6 +82,18 @@ enum {
  * P:543); id_bytes = bytes per token id.  schedule (MLP training only): the
  * pipeline schedule of the D/T/P transform, DISTIR_SCHED_GPIPE (north_star)
  * or DISTIR_SCHED_1F1B (the paper's synchronous 1F1B; P <= 32).
+ * recompute / zero (MLP training only, 0 or 1, DESIGN
+ * readings R8 / R9): the memory-saving variants of the Appendix --
+ *   recompute: gradient checkpointing (Fig. 8): a stage keeps its
+ *              input and output activations; the activations inside it are
+ *              recomputed at the start of its backward, after LossGrad;
+ *   zero:      ZeRO-2/3 partitioning (Fig. 9): W_l and its gradient
+ *              live on replica l mod D of its (tp, stage) group, which
+ *              broadcasts W_l before each forward / backward use and
+ *              receives the gradients by a reduce after the stage's backward;
+ *              GPipe only (DISTIR_E_UNSUPPORTED with 1F1B), and configs with
+ *              D > 1 need next_pow2(pp) * dp <= 32 (DISTIR_E_UNSUPPORTED).
+ *              Broadcast / Reduce cost (g-1) alpha + bytes / bw.
  * Unused fields are ignored. */
 enum { DISTIR_SCHED_GPIPE = 0, DISTIR_SCHED_1F1B = 1 };
 typedef struct {
@@ -89,6 +101,7 @@ typedef struct {
   int32_t n_layer, d_model, n_head, seq_len, vocab_pad, n_ctx;
   int32_t dtype_bytes, id_bytes, lm_head;
   int32_t schedule;
+  int32_t recompute, zero;
 } distir_model;
 
 /* Hardware description ("GPU DRAM bandwidth, kernel launch overhead,

@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 class distir_model(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
-        "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule")]
+        "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule", "recompute", "zero")]
 
 
 class distir_topology(ctypes.Structure):
@@ -194,7 +194,7 @@ def _check(status):
 def model_struct(m) -> distir_model:
     return distir_model(*[int(m.get(k, 0)) for k in (
         "kind", "n_layer", "d_model", "n_head", "seq_len", "vocab_pad",
-        "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule")])
+        "n_ctx", "dtype_bytes", "id_bytes", "lm_head", "schedule", "recompute", "zero")])
 
 
 def topo_struct(t) -> distir_topology:

@@ -17,13 +17,14 @@ constexpr int kMaxK = 64;           // top-k width
 constexpr int kMaxRanks = 8;        // GPUs merged by the all-gather
 constexpr int kNumBuckets = 4096;   // hash slots for warp-shape buckets
 constexpr int kOverflowBucket = kNumBuckets;  // catch-alls: + kind (1 config / warp)
-constexpr int kBucketSlots = kNumBuckets + 3;   // + MLP, GPT-2, MLP-1F1B catch-alls
+constexpr int kBucketSlots = kNumBuckets + 4;   // + MLP, GPT-2, MLP-1F1B, MLP-ZeRO catch-alls
 // Simulate kernels ("groups"): model kind x schedule mode.  Modes 0-2: one
 // lane walks a whole configuration in program order, P <= 1 / 2 / 4 stages;
 // modes 3-4: wavefront, one lane per stage (mode 4: two stages per lane,
 // 32 < P <= 64, and the catch-all buckets); mode 5 (MLP only): the 1F1B
-// co-simulation, one lane per stage, P <= 32.
-constexpr int kModes = 6;
+// co-simulation, one lane per stage, P <= 32; mode 6 (MLP only): ZeRO (f4),
+// one lane per (stage, replica), next_pow2(P) * D <= 32.
+constexpr int kModes = 7;
 constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr int kMaxSplit = 5;        // configs per item divided by up to 2^5
@@ -45,6 +46,7 @@ enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };
 
 struct DModel {          // distir_model, int32
   int32_t kind, L, d, h, S, V, nctx, e, ide, lm, sched;
+  int32_t rc, zero;      // f4: gradient checkpointing, ZeRO-2/3 (MLP training)
 };
 
 struct DTopo {           // distir_topology
@@ -81,7 +83,8 @@ struct SpecBlock {
   int64_t n_total;                    // configs of the whole grid
   int32_t rank, n_ranks;              // shard: global i = rank + q * n_ranks
   int64_t n_local;
-  int32_t f1b;                        // any 1F1B model in use (launch mode 5)
+  int32_t f1b;                        // extra simulate kernels: bit 0 1F1B (mode 5),
+                                      // bit 1 ZeRO (mode 6)
   DModel models[kMaxModels];          // handle tables
   DTopo topos[kMaxTopos];
 };
@@ -100,7 +103,8 @@ struct WsHeader {
 };
 
 struct Bucket {          // per hash slot (plus one overflow slot)
-  uint32_t key;          // kind | (P-1) << 1 | (L-1) << 7 | min(K,255) << 17
+  uint32_t key;          // kind | (P-1) << 1 | (L-1) << 7 | min(K,255) << 17 |
+                         // sched << 25 | log2(D) << 26 | ZeRO << 29 | recompute << 30
   uint32_t count;        // configs in the bucket
   uint32_t cfg_base;     // first position in perm
   uint32_t item_base;    // first work item

@@ -193,6 +193,11 @@ distir_status validate_model(const distir_model& m, int i) {
   if (m.kind == DISTIR_MODEL_MLP_TRAIN && m.schedule != DISTIR_SCHED_GPIPE &&
       m.schedule != DISTIR_SCHED_1F1B)
     return bad("schedule");
+  if (m.kind == DISTIR_MODEL_MLP_TRAIN && ((m.recompute != 0 && m.recompute != 1) ||
+                                           (m.zero != 0 && m.zero != 1)))
+    return bad("recompute / zero must be 0 or 1");
+  if (m.kind == DISTIR_MODEL_MLP_TRAIN && m.zero && m.schedule != DISTIR_SCHED_GPIPE)
+    return fail(DISTIR_E_UNSUPPORTED, "model " + std::to_string(i) + ": ZeRO needs the GPipe schedule");
   if (m.d_model > (1 << 20)) return fail(DISTIR_E_UNSUPPORTED, "d_model > 2^20");
   if (m.kind == DISTIR_MODEL_GPT2_INFER) {
     if (m.n_head < 1 || m.seq_len < 1 || m.vocab_pad < 1 || m.n_ctx < 0 || m.id_bytes < 1)
@@ -269,13 +274,17 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
   if (g->n_batch < 1 || g->n_batch > 32) return fail(DISTIR_E_INVALID_ARG, "spec.n_batch");
   if (g->n_k < 0 || g->n_k > 16) return fail(DISTIR_E_INVALID_ARG, "spec.n_k");
   if (g->k_mode != 0 && g->k_mode != 1) return fail(DISTIR_E_INVALID_ARG, "spec.k_mode");
-  bool any_1f1b = false;
-  for (int mi = 0; mi < g->n_models; mi++) any_1f1b |= sim->models[g->models[mi]].sched == 1;
+  bool any_1f1b = false, any_zero = false;
+  for (int mi = 0; mi < g->n_models; mi++) {
+    any_1f1b |= sim->models[g->models[mi]].sched == 1;
+    any_zero |= sim->models[g->models[mi]].kind == 0 && sim->models[g->models[mi]].zero != 0;
+  }
   for (int i = 0; i < g->n_world; i++) {
     if (!is_pow2(g->world[i]) || (i && g->world[i] <= g->world[i - 1]))
       return fail(DISTIR_E_INVALID_ARG, "spec.world: ascending powers of two");
     if (g->world[i] > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
     if (any_1f1b && g->world[i] > 32) return fail(DISTIR_E_UNSUPPORTED, "1F1B with world size > 32");
+    if (any_zero && g->world[i] > 32) return fail(DISTIR_E_UNSUPPORTED, "ZeRO with world size > 32");
   }
   for (int i = 0; i < g->n_batch; i++) {
     if (g->batch[i] < 1 || (i && g->batch[i] <= g->batch[i - 1]))
@@ -291,7 +300,7 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     if (g->k_set[i] > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
   }
   sp.k_mode = g->k_mode;
-  sp.f1b = any_1f1b ? 1 : 0;
+  sp.f1b = (any_1f1b ? 1 : 0) | (any_zero ? 2 : 0);
   sp.n_k = g->n_k;
   for (int i = 0; i < g->n_k; i++) sp.k_set[i] = g->k_set[i];
   sp.n_batch = g->n_batch;
@@ -333,6 +342,11 @@ distir_status validate_configs(const distir_sim* sim, const distir_config* cf, i
     if ((int64_t)c.dp * c.tp * c.pp > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
     if (sim->models[c.model].sched == 1 && c.pp > 32)
       return fail(DISTIR_E_UNSUPPORTED, "1F1B with more than 32 stages");
+    if (sim->models[c.model].kind == 0 && sim->models[c.model].zero && c.dp > 1) {
+      int64_t p2 = 1;
+      while (p2 < c.pp) p2 <<= 1;
+      if (p2 * c.dp > 32) return fail(DISTIR_E_UNSUPPORTED, "ZeRO needs next_pow2(pp) * dp <= 32");
+    }
     if (c.microbatches > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
     if (!work_fits(sim->models[c.model], c.batch))
       return fail(DISTIR_E_UNSUPPORTED, "per-op work overflows int64");
@@ -440,7 +454,8 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
 #endif
     DISTIR_SIM(0, 3); DISTIR_SIM(0, 4); DISTIR_SIM(1, 3); DISTIR_SIM(1, 4);
     kernels += 4;
-    if (sp.f1b) { DISTIR_SIM(0, 5); kernels++; }
+    if (sp.f1b & 1) { DISTIR_SIM(0, 5); kernels++; }
+    if (sp.f1b & 2) { DISTIR_SIM(0, 6); kernels++; }
 #undef DISTIR_SIM
   }
   CUDA_TRY(mark(2));
@@ -584,7 +599,11 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
     for (size_t i = 0; i < sim->topos.size(); i++) sp.topos[i] = sim->topos[i];
     sp.mode = MODE_EXPLICIT;
     n_total = n_configs;
-    for (int64_t i = 0; i < n_configs && !sp.f1b; i++) sp.f1b = sim->models[configs[i].model].sched;
+    for (int64_t i = 0; i < n_configs; i++) {
+      const DModel& M = sim->models[configs[i].model];
+      if (M.kind == 0 && M.sched == 1) sp.f1b |= 1;
+      if (M.kind == 0 && M.zero && configs[i].dp > 1) sp.f1b |= 2;
+    }
   }
   sp.n_total = n_total;
   sp.rank = rank;
@@ -655,7 +674,9 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
     const distir_model& m = models[i];
     sim->models.push_back(DModel{m.kind, m.n_layer, m.d_model, m.n_head, m.seq_len, m.vocab_pad,
                                  m.n_ctx, m.dtype_bytes, m.id_bytes, m.lm_head,
-                                 m.kind == DISTIR_MODEL_MLP_TRAIN ? m.schedule : 0});
+                                 m.kind == DISTIR_MODEL_MLP_TRAIN ? m.schedule : 0,
+                                 m.kind == DISTIR_MODEL_MLP_TRAIN ? m.recompute : 0,
+                                 m.kind == DISTIR_MODEL_MLP_TRAIN ? m.zero : 0});
   }
   for (int i = 0; i < n_topos; i++) {
     const distir_topology& t = topos[i];
@@ -672,8 +693,9 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   const void* fns[kGroups] = {
       (const void*)k_simulate<0, 0>, (const void*)k_simulate<0, 1>, (const void*)k_simulate<0, 2>,
       (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<0, 5>,
+      (const void*)k_simulate<0, 6>,
       (const void*)k_simulate<1, 0>, (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>,
-      (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr};
+      (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr, nullptr};
   for (int g = 0; g < kGroups && e == cudaSuccess; g++) {
     if (!fns[g]) continue;
     const int smem = sim_smem(g / kModes, g % kModes);

@@ -174,56 +174,79 @@ struct Seg {
 
 // Per-task cache for one binade: the x increment of the whole task from an
 // even / odd significand (+inf: the task never fits this binade), the
-// binade's bounds [lo, hi) = [2^E, 2^(E+1)) (lo = +inf: no binade cached),
-// and each segment's per-pass ulp increments (R[2i], R[2i+1]; kNever if a
-// pass never fits), either in caller-provided per-lane storage or in a
-// per-configuration binade table (BinTab) shared by the configuration's lanes.
+// binade's bounds [2^E, 2^(E+1)) as high words of their bit patterns
+// (lo = INT32_MAX: no binade cached), and each segment's per-pass ulp
+// increments (R[2i], R[2i+1]; kNever if a pass never fits) in
+// caller-provided per-lane storage.
 struct TaskCache {
   int32_t ef;
+  int32_t lo, hi;
   double Su0, Su1;
-  double lo, hi;
   double* R;
-  double* own;          // per-lane storage for binades outside the table
 };
 
-// Per-pass increments of NS segments for the binades [e0, e0 + nb), filled
-// cooperatively by a configuration's lanes before its walk (binade b at
-// tab + b * 2 * NS); nb = 0 disables the table.
+#ifdef __CUDA_ARCH__
+DISTIR_HD int32_t hiword(double x) { return __double2hiint(x); }
+DISTIR_HD int32_t loword(double x) { return __double2loint(x); }
+#else
+DISTIR_HD int32_t hiword(double x) { return (int32_t)(d2bits(x) >> 32); }
+DISTIR_HD int32_t loword(double x) { return (int32_t)d2bits(x); }
+#endif
+
+// Per-pass increments of a configuration's nu distinct segment op lists for
+// the binades [e0, e0 + nb), filled cooperatively by the configuration's
+// lanes before its walk (binade b, list u at tab[(b * nu + u) * 2]); a task
+// cache reads its segments through a map (segment i -> list map[i]).
+// nb = 0 disables the table.
 struct BinTab {
   double* tab;
-  int32_t e0, nb;
+  int32_t e0, nb, nu;
 };
 
 DISTIR_HD TaskCache task_cache_make(double* store) {
-  return TaskCache{-1, kInf(), kInf(), kInf(), kInf(), store, store};
+  return TaskCache{-1, 0x7FFFFFFF, 0, kInf(), kInf(), store};
 }
 
-// Fill binades e0 + first, e0 + first + stride, ... of a table of NS
-// segments (the segments' op lists; reps are ignored).
-template <int NS>
-DISTIR_HD void bintab_fill(const BinTab& t, const Seg (&sg)[NS], int first, int stride) {
+// Fill binades e0 + first, e0 + first + stride, ... of a table of the NU
+// distinct op lists (reps are ignored).
+template <int NU>
+DISTIR_HD void bintab_fill(const BinTab& t, const Seg (&u)[NU], int first, int stride) {
   for (int b = first; b < t.nb; b += stride) {
     const int32_t ef = t.e0 + b;
 #pragma unroll
-    for (int i = 0; i < NS; i++) {
+    for (int i = 0; i < NU; i++) {
       double R0 = kNever, R1 = kNever;
-      if (!(ef >= 53 && ef <= 1993) || !seg_pass(sg[i].a, sg[i].n, ef, R0, R1)) R0 = R1 = kNever;
-      t.tab[(int64_t)b * 2 * NS + 2 * i] = R0;
-      t.tab[(int64_t)b * 2 * NS + 2 * i + 1] = R1;
+      if (!(ef >= 53 && ef <= 1993) || !seg_pass(u[i].a, u[i].n, ef, R0, R1)) R0 = R1 = kNever;
+      t.tab[((int64_t)b * NU + i) * 2] = R0;
+      t.tab[((int64_t)b * NU + i) * 2 + 1] = R1;
     }
   }
 }
 
-// Move the cache to binade field ef: per-pass increments from the table when
-// it covers ef, else computed into the lane's own storage; then the task's
-// total increments from each parity (closed forms of reps_total).
+// Identity segment map (segment i is distinct op list i).
 template <int NS>
-DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS], const BinTab& t) {
+struct IdMap {
+  int v[NS];
+  DISTIR_HD constexpr IdMap() : v() {
+    for (int i = 0; i < NS; i++) v[i] = i;
+  }
+};
+
+// Move the cache to binade field ef: per-pass increments copied from the
+// table when it covers ef, else computed; then the task's total increments
+// from each parity (closed forms of reps_total).
+template <int NS>
+DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS], const BinTab& t,
+                            const int (&map)[NS]) {
   DISTIR_COUNT(2);
   if (ef - t.e0 >= 0 && ef - t.e0 < t.nb) {
-    c.R = t.tab + (int64_t)(ef - t.e0) * 2 * NS;
+    const double* row = t.tab + (int64_t)(ef - t.e0) * t.nu * 2;
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      c.R[2 * i] = row[2 * map[i]];
+      c.R[2 * i + 1] = row[2 * map[i] + 1];
+    }
   } else {
-    c.R = c.own;
 #pragma unroll
     for (int i = 0; i < NS; i++) {
       double R0 = kNever, R1 = kNever;
@@ -248,25 +271,27 @@ DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS], const
   }
   const double u = bits2d((int64_t)(ef - 52) << 52);
   c.ef = ef;
-  c.lo = bits2d((int64_t)ef << 52);
-  c.hi = bits2d((int64_t)(ef + 1) << 52);
+  c.lo = ef << 20;                // high word of 2^E
+  c.hi = (ef + 1) << 20;          // high word of 2^(E+1)
   c.Su0 = (ok && T[0] < kTwo53d) ? xmul(T[0], u) : kInf();     // exact
   c.Su1 = (ok && T[1] < kTwo53d) ? xmul(T[1], u) : kInf();
 }
 template <int NS>
 DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
-  task_refresh(c, ef, sg, BinTab{nullptr, 0, 0});
+  constexpr IdMap<NS> id;
+  task_refresh(c, ef, sg, BinTab{nullptr, 0, 0, 0}, id.v);
 }
 
 // Fast path of a task: when x lies in the cached binade and the whole task
 // stays inside it, x <- x + Su (exact) and true; otherwise x is untouched
 // and false.  x >= 2^E and x + Su < 2^(E+1) is exactly "x in binade E and
-// the rounded sum keeps x's exponent" (Su >= 0; +inf never fits).
+// the rounded sum keeps x's exponent" (Su >= 0; +inf never fits); for
+// non-negative doubles both are 32-bit compares of the high words.
 // Branch-free (the caller branches once, warp-uniformly, on the rare misses).
 DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
-  const double Su = (d2bits(x) & 1) ? c.Su1 : c.Su0;
+  const double Su = (loword(x) & 1) ? c.Su1 : c.Su0;
   const double y = xadd(x, Su);
-  const bool ok = x >= c.lo && y < c.hi;
+  const bool ok = hiword(x) >= c.lo && hiword(y) < c.hi;
   x = ok ? y : x;
   return ok;
 }
@@ -277,12 +302,13 @@ DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
 // walk when the binade has ties), the pass that leaves the binade is done op
 // by op, and the cache follows x into the new binade.
 template <int NS>
-DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t) {
+DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t,
+                             const int (&map)[NS]) {
   DISTIR_COUNT(0);
   {
     const int32_t ef = exp_field(x);
     if (x > 0.0 && ef >= 53 && ef <= 1993) {
-      if (ef != c.ef) task_refresh(c, ef, sg, t);
+      if (ef != c.ef) task_refresh(c, ef, sg, t, map);
       if (task_fast(x, c)) { DISTIR_COUNT(1); return; }
     }
   }
@@ -293,7 +319,7 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
       const int64_t xb = d2bits(x);
       const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
       if (x > 0.0 && ef >= 53 && ef <= 1993) {
-        if (ef != c.ef) task_refresh(c, ef, sg, t);
+        if (ef != c.ef) task_refresh(c, ef, sg, t, map);
         const double R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
         if (R0 < kNever) {
           int64_t M = (xb & kMant) | kHidden;
@@ -335,7 +361,8 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
 
 template <int NS>
 DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c) {
-  add_task(x, sg, c, BinTab{nullptr, 0, 0});
+  constexpr IdMap<NS> id;
+  add_task(x, sg, c, BinTab{nullptr, 0, 0, 0}, id.v);
 }
 
 // ------------------------------------------------------------------ memory --

@@ -87,13 +87,13 @@ __device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t 
     c.K = (c.P == 1) ? 1 : (1ll << (1 + r[3] % 5));
     c.B = 1ll << (7 + r[4] % 12);
     if ((r[0] & 1) == 0) {
-      c.M = DModel{0, (int32_t)(1 << (1 + r[5] % 6)), (int32_t)(1 << (8 + r[6] % 7)), 1, 1, 0, 0, 2, 8, 0, 0};
+      c.M = DModel{0, (int32_t)(1 << (1 + r[5] % 6)), (int32_t)(1 << (8 + r[6] % 7)), 1, 1, 0, 0, 2, 8, 0, 0, 0, 0};
     } else {
       const int q = (int)(r[5] % 4);
       const int32_t L = q == 0 ? 12 : q == 1 ? 24 : q == 2 ? 36 : 48;
       const int32_t d = q == 0 ? 768 : q == 1 ? 1024 : q == 2 ? 1280 : 1600;
       const int32_t h = q == 0 ? 12 : q == 1 ? 16 : q == 2 ? 20 : 25;
-      c.M = DModel{1, L, d, h, 8, 50304, 1024, 2, 8, 1, 0};
+      c.M = DModel{1, L, d, h, 8, 50304, 1024, 2, 8, 1, 0, 0, 0};
     }
     c.topo = sp.topo_ids[r[7] % (uint64_t)sp.n_topos];
     return;
@@ -136,6 +136,24 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
   if (c.M.kind == 0) {
     events = 5 * K * D * T * L + D * T * L + K * D * T + tp * K * D * L + 2 * K * D * T * (P - 1) + dp * T * L;
     steps = K * (5 * L + tp * L + 1 + 2 * (P - 1)) + L * (1 + dp);
+    // f4 (tests/test_oracle_f4.py op-count closed forms): checkpointing
+    // recomputes every layer but each stage's last (MatMul, Relu, a TP
+    // AllReduce for row layers); ZeRO adds per microbatch and layer two
+    // Broadcasts and a Reduce per TP index, Adds / SGDs on the owner only
+    // and no DP AllReduce
+    int64_t rec = 0, rows = 0;
+    if (c.M.rc) {
+      rec = L - P;
+      for (int64_t l = 1; l < L; l += 2) rows++;
+      for (int64_t s = 0; s < P; s++) rows -= (((s + 1) * L / P - 1) & 1);
+      steps += K * (2 * rec + tp * rows);
+    }
+    const int64_t ck = K * (2 * D * T * rec + tp * D * rows);
+    if (c.M.zero && D > 1) {
+      events += -(D - 1) * K * T * L - (D - 1) * T * L - T * L + 3 * K * T * L + K * T * rec;
+      steps += K * (3 * L + rec) - L;
+    }
+    events += ck;
   } else {
     const int64_t lm = c.M.lm != 0;
     events = 12 * K * D * T * L + (2 + lm) * K * D * T + tp * K * D * (2 * L + 1 + lm) + K * D * T * (P - 1);
@@ -143,10 +161,15 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
   }
 }
 
+// ZeRO with D > 1 runs its own kernel (mode 6) with D lanes per stage
+__device__ __forceinline__ bool is_zero(const Cfg& c) { return c.M.kind == 0 && c.M.zero && c.D > 1; }
+
 __device__ __forceinline__ uint32_t bucket_key(const Cfg& c) {
   const uint32_t K = (uint32_t)(c.K < 255 ? c.K : 255);
+  const uint32_t z = is_zero(c) ? 1u : 0u;
+  const uint32_t ld = z ? (uint32_t)(63 - __clzll((unsigned long long)c.D)) : 0u;
   return (uint32_t)c.M.kind | (uint32_t)(c.P - 1) << 1 | (uint32_t)(c.M.L - 1) << 7 | K << 17 |
-         (uint32_t)(c.M.sched & 1) << 25;
+         (uint32_t)(c.M.sched & 1) << 25 | ld << 26 | z << 29 | (uint32_t)(c.M.rc & 1) << 30;
 }
 
 // ------------------------------------------------------------ costs (C.5) ---
@@ -272,7 +295,7 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
     ev += events; st += steps; nv += 1;
     const uint32_t key = bucket_key(c);
     uint32_t slot = (key * 2654435761u) >> 20;                 // 12-bit hash
-    uint32_t found = kOverflowBucket + (c.M.sched ? 2u : (uint32_t)c.M.kind);
+    uint32_t found = kOverflowBucket + (is_zero(c) ? 3u : c.M.sched ? 2u : (uint32_t)c.M.kind);
     for (int probe = 0; probe < kNumBuckets; probe++) {
       const uint32_t sl = (slot + probe) & (kNumBuckets - 1);
       uint32_t cur = *(volatile uint32_t*)&bk[sl].key;
@@ -338,8 +361,10 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
       lanes = 32;
       cls = kNumClasses - 1;
       // MLP / GPT-2 catch-alls run two stages per lane (any P <= 64); the
-      // 1F1B catch-all (P <= 32 by validation) one stage per lane
-      group = b == kOverflowBucket + 2 ? 5 : (uint32_t)(b - kOverflowBucket) * kModes + 4;
+      // 1F1B catch-all (P <= 32 by validation) one stage per lane; the ZeRO
+      // catch-all one (stage, replica) per lane
+      group = b == kOverflowBucket + 3 ? 6
+            : b == kOverflowBucket + 2 ? 5 : (uint32_t)(b - kOverflowBucket) * kModes + 4;
     } else {
       const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, K = (B.key >> 17) & 255;
       uint32_t mode;
@@ -348,6 +373,10 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
         lanes = 1;
         mode = P == 1 ? 0 : (P == 2 ? 1 : 2);
         est = (unsigned long long)K * P * (kind ? 1ull : 2ull);
+      } else if ((B.key >> 29) & 1) {    // ZeRO: D lanes per stage
+        lanes = pow2ceil32(P) << ((B.key >> 26) & 7);
+        mode = 6;
+        est = (2ull * K + P) * 4;
       } else {
         lanes = P < 32 ? pow2ceil32(P) : 32;
         mode = (B.key >> 25) & 1 ? 5 : P > 32 ? 4 : 3;
@@ -443,7 +472,7 @@ __host__ __device__ constexpr int sim_v(int mode) {
   return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : mode == 4 ? 2 : 1;
 }
 __host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per lane row
-  return kind == 1 ? 19 + 6 * sim_v(mode) : 15 + 14 * sim_v(mode);
+  return kind == 1 ? 19 + 6 * sim_v(mode) : mode == 6 ? 43 : 15 + 20 * sim_v(mode);
 }
 __host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per block
   return sim_row(kind, mode) * 8 * 128 <= 48 * 1024 ? 128 : 64;
@@ -452,7 +481,8 @@ __host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per
 // kTabCfgs configurations of a warp (S >= 2 lanes each) get one, filled by
 // their lanes before the walk: binades x 2 parities x segments doubles.
 __host__ __device__ constexpr int sim_tab(int kind, int mode) {   // doubles per config
-  return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3 : kTabBinadesMlp * 2 * 7;
+  return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3
+                     : kTabBinadesMlp * 2 * (mode == 6 ? 9 : 7);
 }
 __host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic smem bytes
   return 8 * (sim_tpb(kind, mode) * sim_row(kind, mode) +
@@ -510,7 +540,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
     if (has) {
       decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);
     } else {
-      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0};
+      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0};
       c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
     }
     const DTopo& tp = sp.topos[c.topo];
@@ -521,7 +551,11 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
     const long long t0 = clock64();
 #endif
     if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk);
-    else run_mlp<V, SEQ, MODE == 5>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+    else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk);
+    else if (warp_max_int(has ? c.M.rc : 0))          // bucket key: warp-uniform
+      run_mlp<V, SEQ, MODE == 5, true>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+    else
+      run_mlp<V, SEQ, MODE == 5, false>(c, tp, has, sl, S, lane, row, tab, ms, pk);
 #ifdef DISTIR_INSTR
     if (lane == 0) {
       const unsigned long long dt = (unsigned long long)(clock64() - t0);

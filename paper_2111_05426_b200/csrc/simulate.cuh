@@ -17,13 +17,13 @@
 // to an upper bound of the makespan (P stages x the busiest stage's total
 // work, doubled for rounding slack), capped at nb_max binades.  `work` is
 // this lane's total work; the max runs over the configuration's S lanes.
-__device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, double cmin, double work,
-                                               int64_t P, int S) {
+__device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, int nu, double cmin,
+                                               double work, int64_t P, int S) {
   for (int o = S >> 1; o > 0; o >>= 1) {
     work = fmax(work, __shfl_xor_sync(0xffffffffu, work, o));
     cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
   }
-  BinTab t{tab, 0, 0};
+  BinTab t{tab, 0, 0, nu};
   if (tab != nullptr && cmin > 0.0 && cmin < kInf()) {
     const int32_t e0 = exp_field(cmin);
     const int32_t e1 = exp_field(__dmul_rn(work, 2.0 * (double)P)) + 1;
@@ -34,6 +34,12 @@ __device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, double c
   return t;
 }
 __device__ __forceinline__ double min_pos(double m, double x) { return x > 0.0 && x < m ? x : m; }
+
+// Segment -> distinct-op-list maps of the task caches (BinTab).
+__device__ constexpr int kMapId3[3] = {0, 1, 2};
+// MLP backward: LossGrad, recompute (the forward lists), layers (desc)
+__device__ constexpr int kMapMlpBwd[7] = {3, 0, 1, 2, 4, 5, 6};
+__device__ constexpr int kMapMlpBwd4[4] = {3, 4, 5, 6};          // without checkpointing
 
 __device__ __forceinline__ MemProf mem_alt(MemProf A, MemProf B, int p0, int n) {
   if (n <= 0) return mem_id();
@@ -56,7 +62,7 @@ __device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, in
   a = Seg{row + oa, na, n1 & 1};
 }
 
-template <int V, bool SEQ, bool F1B>
+template <int V, bool SEQ, bool F1B, bool RC>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                         double* row, double* tab, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
@@ -103,6 +109,15 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   const MemProf lf_a = mem_then(mem_op(m * nout.a * e, 0), mem_op(m * dout.a * e, m * dout.a * e));
   const MemProf lf_b = mem_then(mem_then(mem_op(m * nout.b * e, 0), mem_op(ar_b, ar_b)),
                                 mem_op(m * dout.b * e, m * dout.b * e));
+  // checkpointing (f4, Fig. 8; RC = the model's `recompute`, warp-uniform):
+  // a forward layer inside the stage frees its input activation at its
+  // MatMul (backward uses the recomputed one)
+  constexpr bool rc = RC;
+  constexpr int NB = RC ? 7 : 4;               // backward task segments
+  const MemProf lfk_a = mem_then(mem_op(m * nout.a * e, m * kin.a * e),
+                                 mem_op(m * dout.a * e, m * dout.a * e));
+  const MemProf lfk_b = mem_then(mem_then(mem_op(m * nout.b * e, m * kin.b * e), mem_op(ar_b, ar_b)),
+                                 mem_op(m * dout.b * e, m * dout.b * e));
   auto lb = [&](int p, bool first, bool dead0) -> MemProf {
     const int64_t act_b = m * dout[p] * e, din = m * kin[p] * e;
     const bool col_ar = p == 0 && T > 1;
@@ -139,13 +154,18 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if (ok[q] && s[q] == 0) lv += K * mde;                       // X_k
     if (ok[q] && s[q] == P - 1) lv += K * m * dlast * e;         // Y_k
     live[q] = ok[q] ? lv : 0; peak[q] = live[q]; clk[q] = 0.0;
-    pf[q] = mem_alt(lf_a, lf_b, lo[q] & 1, nl);
+    if (rc && nl > 0) {
+      pf[q] = mem_then(lo[q] & 1 ? lf_b : lf_a, mem_alt(lfk_a, lfk_b, (lo[q] + 1) & 1, nl - 1));
+    } else {
+      pf[q] = mem_alt(lf_a, lf_b, lo[q] & 1, nl);
+    }
     MemProf b = (ok[q] && s[q] == P - 1) ? mem_op(m * dlast * e, m * dlast * e) : mem_id();
+    if (rc && nl > 1) b = mem_then(b, mem_alt(lf_a, lf_b, lo[q] & 1, nl - 1));   // recompute
     if (nl > 1) b = mem_then(b, mem_alt(lb_a, lb_b, (hi[q] - 1) & 1, nl - 1));
     if (nl > 0) b = mem_then(b, lb(lo[q] & 1, true, s[q] == 0 && lo[q] == 0));
     pb[q] = b;
-    cf[q] = task_cache_make(row + 15 + 14 * q);      // 3 fwd segments
-    cb[q] = task_cache_make(row + 15 + 14 * q + 6);  // 4 bwd segments
+    cf[q] = task_cache_make(row + 15 + 20 * q);      // 3 fwd segments
+    cb[q] = task_cache_make(row + 15 + 20 * q + 6);  // 7 bwd segments
   }
 
   // task segments; the op lists are the same on every lane of the
@@ -153,14 +173,16 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   auto fsegs = [&](int q, Seg (&sg)[3]) {
     alt_segs(row, 0, 3, lo[q] & 1, hi[q] - lo[q], sg[0], sg[1], sg[2]);
   };
-  auto bsegs = [&](int q, Seg (&sg)[4]) {                      // LossGrad, layers desc
+  auto bsegs = [&](int q, Seg (&sg)[NB]) {    // LossGrad, [recompute], layers desc
     sg[0] = Seg{row + 14, 1, s[q] == P - 1 ? 1 : 0};
-    alt_segs(row, 6, 4, (hi[q] - 1) & 1, hi[q] - lo[q], sg[1], sg[2], sg[3]);
+    const int nl = hi[q] - lo[q];
+    if constexpr (RC) alt_segs(row, 0, 3, lo[q] & 1, nl > 1 ? nl - 1 : 0, sg[1], sg[2], sg[3]);
+    alt_segs(row, 6, 4, (hi[q] - 1) & 1, nl, sg[NB - 3], sg[NB - 2], sg[NB - 1]);
   };
-  BinTab btf{nullptr, 0, 0}, btb{nullptr, 0, 0};
+  BinTab btf{nullptr, 0, 0, 0};
   if constexpr (!SEQ) {
-    // binade tables of the forward / backward task segments, filled by the
-    // configuration's lanes (forward at tab, backward after it)
+    // binade table of the 7 distinct op lists (forward b / ab / a,
+    // LossGrad, backward b / ab / a), filled by the configuration's lanes
     double cmin = kInf(), work = 0.0;
     for (int j = 0; j < 15; j++) cmin = min_pos(cmin, row[j]);
 #pragma unroll
@@ -169,17 +191,16 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       cmin = min_pos(min_pos(cmin, sendf[q]), sendb[q]);
       double lay = 0.0;
       for (int j = 0; j < 14; j++) lay = lay + row[j];
-      const double w = (double)(hi[q] - lo[q]) * lay + row[14] + sendf[q] + sendb[q];
+      const double w = (double)(hi[q] - lo[q]) * (rc ? 2.0 : 1.0) * lay + row[14] + sendf[q] + sendb[q];
       work = fmax(work, w * (double)K);
     }
-    btf = bintab_range(has ? tab : nullptr, kTabBinadesMlp, cmin, work, P, S);
-    btb = btf;
-    btb.tab = btf.tab ? btf.tab + kTabBinadesMlp * 6 : nullptr;
-    Seg f[3], g[4];
+    btf = bintab_range(has ? tab : nullptr, kTabBinadesMlp, 7, cmin, work, P, S);
+    Seg f[3], g[NB], u[7];
     fsegs(0, f);
     bsegs(0, g);
-    bintab_fill(btf, f, sl, S);
-    bintab_fill(btb, g, sl, S);
+    u[0] = f[0]; u[1] = f[1]; u[2] = f[2]; u[3] = g[0];
+    u[4] = g[NB - 3]; u[5] = g[NB - 2]; u[6] = g[NB - 1];
+    bintab_fill(btf, u, sl, S);
     __syncwarp();
   }
   auto fwd_task = [&](int q, bool act) {
@@ -192,7 +213,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if (any && slow) {
       Seg sg[3];
       fsegs(q, sg);
-      add_task(clk[q], sg, cf[q], btf);
+      add_task(clk[q], sg, cf[q], btf, kMapId3);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -204,9 +225,10 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
-      Seg sg[4];
+      Seg sg[NB];
       bsegs(q, sg);
-      add_task(clk[q], sg, cb[q], btb);
+      if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd);
+      else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -340,39 +362,42 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
   const unsigned int K2 = (unsigned int)(2 * K);
   bool up[V], dn[V];
+  double recvf[V], recvb[V];
 #pragma unroll
   for (int q = 0; q < V; q++) {
     up[q] = ok[q] && s[q] < P - 1;
     dn[q] = ok[q] && s[q] > 0;
+    const int64_t r0 = T * D * (int64_t)s[q];
+    // costs of the Sends this stage receives: activation from s-1 (its last
+    // layer is lo - 1), gradient from s+1 (its first layer is hi)
+    recvf[q] = dn[q] ? cost_send(m * dout[(lo[q] - 1) & 1] * e, group_intra(r0 - T * D, r0, ns), tp) : 0.0;
+    recvb[q] = up[q] ? cost_send(m * kin[hi[q] & 1] * e, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
   }
+  // Each Send ends at max(sender, receiver clock) + cost on both ends
+  // (P:119); both ends compute it from the other's shuffled clock.
   // ---- forward wavefront: task (k, s) at step 2k + s, then Send s -> s+1
   {
     int kk[V];
 #pragma unroll
     for (int q = 0; q < V; q++) kk[q] = -s[q];
     for (int w = 0; w < nsteps; w++) {
-      bool act[V];
+      bool act[V], rcv[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
         act[q] = ok[q] && (unsigned int)kk[q] < K2 && !(kk[q] & 1);
+        rcv[q] = dn[q] && (unsigned int)(kk[q] + 1) < K2 && (kk[q] & 1);   // stage s-1 sent
         kk[q]++;
         fwd_task(q, act[q]);
       }
-      // Send s -> s+1: both ends wait for each other; the end
-      // time travels back to the receiver (-1 = nothing sent)
-      double nb[V], t[V];
-      Nbr<V>::up_stage(clk, nb, lane);
+      double nbu[V], nbd[V];
+      Nbr<V>::up_stage(clk, nbu, lane);
+      Nbr<V>::down_stage(clk, nbd, lane);
 #pragma unroll
       for (int q = 0; q < V; q++) {
-        const bool snd = act[q] && up[q];
-        const double end = dadd(fmax(clk[q], nb[q]), sendf[q]);
-        clk[q] = snd ? end : clk[q];
-        t[q] = snd ? end : -1.0;
+        const bool sd = act[q] && up[q];
+        const double nc = dadd(fmax(clk[q], sd ? nbu[q] : nbd[q]), sd ? sendf[q] : recvf[q]);
+        clk[q] = (sd || rcv[q]) ? nc : clk[q];
       }
-      double tin[V];
-      Nbr<V>::down_stage(t, tin, lane);
-#pragma unroll
-      for (int q = 0; q < V; q++) clk[q] = (dn[q] && tin[q] >= 0.0) ? tin[q] : clk[q];
     }
   }
   // ---- backward wavefront: task (k, s) at step 2k + (P-1-s), then Send s -> s-1
@@ -381,26 +406,23 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 #pragma unroll
     for (int q = 0; q < V; q++) kk[q] = -(int)(P - 1 - s[q]);
     for (int w = 0; w < nsteps; w++) {
-      bool act[V];
+      bool act[V], rcv[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
         act[q] = ok[q] && (unsigned int)kk[q] < K2 && !(kk[q] & 1);
+        rcv[q] = up[q] && (unsigned int)(kk[q] + 1) < K2 && (kk[q] & 1);   // stage s+1 sent
         kk[q]++;
         bwd_task(q, act[q]);
       }
-      double nb[V], t[V];
-      Nbr<V>::down_stage(clk, nb, lane);
+      double nbu[V], nbd[V];
+      Nbr<V>::up_stage(clk, nbu, lane);
+      Nbr<V>::down_stage(clk, nbd, lane);
 #pragma unroll
       for (int q = 0; q < V; q++) {
-        const bool snd = act[q] && dn[q];
-        const double end = dadd(fmax(clk[q], nb[q]), sendb[q]);
-        clk[q] = snd ? end : clk[q];
-        t[q] = snd ? end : -1.0;
+        const bool sd = act[q] && dn[q];
+        const double nc = dadd(fmax(clk[q], sd ? nbd[q] : nbu[q]), sd ? sendb[q] : recvb[q]);
+        clk[q] = (sd || rcv[q]) ? nc : clk[q];
       }
-      double tin[V];
-      Nbr<V>::up_stage(t, tin, lane);
-#pragma unroll
-      for (int q = 0; q < V; q++) clk[q] = (up[q] && tin[q] >= 0.0) ? tin[q] : clk[q];
     }
   }
   }  // wavefront
@@ -549,7 +571,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     sg[1] = Seg{row + 2, 14, nb[q]};
     sg[2] = Seg{row + 16, 3, s[q] == P - 1 ? 1 : 0};
   };
-  BinTab bt{nullptr, 0, 0};
+  BinTab bt{nullptr, 0, 0, 0};
   if constexpr (!SEQ) {
     // binade table of the task segments, filled by the configuration's lanes
     double cmin = kInf(), work = 0.0;
@@ -563,7 +585,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       w = w + row[0] + row[1] + row[16] + row[17] + row[18] + sendf[q];
       work = fmax(work, w * (double)K);
     }
-    bt = bintab_range(has ? tab : nullptr, kTabBinadesGpt2, cmin, work, P, S);
+    bt = bintab_range(has ? tab : nullptr, kTabBinadesGpt2, 3, cmin, work, P, S);
     Seg sg[3];
     segs(0, sg);
     bintab_fill(bt, sg, sl, S);
@@ -579,7 +601,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     if (any && slow) {
       Seg sg[3];
       segs(q, sg);
-      add_task(clk[q], sg, tc[q], bt);
+      add_task(clk[q], sg, tc[q], bt, kMapId3);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -613,41 +635,43 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     const MemProf p1 = mem_then(mem_then(rv, ptask1[q]), sd);
     mem_apply(live[q], peak[q], mem_then(mem_rep(p0, K - 1), p1));
   }
-  // wavefront: task (k, s) at step 2k + s, then Send s -> s+1
+  // wavefront: task (k, s) at step 2k + s, then Send s -> s+1.  Sender
+  // and receiver both wait for each other and end at
+  // max(their clocks) + cost; each computes it from the other's clock
+  // (both neighbours' clocks are shuffled independently), bit-identically.
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
   bool up[V], dn[V];
   int kk[V];
+  double recvc[V];
   const unsigned int K2 = (unsigned int)(2 * K);
 #pragma unroll
   for (int q = 0; q < V; q++) {
     up[q] = ok[q] && s[q] < P - 1;
     dn[q] = ok[q] && s[q] > 0;
     kk[q] = -s[q];
+    const int64_t r0 = T * D * (int64_t)s[q];
+    recvc[q] = dn[q] ? cost_send(nde, group_intra(r0 - T * D, r0, ns), tp) : 0.0;  // Send s-1 -> s
   }
   for (int w = 0; w < nsteps; w++) {
     if (lane == 0) DISTIR_COUNT(4);
-    bool act[V];
+    bool act[V], rcv[V];
 #pragma unroll
     for (int q = 0; q < V; q++) {
       act[q] = ok[q] && (unsigned int)kk[q] < K2 && !(kk[q] & 1);
+      rcv[q] = dn[q] && (unsigned int)(kk[q] + 1) < K2 && (kk[q] & 1);   // stage s-1 sent
       kk[q]++;
       task(q, act[q], false);
     }
-    // Send s -> s+1: both ends wait for each other; the end
-    // time travels back to the receiver (-1 = nothing sent)
-    double nbv[V], t[V];
-    Nbr<V>::up_stage(clk, nbv, lane);
+    double nbu[V], nbd[V];
+    Nbr<V>::up_stage(clk, nbu, lane);
+    Nbr<V>::down_stage(clk, nbd, lane);
 #pragma unroll
     for (int q = 0; q < V; q++) {
-      const bool snd = act[q] && up[q];
-      const double end = dadd(fmax(clk[q], nbv[q]), sendf[q]);
-      clk[q] = snd ? end : clk[q];
-      t[q] = snd ? end : -1.0;
+      const bool sd = act[q] && up[q];
+      const double o = sd ? nbu[q] : nbd[q];
+      const double nc = dadd(fmax(clk[q], o), sd ? sendf[q] : recvc[q]);
+      clk[q] = (sd || rcv[q]) ? nc : clk[q];
     }
-    double tin[V];
-    Nbr<V>::down_stage(t, tin, lane);
-#pragma unroll
-    for (int q = 0; q < V; q++) clk[q] = (dn[q] && tin[q] >= 0.0) ? tin[q] : clk[q];
   }
   }  // wavefront
   double msx = 0.0;
@@ -658,4 +682,221 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   }
   ms_out = msx;
   peak_out = pkx;
+}
+
+// --------------------------------------- MLP training with ZeRO (row f4) ----
+// ZeRO-2/3 (Fig. 9; DESIGN reading R9): W_l and its gradient live on
+// replica l mod D of each (j, s) group.  Lane = (stage s, replica i), sl =
+// i + D * s (S = next_pow2(P) * D lanes per configuration); all TP ranks of
+// a replica run the same ops (Theorem 2 within the replica).  The replicas
+// of a stage differ only by owner-only ops (gradient Add, SGD), and every
+// forward / backward task starts with a Broadcast that synchronises them:
+// a segment max over the D lanes (exact), after which the task's ops are
+// the same on every replica -- including the Reduce / Add chain, because
+// each Reduce waits for the previous owner's Add (max(x + add, x) = x + add,
+// RN is monotone) -- up to the final Add, which only its owner performs.
+// Sends pair replica i of neighbouring stages (lanes D apart).
+__device__ constexpr int kMapZeroBwd[9] = {3, 0, 1, 2, 4, 5, 6, 7, 8};
+
+__device__ __forceinline__ double cost_chain(int64_t g, int64_t bytes, bool intra, const DTopo& t) {
+  // Broadcast from / Reduce to the owner: a pipelined chain over the g
+  // members, (g-1) alpha + bytes / bw (g = 2: a Send, as in Fig. 9)
+  const double a = intra ? t.a_intra : t.a_inter, bw = intra ? t.bw_intra : t.bw_inter;
+  return __dadd_rn(__dmul_rn(__ll2double_rn(g - 1), a), __ddiv_rn(__ll2double_rn(bytes), bw));
+}
+
+__device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
+                             double* row, double* tab, double& ms_out, int64_t& peak_out) {
+  const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
+  const int64_t m = has ? c.B / (D * K) : 0;
+  const int32_t ns = tp.node_size;
+  const bool rc = c.M.rc != 0;
+  const Par<int64_t> kin{d, d / T}, nout{d / T, d}, dout{d / T, d};
+  const bool tp_intra = group_intra(0, T - 1, ns);
+  const bool dp_intra = group_intra(0, T * (D - 1), ns);
+  const int64_t w = kin.a * nout.a;              // == kin.b * nout.b (d^2 / T)
+  const int64_t Wb = w * e;
+  const int64_t mde = m * d * e;
+  const double ar_tp = T > 1 ? cost_allreduce(T, mde, tp_intra, tp) : 0.0;
+  const int64_t ar_b = T > 1 ? mde : 0;
+  const int64_t dlast = dout[(L - 1) & 1];
+  const double bc = D > 1 ? cost_chain(D, Wb, dp_intra, tp) : 0.0;   // Broadcast == Reduce
+  {
+    auto mm_f = [&](int64_t ki, int64_t no) { return cost_op(2 * m * w, (m * ki + w + m * no) * e, true, tp); };
+    auto mm_b = [&](int64_t ki, int64_t no) {
+      return cost_op(4 * m * w, (2 * m * ki + 2 * w + m * no) * e, true, tp);
+    };
+    row[0] = bc; row[1] = mm_f(kin.a, nout.a); row[2] = 0.0;
+    row[3] = cost_op(m * dout.a, 2 * m * dout.a * e, false, tp);
+    row[4] = bc; row[5] = mm_f(kin.b, nout.b); row[6] = ar_tp;
+    row[7] = cost_op(m * dout.b, 2 * m * dout.b * e, false, tp);
+    row[8] = bc; row[9] = cost_op(m * dout.a, 3 * m * dout.a * e, false, tp);
+    row[10] = mm_b(kin.a, nout.a); row[11] = ar_tp;
+    row[12] = bc; row[13] = cost_op(m * dout.b, 3 * m * dout.b * e, false, tp);
+    row[14] = mm_b(kin.b, nout.b); row[15] = 0.0;
+    row[16] = cost_op(3 * m * dlast, 3 * m * dlast * e, false, tp);            // LossGrad
+    row[17] = bc;                                                            // Reduce
+    row[18] = cost_op(w, 3 * w * e, false, tp);                              // Add (owner)
+  }
+  const double sgd = cost_op(2 * w, 3 * w * e, false, tp);
+
+  // D is the same for every configuration of the warp (bucket key); padding
+  // lanes take it from the warp so every shuffle is warp-uniform
+  const int Di = warp_max_int(has ? (int)D : 1);
+  const int ri = sl % Di, st = sl / Di;            // replica, stage
+  const bool ok = has && st < P;
+  const int lo = ok ? (int)((int64_t)st * L / P) : 0;
+  const int hi = ok ? (int)((int64_t)(st + 1) * L / P) : 0;
+  const int nl = hi - lo;
+  const int64_t r0 = T * D * (int64_t)st;
+  const double sendf = (ok && st < P - 1)
+                           ? cost_send(m * dout[(hi - 1) & 1] * e, group_intra(r0, r0 + T * D, ns), tp)
+                           : 0.0;
+  const double sendb = (ok && st > 0) ? cost_send(m * kin[lo & 1] * e, group_intra(r0 - T * D, r0, ns), tp)
+                                      : 0.0;
+  // ---- live memory of replica ri (C.7), composed exactly (Theorem 4)
+  auto own = [&](int l) { return (l % Di) == ri; };
+  auto lfz = [&](int l, bool free_in) -> MemProf {          // [Bcast], MatMul, [AR], Relu
+    const int p = l & 1;
+    const int64_t cp = own(l) ? 0 : Wb;                     // the received copy
+    MemProf r = mem_op(cp, 0);
+    r = mem_then(r, mem_op(m * nout[p] * e, cp + (free_in ? m * kin[p] * e : 0)));
+    if (p == 1) r = mem_then(r, mem_op(ar_b, ar_b));
+    return mem_then(r, mem_op(m * dout[p] * e, m * dout[p] * e));
+  };
+  int64_t live = 0;
+  for (int l = lo; l < hi; l++) live += own(l) ? 2 * Wb : 0;
+  if (ok && st == 0) live += K * mde;                        // X_k
+  if (ok && st == P - 1) live += K * m * dlast * e;          // Y_k
+  if (!ok) live = 0;
+  int64_t peak = live;
+  MemProf pf = mem_id(), pb = mem_id(), tail = mem_id();
+  for (int l = lo; l < hi; l++) pf = mem_then(pf, lfz(l, rc && l > lo));
+  if (ok && st == P - 1) pb = mem_op(m * dlast * e, m * dlast * e);                 // LossGrad
+  if (rc)
+    for (int l = lo; l + 1 < hi; l++) pb = mem_then(pb, lfz(l, false));           // recompute
+  for (int l = hi - 1; l >= lo; l--) {
+    const int p = l & 1;
+    const int64_t cp = own(l) ? 0 : Wb;
+    const int64_t act_b = m * dout[p] * e, din = m * kin[p] * e;
+    const bool first = l == lo, dead0 = st == 0 && l == 0, col_ar = p == 0 && T > 1;
+    pb = mem_then(pb, mem_op(cp, 0));                                              // Broadcast
+    pb = mem_then(pb, mem_op(act_b, 2 * act_b));                                   // ReluGrad
+    pb = mem_then(pb, mem_op(din + Wb, act_b + cp + (first ? din : 0) +
+                                           ((dead0 && T == 1) ? din : 0)));        // MatMulGrad
+    pb = mem_then(pb, mem_op(col_ar ? mde : 0, col_ar ? mde + (dead0 ? mde : 0) : 0));  // TP AR
+  }
+  for (int l = lo; l < hi; l++) {
+    pb = mem_then(pb, own(l) ? mem_op(Wb, Wb) : mem_op(0, Wb));                     // Reduce
+    if (own(l)) pb = mem_then(pb, mem_op(Wb, 2 * Wb));                             // Add
+  }
+  for (int l = lo; l < hi; l++)
+    if (own(l)) tail = mem_then(tail, mem_op(Wb, 2 * Wb));                         // SGD
+  {
+    const MemProf ra = st > 0 ? mem_op(m * kin[lo & 1] * e, 0) : mem_id();
+    const MemProf rg = st < P - 1 ? mem_op(m * dout[(hi - 1) & 1] * e, 0) : mem_id();
+    const MemProf sg = st > 0 ? mem_op(0, m * kin[lo & 1] * e) : mem_id();
+    if (ok)
+      mem_apply(live, peak, mem_then(mem_then(mem_rep(mem_then(ra, pf), K),
+                                              mem_rep(mem_then(mem_then(rg, pb), sg), K)), tail));
+  }
+
+  // ---- task segments and the binade table of the 9 distinct op lists
+  TaskCache cf = task_cache_make(row + 19), cb = task_cache_make(row + 25);
+  auto fsegs = [&](Seg (&sg)[3]) { alt_segs(row, 0, 4, lo & 1, nl, sg[0], sg[1], sg[2]); };
+  auto bsegs = [&](Seg (&sg)[9]) {          // LossGrad, recompute, layers desc, Reduce / Add
+    sg[0] = Seg{row + 16, 1, (ok && st == P - 1) ? 1 : 0};
+    alt_segs(row, 0, 4, lo & 1, (rc && nl > 1) ? nl - 1 : 0, sg[1], sg[2], sg[3]);
+    alt_segs(row, 8, 4, (hi - 1) & 1, nl, sg[4], sg[5], sg[6]);
+    sg[7] = Seg{row + 17, 2, nl > 0 ? nl - 1 : 0};
+    sg[8] = Seg{row + 17, 1, nl > 0 ? 1 : 0};
+  };
+  BinTab bt{nullptr, 0, 0, 0};
+  {
+    double cmin = kInf(), work = 0.0;
+    for (int j = 0; j < 19; j++) cmin = min_pos(cmin, row[j]);
+    if (ok) {
+      cmin = min_pos(min_pos(cmin, sendf), sendb);
+      double lay = 0.0;
+      for (int j = 0; j < 19; j++) lay = lay + row[j];
+      work = (double)nl * (rc ? 2.0 : 1.0) * lay * (double)K + (sendf + sendb) * (double)K;
+    }
+    bt = bintab_range(has ? tab : nullptr, kTabBinadesMlp, 9, cmin, work, P, S);
+    Seg f[3], g[9], u[9];
+    fsegs(f);
+    bsegs(g);
+    u[0] = f[0]; u[1] = f[1]; u[2] = f[2];
+    for (int j = 3; j < 9; j++) u[j] = g[j == 3 ? 0 : j];
+    bintab_fill(bt, u, sl, S);
+    __syncwarp();
+  }
+  double clk = 0.0;
+  // the D replicas of a stage synchronise (Broadcast): exact segment max
+  auto segmax = [&](double x) {
+    for (int o = 1; o < Di; o <<= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+  };
+  auto fwd_task = [&](bool act) {
+    const double mx = segmax(clk);
+    if (act) clk = mx;
+    const bool slow = act && !task_fast(clk, cf);
+    const bool any = __any_sync(0xffffffffu, slow);
+    if (any && slow) {
+      Seg sg[3];
+      fsegs(sg);
+      add_task(clk, sg, cf, bt, kMapId3);
+    }
+  };
+  auto bwd_task = [&](bool act) {
+    const double mx = segmax(clk);
+    if (act) clk = mx;
+    const bool slow = act && !task_fast(clk, cb);
+    const bool any = __any_sync(0xffffffffu, slow);
+    if (any && slow) {
+      Seg sg[9];
+      bsegs(sg);
+      add_task(clk, sg, cb, bt, kMapZeroBwd);
+    }
+    if (act && own(hi - 1)) clk = dadd(clk, row[18]);       // the last Add: owner only
+  };
+  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  const unsigned int K2 = (unsigned int)(2 * K);
+  const bool up = ok && st < P - 1, dn = ok && st > 0;
+  // costs of the Sends this lane receives (replica ri of stage st -/+ 1)
+  const double recvf = dn ? cost_send(m * dout[(lo - 1) & 1] * e, group_intra(r0 - T * D, r0, ns), tp) : 0.0;
+  const double recvb = up ? cost_send(m * kin[hi & 1] * e, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
+  {   // forward wavefront: task (k, s) at step 2k + s, then Send s -> s+1
+    int kk = -st;
+    for (int wv = 0; wv < nsteps; wv++) {
+      const bool act = ok && (unsigned int)kk < K2 && !(kk & 1);
+      const bool rcv = dn && (unsigned int)(kk + 1) < K2 && (kk & 1);
+      kk++;
+      fwd_task(act);
+      const double nbu = __shfl_down_sync(0xffffffffu, clk, Di);
+      const double nbd = __shfl_up_sync(0xffffffffu, clk, Di);
+      const bool sd = act && up;
+      const double nc = dadd(fmax(clk, sd ? nbu : nbd), sd ? sendf : recvf);
+      clk = (sd || rcv) ? nc : clk;
+    }
+  }
+  {   // backward wavefront: task (k, s) at step 2k + (P-1-s), then Send s -> s-1
+    int kk = -(int)(P - 1 - st);
+    for (int wv = 0; wv < nsteps; wv++) {
+      const bool act = ok && (unsigned int)kk < K2 && !(kk & 1);
+      const bool rcv = up && (unsigned int)(kk + 1) < K2 && (kk & 1);
+      kk++;
+      bwd_task(act);
+      const double nbu = __shfl_down_sync(0xffffffffu, clk, Di);
+      const double nbd = __shfl_up_sync(0xffffffffu, clk, Di);
+      const bool sd = act && dn;
+      const double nc = dadd(fmax(clk, sd ? nbd : nbu), sd ? sendb : recvb);
+      clk = (sd || rcv) ? nc : clk;
+    }
+  }
+  // tail: the owner updates its layers (SGD); no DP AllReduce under ZeRO
+  if (ok)
+    for (int l = lo; l < hi; l++)
+      if (own(l)) clk = dadd(clk, sgd);
+  ms_out = ok ? clk : 0.0;
+  peak_out = ok ? peak : 0;
 }

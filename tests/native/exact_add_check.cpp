@@ -38,19 +38,24 @@ static long check(std::mt19937_64& g, int trials, int mode) {
     TaskCache c = task_cache_make(cstore);
     // half of the trials use a binade table (BinTab) covering a random range
     // around the clocks; binades outside it fall back to the lane's storage
+    // (the table holds the segments' op lists in reverse order, read back
+    // through a segment map)
     static double tstore[64 * 2 * NS];
-    BinTab tb{tstore, 0, 0};
+    BinTab tb{tstore, 0, 0, NS};
+    int map[NS];
+    Seg rev[NS];
+    for (int i = 0; i < NS; i++) { map[i] = NS - 1 - i; rev[NS - 1 - i] = sg[i]; }
     if (g() & 1) {
       tb.e0 = 1023 - 45 + (int)(g() % 40);
       tb.nb = 1 + (int)(g() % 64);
-      bintab_fill(tb, sg, 0, 1);
+      bintab_fill(tb, rev, 0, 1);
     }
     const int tasks = 1 + (int)(g() % 40);
     for (int k = 0; k < tasks; k++) {
       for (int i = 0; i < NS; i++)
         for (int64_t r = 0; r < sg[i].reps; r++)
           for (int j = 0; j < sg[i].n; j++) x = x + sg[i].a[j];
-      if ((g() & 1) || !task_fast(y, c)) add_task(y, sg, c, tb);   // as the kernels do
+      if ((g() & 1) || !task_fast(y, c)) add_task(y, sg, c, tb, map);   // as the kernels do
       if (std::memcmp(&x, &y, 8) != 0) {
         if (bad < 5) std::printf("mismatch NS=%d mode=%d task=%d plain=%a agg=%a\n", NS, mode, k, x, y);
         bad++;

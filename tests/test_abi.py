@@ -40,7 +40,7 @@ def test_struct_layouts():
     import paper_2111_05426_b200 as pkg
     assert ctypes.sizeof(pkg.distir_config) == 32
     assert ctypes.sizeof(pkg.distir_topk_entry) == 32
-    assert ctypes.sizeof(pkg.distir_model) == 44
+    assert ctypes.sizeof(pkg.distir_model) == 52      # 13 x int32
     assert ctypes.sizeof(pkg.distir_topology) == 120
     assert pkg.TOPK_DTYPE.itemsize == 32
 
