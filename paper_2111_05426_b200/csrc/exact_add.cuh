@@ -96,6 +96,12 @@ DISTIR_HD int odd(double integral) { return (int)((int64_t)integral & 1); }
 
 constexpr int kSegMax = 14;   // longest op sequence of a segment (GPT-2 block)
 
+#ifdef __CUDA_ARCH__
+DISTIR_HD float fdiv_approx(float a, float b) { return __fdividef(a, b); }
+#else
+DISTIR_HD float fdiv_approx(float a, float b) { return a / b; }
+#endif
+
 DISTIR_HD void seq_plain(double& x, const double* a, int n) {
 #if DISTIR_UNROLL_SEG
 #pragma unroll
@@ -110,7 +116,7 @@ DISTIR_HD void seq_plain(double& x, const double* a, int n) {
 // an odd (R1) significand.  Returns false when the pass can never fit the
 // binade (an op of at least 2^52 ulps).  Exact: a*2^k is exact, floor/rint of
 // such a double are exact, and sums of integers below 2^53 are exact.
-DISTIR_HD bool seg_pass(const double* a, int n, int32_t ef, double& R0, double& R1) {
+DISTIR_HD bool seg_pass_d(const double* a, int n, int32_t ef, double& R0, double& R1) {
   const double inv_u = bits2d((int64_t)(2098 - ef) << 52);    // 2^(52-E)
   double R = 0.0;
   bool tie = false, never = false;
@@ -149,20 +155,29 @@ DISTIR_HD bool seg_pass(const double* a, int n, int32_t ef, double& R0, double& 
   return R0 < kTwo53d && R1 < kTwo53d;
 }
 
+// The per-pass increments as integers (exact: they are integers < 2^53);
+// kNeverI marks a pass that never fits a binade.
+constexpr int64_t kNeverI = int64_t(1) << 60;
+DISTIR_HD bool seg_pass(const double* a, int n, int32_t ef, int64_t& R0, int64_t& R1) {
+  double r0, r1;
+  if (!seg_pass_d(a, n, ef, r0, r1)) { R0 = R1 = kNeverI; return false; }
+  R0 = (int64_t)r0;
+  R1 = (int64_t)r1;
+  return true;
+}
+
 // Total ulps of n passes from significand parity p (the parity sequence has
-// period <= 2); kNever when it cannot fit a binade.
-DISTIR_HD double reps_total(double R0, double R1, int p, int64_t n) {
-  const double Ra = p ? R1 : R0, Rb = p ? R0 : R1;
+// period <= 2); kNeverI when it cannot fit a binade.  Integer arithmetic:
+// R < 2^53 and n <= 2^10 (passes per segment <= layers per stage <= 1024),
+// so no product overflows.
+DISTIR_HD int64_t reps_total(int64_t R0, int64_t R1, int p, int64_t n) {
+  const int64_t Ra = p ? R1 : R0, Rb = p ? R0 : R1;
   if (n == 1) return Ra;
-  const double dn = (double)n;
-  double s;
-  if (!odd(Ra)) s = xmul(dn, Ra);                              // parity stays
-  else if (!odd(Rb)) s = xadd(Ra, xmul(dn - 1.0, Rb));         // flips once
-  else {                                                        // alternates
-    const double h = (double)(n >> 1);
-    s = xadd(xmul(dn - h, Ra), xmul(h, Rb));
-  }
-  return s < kTwo53d ? s : kNever;                              // monotone rounding
+  int64_t s;
+  if (!(Ra & 1)) s = n * Ra;                                    // parity stays
+  else if (!(Rb & 1)) s = Ra + (n - 1) * Rb;                    // flips once
+  else s = (n - (n >> 1)) * Ra + (n >> 1) * Rb;                 // alternates
+  return s < kTwo53 ? s : kNeverI;                              // monotone rounding
 }
 
 // A task is a list of segments: `reps` passes over the op costs a[0..n).
@@ -182,7 +197,7 @@ struct TaskCache {
   int32_t ef;
   int32_t lo, hi;
   double Su0, Su1;
-  double* R;
+  int64_t* R;
 };
 
 #ifdef __CUDA_ARCH__
@@ -199,11 +214,11 @@ DISTIR_HD int32_t loword(double x) { return (int32_t)d2bits(x); }
 // cache reads its segments through a map (segment i -> list map[i]).
 // nb = 0 disables the table.
 struct BinTab {
-  double* tab;
+  int64_t* tab;
   int32_t e0, nb, nu;
 };
 
-DISTIR_HD TaskCache task_cache_make(double* store) {
+DISTIR_HD TaskCache task_cache_make(int64_t* store) {
   return TaskCache{-1, 0x7FFFFFFF, 0, kInf(), kInf(), store};
 }
 
@@ -215,8 +230,8 @@ DISTIR_HD void bintab_fill(const BinTab& t, const Seg (&u)[NU], int first, int s
     const int32_t ef = t.e0 + b;
 #pragma unroll
     for (int i = 0; i < NU; i++) {
-      double R0 = kNever, R1 = kNever;
-      if (!(ef >= 53 && ef <= 1993) || !seg_pass(u[i].a, u[i].n, ef, R0, R1)) R0 = R1 = kNever;
+      int64_t R0 = kNeverI, R1 = kNeverI;
+      if (!(ef >= 53 && ef <= 1993) || !seg_pass(u[i].a, u[i].n, ef, R0, R1)) R0 = R1 = kNeverI;
       t.tab[((int64_t)b * NU + i) * 2] = R0;
       t.tab[((int64_t)b * NU + i) * 2 + 1] = R1;
     }
@@ -240,7 +255,7 @@ DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS], const
                             const int (&map)[NS]) {
   DISTIR_COUNT(2);
   if (ef - t.e0 >= 0 && ef - t.e0 < t.nb) {
-    const double* row = t.tab + (int64_t)(ef - t.e0) * t.nu * 2;
+    const int64_t* row = t.tab + (int64_t)(ef - t.e0) * t.nu * 2;
 #pragma unroll
     for (int i = 0; i < NS; i++) {
       c.R[2 * i] = row[2 * map[i]];
@@ -249,32 +264,32 @@ DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS], const
   } else {
 #pragma unroll
     for (int i = 0; i < NS; i++) {
-      double R0 = kNever, R1 = kNever;
-      if (sg[i].reps > 0 && !seg_pass(sg[i].a, sg[i].n, ef, R0, R1)) R0 = R1 = kNever;
+      int64_t R0 = kNeverI, R1 = kNeverI;
+      if (sg[i].reps > 0) seg_pass(sg[i].a, sg[i].n, ef, R0, R1);
       c.R[2 * i] = R0;
       c.R[2 * i + 1] = R1;
     }
   }
-  double T[2] = {0.0, 0.0};
+  int64_t T[2] = {0, 0};
   bool ok = true;
 #pragma unroll
   for (int i = 0; i < NS; i++) {
     if (sg[i].reps <= 0) continue;
-    const double R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
-    if (!(R0 < kNever)) { ok = false; continue; }
+    const int64_t R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
+    if (R0 >= kNeverI) { ok = false; continue; }
 #pragma unroll
     for (int p = 0; p < 2; p++) {
-      const int pe = p ^ odd(T[p]);                 // parity entering segment i
-      const double s = reps_total(R0, R1, pe, sg[i].reps);
-      T[p] = s < kNever ? xadd(T[p], s) : kNever;
+      const int pe = p ^ (int)(T[p] & 1);           // parity entering segment i
+      const int64_t s = reps_total(R0, R1, pe, sg[i].reps);
+      T[p] = s < kNeverI ? T[p] + s : kNeverI;      // (< 2^60: no overflow)
     }
   }
   const double u = bits2d((int64_t)(ef - 52) << 52);
   c.ef = ef;
   c.lo = ef << 20;                // high word of 2^E
   c.hi = (ef + 1) << 20;          // high word of 2^(E+1)
-  c.Su0 = (ok && T[0] < kTwo53d) ? xmul(T[0], u) : kInf();     // exact
-  c.Su1 = (ok && T[1] < kTwo53d) ? xmul(T[1], u) : kInf();
+  c.Su0 = (ok && T[0] < kTwo53) ? xmul((double)T[0], u) : kInf();     // exact
+  c.Su1 = (ok && T[1] < kTwo53) ? xmul((double)T[1], u) : kInf();
 }
 template <int NS>
 DISTIR_HD void task_refresh(TaskCache& c, int32_t ef, const Seg (&sg)[NS]) {
@@ -294,6 +309,16 @@ DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
   const bool ok = hiword(x) >= c.lo && hiword(y) < c.hi;
   x = ok ? y : x;
   return ok;
+}
+// The same, for a lane that runs the task only when `act`: evaluated
+// unconditionally (no divergent branch), applied under `act`; true when the
+// task still has to be performed (act and not fast).
+DISTIR_HD bool task_fast_or_slow(double& x, const TaskCache& c, bool act) {
+  const double Su = (loword(x) & 1) ? c.Su1 : c.Su0;
+  const double y = xadd(x, Su);
+  const bool ok = act && hiword(x) >= c.lo && hiword(y) < c.hi;
+  x = ok ? y : x;
+  return act && !ok;
 }
 
 // x <- every addition of the task, in order, computed exactly: the cache is
@@ -320,16 +345,16 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
       const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
       if (x > 0.0 && ef >= 53 && ef <= 1993) {
         if (ef != c.ef) task_refresh(c, ef, sg, t, map);
-        const double R0 = c.R[2 * i], R1 = c.R[2 * i + 1];
-        if (R0 < kNever) {
+        const int64_t r0 = c.R[2 * i], r1 = c.R[2 * i + 1];
+        if (r0 < kNeverI) {
           int64_t M = (xb & kMant) | kHidden;
-          const int64_t r0 = (int64_t)R0, r1 = (int64_t)R1;
           const int64_t before = reps;
           if (r0 == r1) {                            // no tie: closed form
             const int64_t avail = kTwo53 - 1 - M;
             int64_t fit = reps;                      // min(reps, avail / r0)
-            if (r0 > 0 && (double)reps * (double)r0 > (double)avail) {   // reps <= 2^10
-              fit = (int64_t)((float)avail / (float)r0);
+            if (r0 > 0 && reps * r0 > avail) {       // (reps <= 2^10, r0 < 2^53)
+              // estimate (relative error ~2^-21, fit < reps <= 2^10), corrected below
+              fit = (int64_t)fdiv_approx((float)avail, (float)r0);
               if (fit > reps) fit = reps;
               if (fit < 0) fit = 0;
             }

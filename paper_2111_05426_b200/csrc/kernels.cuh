@@ -423,17 +423,29 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
     B.item_off = atomicAdd(&s_items[B.group][B.cls], (B.count + cpw - 1) / cpw);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // item numbering: group-major, heaviest class first (per-group prefix by
+  // one thread per group, then the group offsets)
+  __shared__ unsigned int s_gsum[kGroups];
+  if (threadIdx.x < kGroups) {
+    const int g = threadIdx.x;
     unsigned int base = 0;
-    for (int g = 0; g < kGroups; g++) {
-      hdr->group_begin[g] = base;
-      hdr->item_counter[g] = 0;
-      for (int c = kNumClasses - 1; c >= 0; c--) { s_base[g][c] = base; base += s_items[g][c]; }
+    for (int c = kNumClasses - 1; c >= 0; c--) { s_base[g][c] = base; base += s_items[g][c]; }
+    s_gsum[g] = base;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGroups) {
+    const int g = threadIdx.x;
+    unsigned int off = 0;
+    for (int h = 0; h < g; h++) off += s_gsum[h];
+    for (int c = 0; c < kNumClasses; c++) s_base[g][c] += off;
+    hdr->group_begin[g] = off;
+    hdr->item_counter[g] = 0;
+    if (g == kGroups - 1) {
+      hdr->group_begin[kGroups] = off + s_gsum[g];
+      hdr->n_items = off + s_gsum[g];
+      hdr->n_buckets = s_nb;
+      hdr->cfg_total = s_cfg;
     }
-    hdr->group_begin[kGroups] = base;
-    hdr->n_items = base;
-    hdr->n_buckets = s_nb;
-    hdr->cfg_total = s_cfg;
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {

@@ -23,7 +23,7 @@ __device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, int nu, 
     work = fmax(work, __shfl_xor_sync(0xffffffffu, work, o));
     cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
   }
-  BinTab t{tab, 0, 0, nu};
+  BinTab t{reinterpret_cast<int64_t*>(tab), 0, 0, nu};
   if (tab != nullptr && cmin > 0.0 && cmin < kInf()) {
     const int32_t e0 = exp_field(cmin);
     const int32_t e1 = exp_field(__dmul_rn(work, 2.0 * (double)P)) + 1;
@@ -34,6 +34,8 @@ __device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, int nu, 
   return t;
 }
 __device__ __forceinline__ double min_pos(double m, double x) { return x > 0.0 && x < m ? x : m; }
+// per-lane shared-memory storage reused for integer per-pass increments
+__device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int64_t*>(p); }
 
 // Segment -> distinct-op-list maps of the task caches (BinTab).
 __device__ constexpr int kMapId3[3] = {0, 1, 2};
@@ -164,8 +166,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if (nl > 1) b = mem_then(b, mem_alt(lb_a, lb_b, (hi[q] - 1) & 1, nl - 1));
     if (nl > 0) b = mem_then(b, lb(lo[q] & 1, true, s[q] == 0 && lo[q] == 0));
     pb[q] = b;
-    cf[q] = task_cache_make(row + 15 + 20 * q);      // 3 fwd segments
-    cb[q] = task_cache_make(row + 15 + 20 * q + 6);  // 7 bwd segments
+    cf[q] = task_cache_make(i64(row + 15 + 20 * q));      // 3 fwd segments
+    cb[q] = task_cache_make(i64(row + 15 + 20 * q + 6));  // 7 bwd segments
   }
 
   // task segments; the op lists are the same on every lane of the
@@ -207,7 +209,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if constexpr (SEQ || F1B) {
       if (act) mem_apply(live[q], peak[q], pf[q]);
     }
-    const bool slow = act && !task_fast(clk[q], cf[q]);
+    const bool slow = task_fast_or_slow(clk[q], cf[q], act);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
@@ -221,7 +223,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if constexpr (SEQ || F1B) {
       if (act) mem_apply(live[q], peak[q], pb[q]);
     }
-    const bool slow = act && !task_fast(clk[q], cb[q]);
+    const bool slow = task_fast_or_slow(clk[q], cb[q], act);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
@@ -561,7 +563,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       if (s[q] == P - 1) r = mem_then(r, mepi[last]);
       if (last) ptask1[q] = r; else ptask0[q] = r;
     }
-    tc[q] = task_cache_make(row + 19 + 6 * q);       // 3 segments
+    tc[q] = task_cache_make(i64(row + 19 + 6 * q));       // 3 segments
   }
 
   // the task's segments: prologue (stage 0), blocks, epilogue (stage P-1);
@@ -595,7 +597,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     if constexpr (SEQ) {
       if (act) mem_apply(live[q], peak[q], last ? ptask1[q] : ptask0[q]);
     }
-    const bool slow = act && !task_fast(clk[q], tc[q]);
+    const bool slow = task_fast_or_slow(clk[q], tc[q], act);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
@@ -802,7 +804,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
   }
 
   // ---- task segments and the binade table of the 9 distinct op lists
-  TaskCache cf = task_cache_make(row + 19), cb = task_cache_make(row + 25);
+  TaskCache cf = task_cache_make(i64(row + 19)), cb = task_cache_make(i64(row + 25));
   auto fsegs = [&](Seg (&sg)[3]) { alt_segs(row, 0, 4, lo & 1, nl, sg[0], sg[1], sg[2]); };
   auto bsegs = [&](Seg (&sg)[9]) {          // LossGrad, recompute, layers desc, Reduce / Add
     sg[0] = Seg{row + 16, 1, (ok && st == P - 1) ? 1 : 0};
@@ -839,7 +841,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
   auto fwd_task = [&](bool act) {
     const double mx = segmax(clk);
     if (act) clk = mx;
-    const bool slow = act && !task_fast(clk, cf);
+    const bool slow = task_fast_or_slow(clk, cf, act);
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
       Seg sg[3];
@@ -850,7 +852,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
   auto bwd_task = [&](bool act) {
     const double mx = segmax(clk);
     if (act) clk = mx;
-    const bool slow = act && !task_fast(clk, cb);
+    const bool slow = task_fast_or_slow(clk, cb, act);
     const bool any = __any_sync(0xffffffffu, slow);
     if (any && slow) {
       Seg sg[9];

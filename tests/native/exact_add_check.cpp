@@ -34,13 +34,13 @@ static long check(std::mt19937_64& g, int trials, int mode) {
     }
     double x = (g() % 5 == 0) ? 0.0 : std::ldexp(U(g), -(int)(g() % 30));
     double y = x;
-    double cstore[2 * NS];
+    int64_t cstore[2 * NS];
     TaskCache c = task_cache_make(cstore);
     // half of the trials use a binade table (BinTab) covering a random range
     // around the clocks; binades outside it fall back to the lane's storage
     // (the table holds the segments' op lists in reverse order, read back
     // through a segment map)
-    static double tstore[64 * 2 * NS];
+    static int64_t tstore[64 * 2 * NS];
     BinTab tb{tstore, 0, 0, NS};
     int map[NS];
     Seg rev[NS];

@@ -9,3 +9,9 @@ echo "pytest_gpu exit $?" >> "$OUT/pytest_gpu.log"
 timeout 300 python tools/probe_longpole.py > "$OUT/longpole.txt" 2>&1
 timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench.json" 2> "$OUT/bench.err"
 tail -3 "$OUT/pytest_gpu.log"; cat "$OUT/longpole.txt"; cat "$OUT/bench.json" | cut -c1-400
+if [ "$3" = "ncu" ]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file "$OUT/launches.csv" python bench.py --steps 5 --warmup 3 --no-cpu-baseline \
+    --e2e-steps 1 > "$OUT/ncu_launch_bench.log" 2>&1
+  python tools/ncu_summary.py "$OUT/launches.csv" "bench.py --steps 5 --warmup 3 (W3, B200)"
+fi
