@@ -140,16 +140,18 @@ class ClockSampler:
 
 # --------------------------------------------------------- CPU baseline -----
 
-def cpu_oracle_rate(grid, seconds, seed=20211105426, threads=1):
-    """Time the oracle (as it stands, single-threaded) on seeded random
-    configs of the grid until `seconds` of CPU work; op-events/s."""
+def cpu_oracle_rate(grid, seconds, seed=20211105426, threads=None):
+    """Time the oracle (as it stands) on seeded random configs of the grid
+    until `seconds` of wall time, on all host threads (each thread owns
+    whole configurations); op-events/s."""
     import oracle
     oracle.build()
+    threads = threads or os.cpu_count() or 1
     n = len(oracle.enumerate_grid(grid)) if grid["synth_count"] == 0 else grid["synth_count"]
     rng = np.random.default_rng(seed)
     order = rng.permutation(n)
     done, ops, cfgs, t0 = 0, 0, 0, time.perf_counter()
-    chunk = 16
+    chunk = max(16, 8 * threads)
     while time.perf_counter() - t0 < seconds and done < n:
         idx = np.sort(order[done:done + chunk])
         r = oracle.grid_eval(grid, indices=idx, threads=threads)
@@ -171,17 +173,26 @@ def run_reference(args):
     n = len(oracle.enumerate_grid(grid))
     rng = np.random.default_rng(11)
     order = rng.permutation(n)
-    per = 12          # configs per step: a bounded sample of the grid
+    threads = os.cpu_count() or 1
+    # each step: seeded random configs of the grid, 4 per thread at a time, for
+    # a bounded time, so that the whole --steps/--warmup run ends in minutes
+    budget = min(0.25, 100.0 / max(args.steps + args.warmup, 1))
     pos = 0
+    cfg_total = 0
 
     def step():
-        nonlocal pos
-        idx = np.sort(order[pos % n: pos % n + per])
-        pos += per
-        t = time.perf_counter()
-        r = oracle.grid_eval(grid, indices=idx, threads=1)
-        dt = time.perf_counter() - t
-        return int(r["n_ops"][(r["reason"] & 0x1F) == 0].sum()), dt
+        nonlocal pos, cfg_total
+        ops, dt = 0, 0.0
+        while True:
+            idx = np.sort(order[pos % n: pos % n + 4 * threads])
+            pos += 4 * threads
+            t = time.perf_counter()
+            r = oracle.grid_eval(grid, indices=idx, threads=threads)
+            dt += time.perf_counter() - t
+            ops += int(r["n_ops"][(r["reason"] & 0x1F) == 0].sum())
+            cfg_total += len(idx)
+            if dt >= budget:
+                return ops, dt
 
     for _ in range(args.warmup):
         step()
@@ -197,9 +208,11 @@ def run_reference(args):
            "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": bench_config(args.workload, grid, n, args.k, args.gpus),
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": "%d configs/step x %d steps of %s, 1 thread"
-                                      % (per, args.steps, args.workload)},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": "%d seeded random configs of %s over %d steps "
+                                      "(%.2f s each), %d threads"
+                                      % (cfg_total, args.workload, args.steps + args.warmup,
+                                         budget, threads)},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -314,8 +327,8 @@ def main():
             cpu = {"value": c["value"], "unit": UNIT, "cores": c["threads"],
                    "kind": "oracle",
                    "sample": "seeded random %d of %d %s configs (%d op-events), %.1f s, "
-                             "1 thread" % (c["configs"], n_total, args.workload, c["ops"],
-                                           c["seconds"])}
+                             "%d threads" % (c["configs"], n_total, args.workload, c["ops"],
+                                             c["seconds"], c["threads"])}
         value = ops_all / (ms_step / 1e3)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
