@@ -28,6 +28,7 @@ constexpr int kModes = 7;
 constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr int kMaxSplit = 5;        // configs per item divided by up to 2^5
+constexpr double kPlanBudgetX = 1.0; // k_plan splits while items <= X x resident warps
 struct PlanBudget {                 // resident warps of each simulate kernel
   uint32_t warps[kGroups];
 };

@@ -148,6 +148,7 @@ struct GraphCache {
 
 struct distir_sim {
   int device = 0;
+  double plan_x = 1.0;
   cudaStream_t stream = nullptr;
   std::vector<DModel> models;
   std::vector<DTopo> topos;
@@ -431,7 +432,8 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     const int eg = (int)std::min<int64_t>((n + 255) / 256, sim->enum_grid);
     k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, hdr);
     PlanBudget pb;
-    for (int g = 0; g < kGroups; g++) pb.warps[g] = (uint32_t)sim->sim_grid[g] * (sim_tpb(g / kModes, g % kModes) / 32);
+    for (int g = 0; g < kGroups; g++)
+      pb.warps[g] = (uint32_t)(sim->plan_x * sim->sim_grid[g] * (sim_tpb(g / kModes, g % kModes) / 32));
     k_plan<<<1, 1024, 0, st>>>(bk, hdr, pb);
     k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, perm, items);
     kernels += 3;
@@ -707,7 +709,19 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
     delete sim;
     return fail(DISTIR_E_CUDA, std::string("device setup: ") + cudaGetErrorString(e));
   }
-  for (int g = 0; g < kGroups; g++) sim->sim_grid[g] = sim->num_sms * (per_sm[g] > 0 ? per_sm[g] : 1);
+  // resident blocks per SM of the persistent simulate kernels (occupancy
+  // limit; DISTIR_SIM_BLOCKS_PER_SM caps it for experiments)
+  const char* bps = getenv("DISTIR_SIM_BLOCKS_PER_SM");
+  const int cap = bps ? atoi(bps) : 0;
+  for (int g = 0; g < kGroups; g++) {
+    int b = per_sm[g] > 0 ? per_sm[g] : 1;
+    if (cap > 0 && b > cap) b = cap;
+    sim->sim_grid[g] = sim->num_sms * b;
+  }
+  // work-item budget of k_plan's splitting, in resident warps of each
+  // simulate kernel (DISTIR_PLAN_BUDGET_X scales it for experiments)
+  const char* px = getenv("DISTIR_PLAN_BUDGET_X");
+  sim->plan_x = px ? atof(px) : kPlanBudgetX;
   const char* ng = getenv("DISTIR_NO_GRAPH");
   sim->use_graph = !(ng && ng[0] == '1');
   sim->enum_grid = sim->num_sms * 8;

@@ -321,6 +321,97 @@ DISTIR_HD bool task_fast_or_slow(double& x, const TaskCache& c, bool act) {
   return act && !ok;
 }
 
+// The common slow case in straight-line code: the task crosses exactly one
+// binade boundary (E -> E+1), no segment has ties in E or E+1, and the table
+// covers E+1.  Segment j holding the crossing is found from the prefix sums
+// of reps * R(E); its whole passes that still fit are added in closed form,
+// the crossing pass op by op, and the rest of the task in closed form in
+// E+1; the cache then moves to E+1 (its increments from the table).  On any
+// other case x is left untouched and false is returned (add_task handles it).
+// Cheap pre-check of task_cross1's preconditions (x in the cached binade,
+// the table covering the next one).
+DISTIR_HD bool cross1_eligible(double x, const TaskCache& c, const BinTab& t) {
+  const int32_t ef = exp_field(x);
+  return x > 0.0 && ef == c.ef && ef + 1 - t.e0 >= 0 && ef + 1 - t.e0 < t.nb && ef + 1 <= 1993;
+}
+
+template <int NS>
+DISTIR_HD bool task_cross1(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t,
+                           const int (&map)[NS]) {
+  const int64_t xb = d2bits(x);
+  const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+  if (!(x > 0.0) || ef != c.ef || ef + 1 > 1993) return false;
+  const int32_t b1 = ef + 1 - t.e0;
+  if (b1 < 0 || b1 >= t.nb) return false;
+  const int64_t* row1 = t.tab + (int64_t)b1 * t.nu * 2;
+  const int64_t M = (xb & kMant) | kHidden;
+  const int64_t avail = kTwo53 - 1 - M;
+  // segment j where the task leaves binade E; C = ulps of the segments before
+  int j = -1;
+  int64_t C = 0;
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    const int64_t r = c.R[2 * i], rb = c.R[2 * i + 1];
+    const int64_t r1 = row1[2 * map[i]], r1b = row1[2 * map[i] + 1];
+    if (sg[i].reps > 0) {
+      ok = ok && r < kNeverI && r == rb && r1 < kNeverI && r1 == r1b;
+      if (j < 0) {
+        int64_t need = sg[i].reps * r;                // < 2^63 (reps <= 2^10)
+        need = need < kTwo53 ? need : kTwo53;         // (C + need cannot overflow)
+        if (C + need > avail) j = i; else C += need;
+      }
+    }
+  }
+  if (!ok || j < 0) return false;
+  // whole passes of segment j that still fit, then the crossing pass
+  int64_t rj = 0, nj = 0;
+  const double* aj = nullptr;
+  int naj = 0;
+#pragma unroll
+  for (int i = 0; i < NS; i++)
+    if (i == j) { rj = c.R[2 * i]; nj = sg[i].reps; aj = sg[i].a; naj = sg[i].n; }
+  const int64_t room = avail - C;                     // >= 0, < nj * rj
+  int64_t fit = (int64_t)fdiv_approx((float)room, (float)rj);
+  if (fit > nj - 1) fit = nj - 1;
+  if (fit < 0) fit = 0;
+  while (fit > 0 && fit * rj > room) fit--;
+  while (fit + 1 < nj && (fit + 1) * rj <= room) fit++;
+  double y = bits2d(((int64_t)ef << 52) | ((M + C + fit * rj) & kMant));   // exact, in E
+  seq_plain(y, aj, naj);
+  const int64_t yb = d2bits(y);
+  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) return false;
+  // the rest of the task in E+1
+  int64_t rest = 0, T1 = 0;                           // both capped at 2^53
+  auto cap_add = [](int64_t a, int64_t b) { return (a >= kTwo53 || b >= kTwo53) ? kTwo53 : a + b; };
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    if (sg[i].reps <= 0) continue;
+    const int64_t r1 = row1[2 * map[i]];
+    T1 = cap_add(T1, sg[i].reps * r1);
+    if (i == j) rest = cap_add(rest, (nj - fit - 1) * r1);
+    else if (i > j) rest = cap_add(rest, sg[i].reps * r1);
+  }
+  const int64_t M1 = (yb & kMant) | kHidden;
+  if (M1 + rest > kTwo53 - 1) return false;
+  x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
+  // the cache follows x into E+1 (no ties: the total does not depend on parity)
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    c.R[2 * i] = row1[2 * map[i]];
+    c.R[2 * i + 1] = row1[2 * map[i] + 1];
+  }
+  bool all = true;
+#pragma unroll
+  for (int i = 0; i < NS; i++) all = all && (sg[i].reps <= 0 || c.R[2 * i] < kNeverI);
+  const double u = bits2d((int64_t)(ef + 1 - 52) << 52);
+  c.ef = ef + 1;
+  c.lo = (ef + 1) << 20;
+  c.hi = (ef + 2) << 20;
+  c.Su0 = c.Su1 = (all && T1 < kTwo53) ? xmul((double)T1, u) : kInf();
+  return true;
+}
+
 // x <- every addition of the task, in order, computed exactly: the cache is
 // moved to x's binade and the fast path retried; otherwise each segment
 // advances by whole passes while they fit (closed form, or a short parity

@@ -574,6 +574,9 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
       atomicAdd(&g_distir_instr[5], dt);
       atomicAdd(&g_distir_instr[7], 1ull);
       atomicMax(&g_distir_instr[8], dt);
+      // slowest item: cycles and its bucket key / configs (for probe_instr)
+      atomicMax(&g_distir_instr[11], (dt << 24) | ((unsigned long long)(B.key & 0x7FFFF) << 5) |
+                                         (unsigned long long)(it.n & 31));
     }
 #endif
     // makespan and peak: max over the stages of the segment

@@ -37,6 +37,10 @@ __device__ __forceinline__ double min_pos(double m, double x) { return x > 0.0 &
 // per-lane shared-memory storage reused for integer per-pass increments
 __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int64_t*>(p); }
 
+#ifndef DISTIR_CROSS1
+#define DISTIR_CROSS1 0     // straight-line single-binade-crossing slow path (task_cross1):
+                            // faster single long configurations, slower grids (registers)
+#endif
 // Segment -> distinct-op-list maps of the task caches (BinTab).
 __device__ constexpr int kMapId3[3] = {0, 1, 2};
 // MLP backward: LossGrad, recompute (the forward lists), layers (desc)
@@ -212,10 +216,15 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     const bool slow = task_fast_or_slow(clk[q], cf[q], act);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
-    if (any && slow) {
+    if (any) {
       Seg sg[3];
       fsegs(q, sg);
-      add_task(clk[q], sg, cf[q], btf, kMapId3);
+      // the single-crossing path only when every slow lane qualifies (else
+      // add_task runs anyway and would pay for both)
+      bool s2 = slow;
+      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], cf[q], btf)))
+        s2 = slow && !task_cross1(clk[q], sg, cf[q], btf, kMapId3);
+      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk[q], sg, cf[q], btf, kMapId3);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -226,11 +235,18 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     const bool slow = task_fast_or_slow(clk[q], cb[q], act);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
-    if (any && slow) {
+    if (any) {
       Seg sg[NB];
       bsegs(q, sg);
-      if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd);
-      else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4);
+      bool s2 = slow;
+      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], cb[q], btf))) {
+        if constexpr (RC) s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd);
+        else s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd4);
+      }
+      if (__any_sync(0xffffffffu, s2) && s2) {
+        if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd);
+        else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4);
+      }
     }
     DISTIR_SLOW_T1(any)
   };
@@ -600,10 +616,15 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     const bool slow = task_fast_or_slow(clk[q], tc[q], act);
     DISTIR_SLOW_T0
     const bool any = __any_sync(0xffffffffu, slow);
-    if (any && slow) {
+    if (any) {
       Seg sg[3];
       segs(q, sg);
-      add_task(clk[q], sg, tc[q], bt, kMapId3);
+      // the single-crossing path only when every slow lane qualifies (else
+      // add_task runs anyway and would pay for both)
+      bool s2 = slow;
+      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], tc[q], bt)))
+        s2 = slow && !task_cross1(clk[q], sg, tc[q], bt, kMapId3);
+      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -843,10 +864,15 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
     if (act) clk = mx;
     const bool slow = task_fast_or_slow(clk, cf, act);
     const bool any = __any_sync(0xffffffffu, slow);
-    if (any && slow) {
+    if (any) {
       Seg sg[3];
       fsegs(sg);
-      add_task(clk, sg, cf, bt, kMapId3);
+      // the single-crossing path only when every slow lane qualifies (else
+      // add_task runs anyway and would pay for both)
+      bool s2 = slow;
+      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk, cf, bt)))
+        s2 = slow && !task_cross1(clk, sg, cf, bt, kMapId3);
+      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk, sg, cf, bt, kMapId3);
     }
   };
   auto bwd_task = [&](bool act) {
@@ -854,10 +880,15 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
     if (act) clk = mx;
     const bool slow = task_fast_or_slow(clk, cb, act);
     const bool any = __any_sync(0xffffffffu, slow);
-    if (any && slow) {
+    if (any) {
       Seg sg[9];
       bsegs(sg);
-      add_task(clk, sg, cb, bt, kMapZeroBwd);
+      // the single-crossing path only when every slow lane qualifies (else
+      // add_task runs anyway and would pay for both)
+      bool s2 = slow;
+      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk, cb, bt)))
+        s2 = slow && !task_cross1(clk, sg, cb, bt, kMapZeroBwd);
+      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk, sg, cb, bt, kMapZeroBwd);
     }
     if (act && own(hi - 1)) clk = dadd(clk, row[18]);       // the last Add: owner only
   };

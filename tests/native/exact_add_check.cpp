@@ -55,7 +55,9 @@ static long check(std::mt19937_64& g, int trials, int mode) {
       for (int i = 0; i < NS; i++)
         for (int64_t r = 0; r < sg[i].reps; r++)
           for (int j = 0; j < sg[i].n; j++) x = x + sg[i].a[j];
-      if ((g() & 1) || !task_fast(y, c)) add_task(y, sg, c, tb, map);   // as the kernels do
+      // as the kernels do: fast path, else the single-crossing path, else add_task
+      if ((g() & 1) || !task_fast(y, c))
+        if (!(g() & 3) || !task_cross1(y, sg, c, tb, map)) add_task(y, sg, c, tb, map);
       if (std::memcmp(&x, &y, 8) != 0) {
         if (bad < 5) std::printf("mismatch NS=%d mode=%d task=%d plain=%a agg=%a\n", NS, mode, k, x, y);
         bad++;

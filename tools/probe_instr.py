@@ -12,7 +12,7 @@ import paper_2111_05426_b200 as pkg
 from paper_2111_05426_b200 import Simulator
 
 NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles",
-         "slow_cycles", "slow_entries"]
+         "slow_cycles", "slow_entries", "max_item_tag"]
 
 
 def counters():
@@ -48,6 +48,10 @@ def main():
                   d["refresh"] / max(d["tasks"], 1), d["plain"] / max(d["tasks"], 1), d["steps"],
                   d["items"], d["item_cycles"] / max(d["items"], 1), d["max_item_cycles"],
                   d["slow_cycles"] / max(d["items"], 1), d["slow_entries"] / max(d["items"], 1)))
+        tag = d["max_item_tag"]
+        key = (tag >> 5) & 0x7FFFF
+        print("   slowest item: %d cycles, kind %d P %d L %d, %d configs" % (
+            tag >> 24, key & 1, ((key >> 1) & 63) + 1, ((key >> 7) & 1023) + 1, tag & 31))
 
 
 if __name__ == "__main__":
