@@ -84,8 +84,8 @@ struct SpecBlock {
   int64_t n_total;                    // configs of the whole grid
   int32_t rank, n_ranks;              // shard: global i = rank + q * n_ranks
   int64_t n_local;
-  int32_t f1b;                        // extra simulate kernels: bit 0 1F1B (mode 5),
-                                      // bit 1 ZeRO (mode 6)
+  uint32_t f1b;                       // simulate kernels to launch: bit kind * kModes
+                                      // + mode (distir.cu gbit)
   DModel models[kMaxModels];          // handle tables
   DTopo topos[kMaxTopos];
 };

@@ -143,7 +143,7 @@ struct GraphCache {
   void* comm = nullptr;
   int64_t n_local = -1, n_total = -1;
   int32_t mode = -1;
-  int32_t f1b = -1;
+  uint32_t f1b = 0xFFFFFFFFu;
 };
 
 struct distir_sim {
@@ -178,6 +178,9 @@ struct distir_sim {
 };
 
 namespace {
+
+// bit of simulate kernel (kind, mode) in SpecBlock.f1b
+constexpr uint32_t gbit(int kind, int mode) { return 1u << (kind * kModes + mode); }
 
 distir_status check_handle(const distir_sim* sim) {
   if (!sim) return fail(DISTIR_E_INVALID_ARG, "sim is NULL");
@@ -261,6 +264,8 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     sp.mode = MODE_SYNTH;
     sp.synth_seed = g->synth_seed;
     n_total = g->synth_count;
+    // synthetic sweep: GPipe MLP and GPT-2, P up to 64
+    sp.f1b = gbit(0, 3) | gbit(0, 4) | gbit(1, 3) | gbit(1, 4);
     return DISTIR_OK;
   }
   sp.mode = MODE_GRID;
@@ -301,7 +306,22 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     if (g->k_set[i] > 4096) return fail(DISTIR_E_UNSUPPORTED, "microbatches > 4096");
   }
   sp.k_mode = g->k_mode;
-  sp.f1b = (any_1f1b ? 1 : 0) | (any_zero ? 2 : 0);
+  // simulate kernels this grid can need (k_plan's group choice, bucket_key):
+  // the wavefront kernel of each model kind, its two-stages-per-lane variant
+  // when P > 32 is possible, 1F1B and ZeRO when a model uses them (a grid
+  // has far fewer than 4096 warp shapes, so the catch-all buckets stay empty)
+  {
+    const int32_t wmax = g->world[g->n_world - 1];
+    uint32_t m = 0;
+    for (int mi = 0; mi < g->n_models; mi++) {
+      const DModel& M = sim->models[g->models[mi]];
+      if (M.kind == 0 && M.sched == 1) { m |= gbit(0, 5); continue; }
+      m |= gbit(M.kind, 3);
+      if (wmax > 32) m |= gbit(M.kind, 4);
+      if (M.kind == 0 && M.zero) m |= gbit(0, 6);
+    }
+    sp.f1b = m;
+  }
   sp.n_k = g->n_k;
   for (int i = 0; i < g->n_k; i++) sp.k_set[i] = g->k_set[i];
   sp.n_batch = g->n_batch;
@@ -454,10 +474,13 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     DISTIR_SIM(0, 2); DISTIR_SIM(1, 2);
     kernels += 2;
 #endif
-    DISTIR_SIM(0, 3); DISTIR_SIM(0, 4); DISTIR_SIM(1, 3); DISTIR_SIM(1, 4);
-    kernels += 4;
-    if (sp.f1b & 1) { DISTIR_SIM(0, 5); kernels++; }
-    if (sp.f1b & 2) { DISTIR_SIM(0, 6); kernels++; }
+    // only the simulate kernels the grid can need (SpecBlock.f1b mask)
+    if (sp.f1b & gbit(0, 3)) { DISTIR_SIM(0, 3); kernels++; }
+    if (sp.f1b & gbit(0, 4)) { DISTIR_SIM(0, 4); kernels++; }
+    if (sp.f1b & gbit(0, 5)) { DISTIR_SIM(0, 5); kernels++; }
+    if (sp.f1b & gbit(0, 6)) { DISTIR_SIM(0, 6); kernels++; }
+    if (sp.f1b & gbit(1, 3)) { DISTIR_SIM(1, 3); kernels++; }
+    if (sp.f1b & gbit(1, 4)) { DISTIR_SIM(1, 4); kernels++; }
 #undef DISTIR_SIM
   }
   CUDA_TRY(mark(2));
@@ -601,11 +624,19 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
     for (size_t i = 0; i < sim->topos.size(); i++) sp.topos[i] = sim->topos[i];
     sp.mode = MODE_EXPLICIT;
     n_total = n_configs;
+    // simulate kernels the configurations need (k_plan's group choice);
+    // with more configurations than hash buckets, the catch-alls too
+    uint32_t m = 0, kinds = 0;
     for (int64_t i = 0; i < n_configs; i++) {
       const DModel& M = sim->models[configs[i].model];
-      if (M.kind == 0 && M.sched == 1) sp.f1b |= 1;
-      if (M.kind == 0 && M.zero && configs[i].dp > 1) sp.f1b |= 2;
+      kinds |= 1u << (M.kind == 0 && M.sched == 1 ? 2 : M.kind == 0 && M.zero && configs[i].dp > 1 ? 3 : M.kind);
+      if (M.kind == 0 && M.sched == 1) m |= gbit(0, 5);
+      else if (M.kind == 0 && M.zero && configs[i].dp > 1) m |= gbit(0, 6);
+      else m |= gbit(M.kind, configs[i].pp > 32 ? 4 : 3);
     }
+    if (n_configs > kNumBuckets / 2)
+      m |= ((kinds & 1) ? gbit(0, 4) : 0) | ((kinds & 2) ? gbit(1, 4) : 0);
+    sp.f1b = m;
   }
   sp.n_total = n_total;
   sp.rank = rank;

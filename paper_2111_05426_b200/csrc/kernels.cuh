@@ -403,8 +403,9 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
     const int g = threadIdx.x;
     unsigned int total = 0;
     for (int c = 0; c < kNumClasses; c++) total += s_alt[g][c][0];
-    for (int c = kNumClasses - 1; c >= 0; c--) {
+    for (int c = kNumClasses - 1; c >= 0 && total > 0; c--) {
       int j = 0;
+      if (s_alt[g][c][0] == 0) { s_shift[g][c] = 0; continue; }       // empty class
       while (j < kMaxSplit && total - s_alt[g][c][j] + s_alt[g][c][j + 1] <= budget.warps[g]) {
         total = total - s_alt[g][c][j] + s_alt[g][c][j + 1];
         j++;
