@@ -66,7 +66,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 
 // Decode canonical index i (C.1 nested order, or the synthetic sweep of
 // SURVEY §8d D.1, or an explicit list).
-__device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t i, Cfg& c) {
+__device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t i, Cfg& c,
+                              const DEntry* __restrict__ entries = nullptr) {
   if (sp.mode == MODE_EXPLICIT) {
     const DExplicit x = ex[i];
     c.M = sp.models[x.model];
@@ -101,12 +102,13 @@ __device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t 
   const int64_t mt = i / sp.per_mt;
   const int64_t r = i - mt * sp.per_mt;
   const int mi = (int)(mt / sp.n_topos), ti = (int)(mt - (int64_t)mi * sp.n_topos);
+  const DEntry* E = entries ? entries : sp.entries;
   int lo = 0, hi = sp.n_entries - 1;            // last entry with cum <= r
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (sp.entries[mid].cum <= r) lo = mid; else hi = mid - 1;
+    if (E[mid].cum <= r) lo = mid; else hi = mid - 1;
   }
-  const DEntry en = sp.entries[lo];
+  const DEntry en = E[lo];
   const int64_t r2 = r - en.cum;
   const int64_t kq = r2 / sp.n_batch, bq = r2 - kq * sp.n_batch;
   c.M = sp.models[sp.model_ids[mi]];
@@ -276,11 +278,15 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
   const SpecBlock& sp = *spp;
   const int64_t nloc = sp.n_local;
   unsigned long long ev = 0, st = 0, nv = 0;
+  // the decode table, staged in shared memory (a binary search per config)
+  __shared__ DEntry s_ent[kMaxEntries];
+  for (int j = threadIdx.x; j < sp.n_entries; j += blockDim.x) s_ent[j] = sp.entries[j];
+  __syncthreads();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nloc;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = sp.rank + q * sp.n_ranks;
     Cfg c;
-    decode(sp, ex, i, c);
+    decode(sp, ex, i, c, s_ent);
     const uint32_t r = validity(c, sp.topos[c.topo]);
     if (r) {
       rs_out[q] = r;
@@ -752,7 +758,12 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(
 #pragma unroll
     for (int i = 0; i < kTopkIPT; i++) {
       const int64_t q = c * per + threadIdx.x + (int64_t)i * kTopkThreads;
-      it[i] = (q < n && rs[q] == 0) ? make_key(tpv[q], pk[q], rank + q * nr, ms[q]) : no_key();
+      // the four loads are independent (one memory round trip), selected after
+      const bool in = q < n;
+      const uint32_t rq = in ? rs[q] : 1u;
+      const double tq = in ? tpv[q] : 0.0, mq = in ? ms[q] : 0.0;
+      const int64_t pq = in ? pk[q] : 0;
+      it[i] = rq == 0 ? make_key(tq, pq, rank + q * nr, mq) : no_key();
     }
     static_assert(kTopkIPT == 2, "one compare-exchange sorts a thread's candidates");
     cswap(it[0], it[1]);
