@@ -31,6 +31,9 @@
 #ifndef DISTIR_COLD_NOINLINE
 #define DISTIR_COLD_NOINLINE 0
 #endif
+#ifndef DISTIR_SEGWALK
+#define DISTIR_SEGWALK 0   // per-segment binade increments in the slow walk
+#endif
 #ifndef DISTIR_UNROLL_SEG
 #define DISTIR_UNROLL_SEG 0
 #endif
@@ -50,6 +53,10 @@
 
 #ifndef DISTIR_COUNT
 #define DISTIR_COUNT(i)
+#endif
+#ifndef DISTIR_CLK_ADD
+#define DISTIR_CLK_ADD(i, t0)       // instrumentation: cycles since t0 into counter i
+#define DISTIR_CLK_NOW() 0ll
 #endif
 
 namespace distir {
@@ -421,22 +428,53 @@ template <int NS>
 DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t,
                              const int (&map)[NS]) {
   DISTIR_COUNT(0);
+  const long long t_all = DISTIR_CLK_NOW();
   {
     const int32_t ef = exp_field(x);
     if (x > 0.0 && ef >= 53 && ef <= 1993) {
-      if (ef != c.ef) task_refresh(c, ef, sg, t, map);
-      if (task_fast(x, c)) { DISTIR_COUNT(1); return; }
+      if (ef != c.ef) {
+        const long long t0 = DISTIR_CLK_NOW();
+        task_refresh(c, ef, sg, t, map);
+        DISTIR_CLK_ADD(12, t0);
+      }
+      if (task_fast(x, c)) { DISTIR_COUNT(1); DISTIR_CLK_ADD(15, t_all); return; }
     }
   }
 #pragma unroll
   for (int i = 0; i < NS; i++) {
     int64_t reps = sg[i].reps;
+#if DISTIR_SEGWALK
+    int32_t ef_r = -1;              // binade of this segment's (r0, r1)
+    int64_t r0 = kNeverI, r1 = kNeverI;
+#endif
     while (reps > 0) {
       const int64_t xb = d2bits(x);
       const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
       if (x > 0.0 && ef >= 53 && ef <= 1993) {
-        if (ef != c.ef) task_refresh(c, ef, sg, t, map);
+#if DISTIR_SEGWALK
+        // only this segment's increments in binade ef (table, cache or one
+        // seg_pass); the cache follows x once, after the task
+        if (ef != ef_r) {
+          const long long t0 = DISTIR_CLK_NOW();
+          if (ef == c.ef) {
+            r0 = c.R[2 * i]; r1 = c.R[2 * i + 1];
+          } else if (ef - t.e0 >= 0 && ef - t.e0 < t.nb) {
+            const int64_t* row = t.tab + ((int64_t)(ef - t.e0) * t.nu + map[i]) * 2;
+            r0 = row[0]; r1 = row[1];
+          } else {
+            seg_pass(sg[i].a, sg[i].n, ef, r0, r1);
+          }
+          ef_r = ef;
+          DISTIR_CLK_ADD(12, t0);
+        }
+#else
+        if (ef != c.ef) {
+          const long long t0 = DISTIR_CLK_NOW();
+          task_refresh(c, ef, sg, t, map);
+          DISTIR_CLK_ADD(12, t0);
+        }
         const int64_t r0 = c.R[2 * i], r1 = c.R[2 * i + 1];
+#endif
         if (r0 < kNeverI) {
           int64_t M = (xb & kMant) | kHidden;
           const int64_t before = reps;
@@ -468,11 +506,24 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
       }
       if (reps > 0) {                                // the crossing pass
         DISTIR_COUNT(3);
+        const long long t0 = DISTIR_CLK_NOW();
         seq_plain(x, sg[i].a, sg[i].n);
+        DISTIR_CLK_ADD(13, t0);
         reps--;
       }
     }
   }
+#if DISTIR_SEGWALK
+  {
+    const int32_t ef = exp_field(x);
+    if (x > 0.0 && ef >= 53 && ef <= 1993 && ef != c.ef) {
+      const long long t0 = DISTIR_CLK_NOW();
+      task_refresh(c, ef, sg, t, map);
+      DISTIR_CLK_ADD(12, t0);
+    }
+  }
+#endif
+  DISTIR_CLK_ADD(15, t_all);
 }
 
 template <int NS>

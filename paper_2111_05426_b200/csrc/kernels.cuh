@@ -35,6 +35,16 @@ __device__ __forceinline__ void distir_count(int i) {
   if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));
 }
 #define DISTIR_COUNT(i) NV_IF_TARGET(NV_IS_DEVICE, (distir_count(i);))
+// per-lane cycle accounting of the slow path ([12] refresh, [13] crossing
+// passes, [15] whole add_task), summed over lanes
+__host__ __device__ __forceinline__ long long distir_clk_now() {
+  NV_IF_ELSE_TARGET(NV_IS_DEVICE, (return clock64();), (return 0;))
+}
+__host__ __device__ __forceinline__ void distir_clk_add(int i, long long t0) {
+  NV_IF_TARGET(NV_IS_DEVICE, (atomicAdd(&g_distir_instr[i], (unsigned long long)(clock64() - t0));))
+}
+#define DISTIR_CLK_NOW() distir_clk_now()
+#define DISTIR_CLK_ADD(i, t0) distir_clk_add(i, t0)
 // warp-level timing of the divergent slow path: [9] cycles, [10] entries
 #define DISTIR_SLOW_T0 const long long slow_t0_ = clock64();
 #define DISTIR_SLOW_T1(any)                                                   \

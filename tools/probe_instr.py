@@ -12,7 +12,7 @@ import paper_2111_05426_b200 as pkg
 from paper_2111_05426_b200 import Simulator
 
 NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles",
-         "slow_cycles", "slow_entries", "max_item_tag"]
+         "slow_cycles", "slow_entries", "max_item_tag", "refresh_cyc", "cross_cyc", "-", "addtask_cyc"]
 
 
 def counters():
@@ -30,7 +30,13 @@ def main():
              ("xl P16 K128", None, [(mi["gpt2_xl"], tb, 1, 1, 16, 128, 1 << 20)]),
              ("mlp1b P2 K128", None, [(mi["mlp_1b"], tb, 8, 1, 2, 128, 1 << 18)]),
              ("16x xl P2 K128", None, [(mi["gpt2_xl"], tb, 8, 1, 2, 128, 1 << e) for e in range(7, 21)])]
-    cases += [(g, W.GRIDS[g], None) for g in ["W3", "W2", "W5"]]
+    # one warp each when DISTIR_PLAN_BUDGET_X=0 (no splitting): do the binade
+    # crossings of configurations that differ only in batch size line up?
+    cases += [("8x xl P2 K128 Bsweep", None, [(mi["gpt2_xl"], tb, 1, 1, 2, 128, 1 << e) for e in range(13, 21)]),
+              ("8x xl P2 K128 DTmix", None, [(mi["gpt2_xl"], tb, D, T, 2, 128, 1 << 20)
+                                             for D, T in [(1, 1), (2, 1), (1, 2), (4, 1), (2, 2), (1, 4), (8, 1), (4, 2)]])]
+    if os.environ.get("PROBE_GRIDS", "1") == "1":
+        cases += [(g, W.GRIDS[g], None) for g in ["W3", "W2", "W5"]]
     for name, grid, cfgs in cases:
         n = sim.upload(grid=grid, configs=cfgs)
         outs = sim.device_outputs(n, k=10)
@@ -48,6 +54,9 @@ def main():
                   d["refresh"] / max(d["tasks"], 1), d["plain"] / max(d["tasks"], 1), d["steps"],
                   d["items"], d["item_cycles"] / max(d["items"], 1), d["max_item_cycles"],
                   d["slow_cycles"] / max(d["items"], 1), d["slow_entries"] / max(d["items"], 1)))
+        print("   lane-cycles in add_task %d: refresh %d, crossing passes %d (per add_task call: %.0f / %.0f / %.0f)" % (
+            d["addtask_cyc"], d["refresh_cyc"], d["cross_cyc"], d["addtask_cyc"] / max(d["tasks"], 1),
+            d["refresh_cyc"] / max(d["tasks"], 1), d["cross_cyc"] / max(d["tasks"], 1)))
         tag = d["max_item_tag"]
         key = (tag >> 5) & 0x7FFFF
         print("   slowest item: %d cycles, kind %d P %d L %d, %d configs" % (
