@@ -303,11 +303,12 @@ class Simulator:
 
     # -- synchronous evaluation with host buffers (the e2e path)
     def eval(self, grid=None, configs=None, k=10, per_config=True, pinned=True,
-             rank=0, n_ranks=1, comm=None):
+             rank=0, n_ranks=1, comm=None, copy=True):
         """Synchronous evaluation through distir_grid_eval_sharded with host
         buffers (spec H2D and results D2H inside the call).  Per-config
-        outputs are global-indexed numpy copies (only this rank's entries are
-        written when n_ranks > 1)."""
+        outputs are global-indexed numpy arrays (only this rank's entries are
+        written when n_ranks > 1): copies, or with copy=False views of the
+        handle's pinned buffers that the next call overwrites."""
         torch = self.torch
         if grid is not None:
             key = repr(sorted(grid.items()))
@@ -335,7 +336,7 @@ class Simulator:
                 bufs[0][:n].fill_(float("nan"))
                 bufs[1][:n].fill_(-2)
                 bufs[2][:n].fill_(-1)
-        topk = np.zeros(max(k, 1), dtype=TOPK_DTYPE)
+        topk = np.zeros(max(k, 1), dtype=TOPK_DTYPE) if copy else self._topk_buf(k)
         ntopk = ctypes.c_int32()
         st = distir_stats()
         p = lambda name: ctypes.c_void_p(outs[name].data_ptr()) if name in outs else None
@@ -348,10 +349,16 @@ class Simulator:
         res = dict(topk=topk[:ntopk.value], n=n,
                    stats={f: getattr(st, f) for f, _ in distir_stats._fields_})
         for name, t in outs.items():
-            res[name] = t.numpy()[:n].copy()
+            res[name] = t.numpy()[:n].copy() if copy else t.numpy()[:n]
         if per_config:
             res["reason"] = res["reason"].view(np.uint32)
         return res
+
+    def _topk_buf(self, k):
+        b = getattr(self, "_topk_host", None)
+        if b is None or len(b) < max(k, 1):
+            b = self._topk_host = np.zeros(max(k, 1), dtype=TOPK_DTYPE)
+        return b[:max(k, 1)]
 
     # -- device-resident pipeline (the timed `value` path)
     def upload(self, grid=None, configs=None, rank=0, n_ranks=1):

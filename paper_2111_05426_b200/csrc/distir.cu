@@ -167,7 +167,20 @@ struct distir_sim {
   int64_t kernels = 0, launches = 0;
   GraphCache graph;
   bool use_graph = true;
+  // pinned host staging of the per-call small copies (spec H2D; top-k,
+  // its count and the statistics header D2H), so they are true async DMA
+  struct Pinned {
+    SpecBlock spec;
+    WsHeader hdr;
+    TopkRec topk[kMaxK];
+    int32_t ntopk;
+  };
+  Pinned* pin = nullptr;
+  cudaEvent_t pin_ev = nullptr;     // the last H2D from pin->spec
+  bool pin_pending = false;
   ~distir_sim() {
+    if (pin) cudaFreeHost(pin);
+    if (pin_ev) cudaEventDestroy(pin_ev);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
     if (graph.graph) cudaGraphDestroy(graph.graph);
@@ -645,8 +658,18 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
   const Layout L = layout(sp.n_local, sp.mode == MODE_EXPLICIT ? n_total : 0);
   if ((s = check_ws(ws, ws_bytes, L.total)) != DISTIR_OK) return s;
   CUDA_TRY(cudaSetDevice(sim->device));
-  CUDA_TRY(cudaMemcpyAsync(at<SpecBlock>(ws, L.spec), &sp, sizeof(SpecBlock),
-                           cudaMemcpyHostToDevice, sim->stream));
+  if (sim->pin) {
+    // the staging buffer may still feed the previous upload's copy
+    if (sim->pin_pending) CUDA_TRY(cudaEventSynchronize(sim->pin_ev));
+    std::memcpy(&sim->pin->spec, &sp, sizeof(SpecBlock));
+    CUDA_TRY(cudaMemcpyAsync(at<SpecBlock>(ws, L.spec), &sim->pin->spec, sizeof(SpecBlock),
+                             cudaMemcpyHostToDevice, sim->stream));
+    CUDA_TRY(cudaEventRecord(sim->pin_ev, sim->stream));
+    sim->pin_pending = true;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(at<SpecBlock>(ws, L.spec), &sp, sizeof(SpecBlock),
+                             cudaMemcpyHostToDevice, sim->stream));
+  }
   if (sp.mode == MODE_EXPLICIT && n_total > 0)
     CUDA_TRY(cudaMemcpyAsync(at<DExplicit>(ws, L.ex), configs, n_total * sizeof(DExplicit),
                              cudaMemcpyHostToDevice, sim->stream));
@@ -753,6 +776,13 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   // simulate kernel (DISTIR_PLAN_BUDGET_X scales it for experiments)
   const char* px = getenv("DISTIR_PLAN_BUDGET_X");
   sim->plan_x = px ? atof(px) : kPlanBudgetX;
+  if (cudaMallocHost(&sim->pin, sizeof(distir_sim::Pinned)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&sim->pin_ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();            // pageable fallback
+    if (sim->pin) cudaFreeHost(sim->pin);
+    sim->pin = nullptr;
+    sim->pin_ev = nullptr;
+  }
   const char* ng = getenv("DISTIR_NO_GRAPH");
   sim->use_graph = !(ng && ng[0] == '1');
   sim->enum_grid = sim->num_sms * 8;
@@ -870,26 +900,48 @@ distir_status distir_grid_eval_sharded(distir_sim* sim, const distir_grid_spec* 
   sim->d2h = n * ((makespan_out ? 8 : 0) + (peak_out ? 8 : 0) + (reason_out ? 4 : 0)) +
              (k > 0 ? (int64_t)k * (int64_t)sizeof(TopkRec) + 4 : 0);
   if (n > 0) {
+    // per-config results straight into the caller's (pinned) buffers; a
+    // strided copy only when shards interleave
     const size_t pitch = (size_t)n_ranks;
-    if (makespan_out)
-      CUDA_TRY(cudaMemcpy2DAsync(makespan_out + rank, pitch * 8, at<double>(d_workspace, L.ms), 8, 8,
-                                 n, cudaMemcpyDeviceToHost, sim->stream));
-    if (peak_out)
-      CUDA_TRY(cudaMemcpy2DAsync(peak_out + rank, pitch * 8, at<int64_t>(d_workspace, L.pk), 8, 8, n,
-                                 cudaMemcpyDeviceToHost, sim->stream));
-    if (reason_out)
-      CUDA_TRY(cudaMemcpy2DAsync(reason_out + rank, pitch * 4, at<uint32_t>(d_workspace, L.rs), 4, 4,
-                                 n, cudaMemcpyDeviceToHost, sim->stream));
+    auto get = [&](void* dst, const void* src, size_t w) -> cudaError_t {
+      if (n_ranks == 1) return cudaMemcpyAsync(dst, src, w * n, cudaMemcpyDeviceToHost, sim->stream);
+      return cudaMemcpy2DAsync(dst, pitch * w, src, w, w, n, cudaMemcpyDeviceToHost, sim->stream);
+    };
+    if (makespan_out) CUDA_TRY(get(makespan_out + rank, at<double>(d_workspace, L.ms), 8));
+    if (peak_out) CUDA_TRY(get(peak_out + rank, at<int64_t>(d_workspace, L.pk), 8));
+    if (reason_out) CUDA_TRY(get(reason_out + rank, at<uint32_t>(d_workspace, L.rs), 4));
   }
+  distir_sim::Pinned* P = sim->pin;
   if (k > 0) {
-    CUDA_TRY(cudaMemcpyAsync(topk_out, fin, (size_t)k * sizeof(TopkRec), cudaMemcpyDeviceToHost,
-                             sim->stream));
-    CUDA_TRY(cudaMemcpyAsync(n_topk_out, fin_n, sizeof(int32_t), cudaMemcpyDeviceToHost, sim->stream));
+    CUDA_TRY(cudaMemcpyAsync(P ? (void*)P->topk : (void*)topk_out, fin, (size_t)k * sizeof(TopkRec),
+                             cudaMemcpyDeviceToHost, sim->stream));
+    CUDA_TRY(cudaMemcpyAsync(P ? &P->ntopk : n_topk_out, fin_n, sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, sim->stream));
+  }
+  if (stats_out && P)
+    CUDA_TRY(cudaMemcpyAsync(&P->hdr, at<WsHeader>(d_workspace, L.hdr), sizeof(WsHeader),
+                             cudaMemcpyDeviceToHost, sim->stream));
+  CUDA_TRY(cudaStreamSynchronize(sim->stream));
+  if (P && k > 0) {
+    std::memcpy(topk_out, P->topk, (size_t)k * sizeof(TopkRec));
+    *n_topk_out = P->ntopk;
   }
   if (stats_out) {
-    if ((s = fetch_stats(sim, d_workspace, stats_out)) != DISTIR_OK) return s;
+    if (P) {
+      const WsHeader& h = P->hdr;
+      stats_out->n_configs = sp.n_local;
+      stats_out->n_valid = (int64_t)h.n_valid;
+      stats_out->n_feasible = (int64_t)h.n_feasible;
+      stats_out->op_events = (int64_t)h.op_events;
+      stats_out->stage_steps = (int64_t)h.stage_steps;
+      stats_out->n_buckets = h.n_buckets;
+      stats_out->n_items = h.n_items;
+      stats_out->h2d_bytes = sim->h2d;
+      stats_out->d2h_bytes = sim->d2h + (int64_t)sizeof(WsHeader);
+    } else if ((s = fetch_stats(sim, d_workspace, stats_out)) != DISTIR_OK) {
+      return s;
+    }
   }
-  CUDA_TRY(cudaStreamSynchronize(sim->stream));
   return DISTIR_OK;
 }
 

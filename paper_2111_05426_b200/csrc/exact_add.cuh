@@ -55,7 +55,7 @@
 #define DISTIR_COUNT(i)
 #endif
 #ifndef DISTIR_CLK_ADD
-#define DISTIR_CLK_ADD(i, t0)       // instrumentation: cycles since t0 into counter i
+#define DISTIR_CLK_ADD(i, t0) ((void)(t0))   // instrumentation: cycles since t0 into counter i
 #define DISTIR_CLK_NOW() 0ll
 #endif
 
