@@ -31,6 +31,15 @@
 #ifndef DISTIR_COLD_NOINLINE
 #define DISTIR_COLD_NOINLINE 0
 #endif
+#ifndef DISTIR_PLAIN_AFTER
+#define DISTIR_PLAIN_AFTER 0   // crossings after which a task is walked op by op (0: never)
+#endif
+#ifndef DISTIR_PLAIN_OPS
+#define DISTIR_PLAIN_OPS 0     // after a crossing, walk the rest op by op when <= this many ops
+#endif
+#ifndef DISTIR_PLAIN_ZERO
+#define DISTIR_PLAIN_ZERO 0    // a task from a zero clock is walked op by op
+#endif
 #ifndef DISTIR_SEGWALK
 #define DISTIR_SEGWALK 0   // per-segment binade increments in the slow walk
 #endif
@@ -426,9 +435,21 @@ DISTIR_HD bool task_cross1(double& x, const Seg (&sg)[NS], TaskCache& c, const B
 // by op, and the cache follows x into the new binade.
 template <int NS>
 DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t,
-                             const int (&map)[NS]) {
+                             const int (&map)[NS], int plain_after = DISTIR_PLAIN_AFTER) {
   DISTIR_COUNT(0);
   const long long t_all = DISTIR_CLK_NOW();
+  // a task that spans several binades (a clock starting at zero, a
+  // single-stage configuration's tasks) is cheaper op by op than binade by
+  // binade: from a zero clock or after `plain_after` crossings (0: never),
+  // walk it plainly
+  if (plain_after > 0 && x == 0.0) {
+#pragma unroll
+    for (int i = 0; i < NS; i++)
+      for (int64_t r = 0; r < sg[i].reps; r++) seq_plain(x, sg[i].a, sg[i].n);
+    DISTIR_CLK_ADD(15, t_all);
+    return;
+  }
+  int crossings = 0;
   {
     const int32_t ef = exp_field(x);
     if (x > 0.0 && ef >= 53 && ef <= 1993) {
@@ -441,8 +462,21 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
     }
   }
 #pragma unroll
+#if DISTIR_PLAIN_OPS > 0
+  bool plain_rest = false;
+#endif
   for (int i = 0; i < NS; i++) {
     int64_t reps = sg[i].reps;
+    if (plain_after > 0 && crossings >= plain_after) {
+      for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
+      continue;
+    }
+#if DISTIR_PLAIN_OPS > 0
+    if (plain_rest) {
+      for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
+      continue;
+    }
+#endif
 #if DISTIR_SEGWALK
     int32_t ef_r = -1;              // binade of this segment's (r0, r1)
     int64_t r0 = kNeverI, r1 = kNeverI;
@@ -510,6 +544,20 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
         seq_plain(x, sg[i].a, sg[i].n);
         DISTIR_CLK_ADD(13, t0);
         reps--;
+        if (plain_after > 0 && ++crossings >= plain_after)
+          for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
+#if DISTIR_PLAIN_OPS > 0
+        {   // few ops left: op by op is cheaper than moving to the new binade
+          int64_t left = reps * sg[i].n;
+#pragma unroll
+          for (int i2 = 0; i2 < NS; i2++)
+            if (i2 > i) left += sg[i2].reps * sg[i2].n;
+          if (left <= DISTIR_PLAIN_OPS) {
+            for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
+            plain_rest = true;
+          }
+        }
+#endif
       }
     }
   }

@@ -57,7 +57,7 @@ static long check(std::mt19937_64& g, int trials, int mode) {
           for (int j = 0; j < sg[i].n; j++) x = x + sg[i].a[j];
       // as the kernels do: fast path, else the single-crossing path, else add_task
       if ((g() & 1) || !task_fast(y, c))
-        if (!(g() & 3) || !task_cross1(y, sg, c, tb, map)) add_task(y, sg, c, tb, map);
+        if (!(g() & 3) || !task_cross1(y, sg, c, tb, map)) add_task(y, sg, c, tb, map, (int)(g() % 3));
       if (std::memcmp(&x, &y, 8) != 0) {
         if (bad < 5) std::printf("mismatch NS=%d mode=%d task=%d plain=%a agg=%a\n", NS, mode, k, x, y);
         bad++;

@@ -267,3 +267,34 @@ def test_nccl_single_rank(sim):
         assert res["topk"]["index"].tolist() == ref["topk"]["index"].tolist()
     finally:
         pkg.distir_nccl_comm_destroy(comm)
+
+
+def test_explicit_gpipe_catch_all_buckets():
+    """More distinct warp shapes (kind, P, L, K) than hash buckets in one
+    explicit list: the GPipe MLP and GPT-2 catch-all buckets (two stages per
+    lane, one configuration per warp) run and agree with the oracle -- and
+    the launch mask includes their kernels."""
+    from paper_2111_05426_b200 import Simulator
+    models = {"m": W.mlp(64, 32), "g": dict(W.MODELS["gpt2_small"], n_layer=40, d_model=64,
+                                            n_head=4, vocab_pad=128, n_ctx=16)}
+    topos = {"TB200": W.TOPOLOGIES["TB200"], "TM4": W.TOPOLOGIES["TM4"]}
+    s = Simulator(models, topos, device=0)
+    rng = np.random.default_rng(4096)
+    cfgs = []
+    for mi in (0, 1):
+        for P in range(1, 41):
+            for K in range(1, 61):
+                cfgs.append((mi, int(rng.integers(2)), 1, 1, P, K, K * int(rng.integers(1, 4))))
+    res = s.eval(configs=cfgs, k=8)
+    idx = np.sort(rng.choice(len(cfgs), size=300, replace=False))
+    ref = {"makespan": [], "peak": [], "reason": []}
+    for i in idx:
+        mi, ti, D, T, P, K, B = cfgs[i]
+        r = oracle.eval_config(models[list(models)[mi]], topos[list(topos)[ti]], D, T, P, K, B)
+        for k in ref:
+            ref[k].append(r[k])
+    ref = {k: np.array(v) for k, v in ref.items()}
+    ref["reason"] = ref["reason"].astype(np.uint32)
+    assert assert_parity({k: res[k][idx] for k in ref}, ref, "catch-all") == 1.0
+    assert res["stats"]["n_buckets"] > 4096
+    s.close()
