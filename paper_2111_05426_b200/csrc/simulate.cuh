@@ -40,9 +40,28 @@ __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int
 #ifndef DISTIR_PLAIN_S1
 #define DISTIR_PLAIN_S1 0   // single-stage configs (S == 1): walk tasks op by op after N crossings (A/B: slower)
 #endif
+// Slow path entry: a warp vote and a uniform branch (DISTIR_VOTE=1), or a
+// plain divergent branch (0: no vote; the slow path has no warp-collective
+// operations).  Measured in isolation (tools/stepbench.cu): the vote and its
+// branch cost ~110 cycles per wavefront step, the divergent branch ~50.
+#ifndef DISTIR_VOTE
+#ifdef DISTIR_INSTR
+#define DISTIR_VOTE 1
+#else
+#define DISTIR_VOTE 0
+#endif
+#endif
+#if DISTIR_VOTE
+#define DISTIR_ANY(p) __any_sync(0xffffffffu, (p))
+#else
+#define DISTIR_ANY(p) (p)
+#endif
 #ifndef DISTIR_CROSS1
 #define DISTIR_CROSS1 0     // straight-line single-binade-crossing slow path (task_cross1):
                             // faster single long configurations, slower grids (registers)
+#endif
+#if DISTIR_CROSS1 && !DISTIR_VOTE
+#error "DISTIR_CROSS1 uses warp votes inside the slow path: build with DISTIR_VOTE=1"
 #endif
 // Segment -> distinct-op-list maps of the task caches (BinTab).
 __device__ constexpr int kMapId3[3] = {0, 1, 2};
@@ -218,7 +237,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     }
     const bool slow = task_fast_or_slow(clk[q], cf[q], act);
     DISTIR_SLOW_T0
-    const bool any = __any_sync(0xffffffffu, slow);
+    const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[3];
       fsegs(q, sg);
@@ -227,7 +246,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], cf[q], btf)))
         s2 = slow && !task_cross1(clk[q], sg, cf[q], btf, kMapId3);
-      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk[q], sg, cf[q], btf, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, cf[q], btf, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -237,7 +256,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     }
     const bool slow = task_fast_or_slow(clk[q], cb[q], act);
     DISTIR_SLOW_T0
-    const bool any = __any_sync(0xffffffffu, slow);
+    const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[NB];
       bsegs(q, sg);
@@ -246,7 +265,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         if constexpr (RC) s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd);
         else s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd4);
       }
-      if (__any_sync(0xffffffffu, s2) && s2) {
+      if (DISTIR_ANY(s2) && s2) {
         if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd, S == 1 ? DISTIR_PLAIN_S1 : 0);
         else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4, S == 1 ? DISTIR_PLAIN_S1 : 0);
       }
@@ -618,7 +637,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     }
     const bool slow = task_fast_or_slow(clk[q], tc[q], act);
     DISTIR_SLOW_T0
-    const bool any = __any_sync(0xffffffffu, slow);
+    const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[3];
       segs(q, sg);
@@ -627,7 +646,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], tc[q], bt)))
         s2 = slow && !task_cross1(clk[q], sg, tc[q], bt, kMapId3);
-      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -866,7 +885,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
     const double mx = segmax(clk);
     if (act) clk = mx;
     const bool slow = task_fast_or_slow(clk, cf, act);
-    const bool any = __any_sync(0xffffffffu, slow);
+    const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[3];
       fsegs(sg);
@@ -875,14 +894,14 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk, cf, bt)))
         s2 = slow && !task_cross1(clk, sg, cf, bt, kMapId3);
-      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk, sg, cf, bt, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk, sg, cf, bt, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
     }
   };
   auto bwd_task = [&](bool act) {
     const double mx = segmax(clk);
     if (act) clk = mx;
     const bool slow = task_fast_or_slow(clk, cb, act);
-    const bool any = __any_sync(0xffffffffu, slow);
+    const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[9];
       bsegs(sg);
@@ -891,7 +910,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk, cb, bt)))
         s2 = slow && !task_cross1(clk, sg, cb, bt, kMapZeroBwd);
-      if (__any_sync(0xffffffffu, s2) && s2) add_task(clk, sg, cb, bt, kMapZeroBwd, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk, sg, cb, bt, kMapZeroBwd, S == 1 ? DISTIR_PLAIN_S1 : 0);
     }
     if (act && own(hi - 1)) clk = dadd(clk, row[18]);       // the last Add: owner only
   };
