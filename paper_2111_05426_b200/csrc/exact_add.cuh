@@ -34,15 +34,6 @@
 #ifndef DISTIR_PLAIN_AFTER
 #define DISTIR_PLAIN_AFTER 0   // crossings after which a task is walked op by op (0: never)
 #endif
-#ifndef DISTIR_PLAIN_OPS
-#define DISTIR_PLAIN_OPS 0     // after a crossing, walk the rest op by op when <= this many ops
-#endif
-#ifndef DISTIR_PLAIN_ZERO
-#define DISTIR_PLAIN_ZERO 0    // a task from a zero clock is walked op by op
-#endif
-#ifndef DISTIR_SEGWALK
-#define DISTIR_SEGWALK 0   // per-segment binade increments in the slow walk
-#endif
 #ifndef DISTIR_UNROLL_SEG
 #define DISTIR_UNROLL_SEG 0
 #endif
@@ -462,53 +453,22 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
     }
   }
 #pragma unroll
-#if DISTIR_PLAIN_OPS > 0
-  bool plain_rest = false;
-#endif
   for (int i = 0; i < NS; i++) {
     int64_t reps = sg[i].reps;
     if (plain_after > 0 && crossings >= plain_after) {
       for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
       continue;
     }
-#if DISTIR_PLAIN_OPS > 0
-    if (plain_rest) {
-      for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
-      continue;
-    }
-#endif
-#if DISTIR_SEGWALK
-    int32_t ef_r = -1;              // binade of this segment's (r0, r1)
-    int64_t r0 = kNeverI, r1 = kNeverI;
-#endif
     while (reps > 0) {
       const int64_t xb = d2bits(x);
       const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
       if (x > 0.0 && ef >= 53 && ef <= 1993) {
-#if DISTIR_SEGWALK
-        // only this segment's increments in binade ef (table, cache or one
-        // seg_pass); the cache follows x once, after the task
-        if (ef != ef_r) {
-          const long long t0 = DISTIR_CLK_NOW();
-          if (ef == c.ef) {
-            r0 = c.R[2 * i]; r1 = c.R[2 * i + 1];
-          } else if (ef - t.e0 >= 0 && ef - t.e0 < t.nb) {
-            const int64_t* row = t.tab + ((int64_t)(ef - t.e0) * t.nu + map[i]) * 2;
-            r0 = row[0]; r1 = row[1];
-          } else {
-            seg_pass(sg[i].a, sg[i].n, ef, r0, r1);
-          }
-          ef_r = ef;
-          DISTIR_CLK_ADD(12, t0);
-        }
-#else
         if (ef != c.ef) {
           const long long t0 = DISTIR_CLK_NOW();
           task_refresh(c, ef, sg, t, map);
           DISTIR_CLK_ADD(12, t0);
         }
         const int64_t r0 = c.R[2 * i], r1 = c.R[2 * i + 1];
-#endif
         if (r0 < kNeverI) {
           int64_t M = (xb & kMant) | kHidden;
           const int64_t before = reps;
@@ -546,31 +506,9 @@ DISTIR_HD_COLD void add_task(double& x, const Seg (&sg)[NS], TaskCache& c, const
         reps--;
         if (plain_after > 0 && ++crossings >= plain_after)
           for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
-#if DISTIR_PLAIN_OPS > 0
-        {   // few ops left: op by op is cheaper than moving to the new binade
-          int64_t left = reps * sg[i].n;
-#pragma unroll
-          for (int i2 = 0; i2 < NS; i2++)
-            if (i2 > i) left += sg[i2].reps * sg[i2].n;
-          if (left <= DISTIR_PLAIN_OPS) {
-            for (; reps > 0; reps--) seq_plain(x, sg[i].a, sg[i].n);
-            plain_rest = true;
-          }
-        }
-#endif
       }
     }
   }
-#if DISTIR_SEGWALK
-  {
-    const int32_t ef = exp_field(x);
-    if (x > 0.0 && ef >= 53 && ef <= 1993 && ef != c.ef) {
-      const long long t0 = DISTIR_CLK_NOW();
-      task_refresh(c, ef, sg, t, map);
-      DISTIR_CLK_ADD(12, t0);
-    }
-  }
-#endif
   DISTIR_CLK_ADD(15, t_all);
 }
 

@@ -37,9 +37,6 @@ __device__ __forceinline__ double min_pos(double m, double x) { return x > 0.0 &
 // per-lane shared-memory storage reused for integer per-pass increments
 __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int64_t*>(p); }
 
-#ifndef DISTIR_PLAIN_S1
-#define DISTIR_PLAIN_S1 0   // single-stage configs (S == 1): walk tasks op by op after N crossings (A/B: slower)
-#endif
 // Slow path entry: a warp vote and a uniform branch (DISTIR_VOTE=1), or a
 // plain divergent branch (0: no vote; the slow path has no warp-collective
 // operations).  Measured in isolation (tools/stepbench.cu): the vote and its
@@ -246,7 +243,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], cf[q], btf)))
         s2 = slow && !task_cross1(clk[q], sg, cf[q], btf, kMapId3);
-      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, cf[q], btf, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, cf[q], btf, kMapId3);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -266,8 +263,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         else s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd4);
       }
       if (DISTIR_ANY(s2) && s2) {
-        if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd, S == 1 ? DISTIR_PLAIN_S1 : 0);
-        else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4, S == 1 ? DISTIR_PLAIN_S1 : 0);
+        if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd);
+        else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4);
       }
     }
     DISTIR_SLOW_T1(any)
@@ -646,7 +643,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], tc[q], bt)))
         s2 = slow && !task_cross1(clk[q], sg, tc[q], bt, kMapId3);
-      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3);
     }
     DISTIR_SLOW_T1(any)
   };
@@ -894,7 +891,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk, cf, bt)))
         s2 = slow && !task_cross1(clk, sg, cf, bt, kMapId3);
-      if (DISTIR_ANY(s2) && s2) add_task(clk, sg, cf, bt, kMapId3, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk, sg, cf, bt, kMapId3);
     }
   };
   auto bwd_task = [&](bool act) {
@@ -910,7 +907,7 @@ __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, in
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk, cb, bt)))
         s2 = slow && !task_cross1(clk, sg, cb, bt, kMapZeroBwd);
-      if (DISTIR_ANY(s2) && s2) add_task(clk, sg, cb, bt, kMapZeroBwd, S == 1 ? DISTIR_PLAIN_S1 : 0);
+      if (DISTIR_ANY(s2) && s2) add_task(clk, sg, cb, bt, kMapZeroBwd);
     }
     if (act && own(hi - 1)) clk = dadd(clk, row[18]);       // the last Add: owner only
   };
