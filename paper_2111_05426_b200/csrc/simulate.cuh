@@ -294,16 +294,22 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       return (((int64_t)t * 2 + cls) * 64 + lower) * 2 + kind;
     };
     constexpr int64_t kDone = INT64_MAX;
+#ifndef DISTIR_F1B_TASKS
+#define DISTIR_F1B_TASKS 2
+#endif
+    constexpr int kF1bTasks = DISTIR_F1B_TASKS;
     int jt = 0, ka_in = 0, ka_out = 0, kg_out = 0, kg_in = 0;
     const int n_tasks = ok[0] ? 2 * Ki : 0;
     // every iteration runs >= 1 event of each configuration (its globally
     // first one); the guard only bounds a broken schedule
     const int max_iter = warp_max_int(has ? 4 * Pi * Ki + 64 : 0);
-    for (int iter = 0; iter < max_iter; iter++) {
-      // next event of each stream of this stage
+    // next event of this stage's five streams (task, recv act, send act,
+    // send grad, recv grad), by the unit-time keys
+    auto next_event = [&](int& which, int& tkind) {
       int64_t best = kDone;
-      int which = -1;                  // 0 task, 1 recvA, 2 sendA, 3 sendG, 4 recvG
-      int tkind = 0, tk = 0;
+      int tk = 0;
+      which = -1;
+      tkind = 0;
       if (jt < n_tasks) {
         if (jt < w) { tkind = 0; tk = jt; }
         else if (jt < 2 * Ki - w) { const int jj = jt - w; tkind = jj & 1; tk = (jj >> 1) + (tkind ? 0 : w); }
@@ -328,6 +334,17 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         const int64_t k2 = key(2 * Pi - (st + 1) + 2 * kg_in, 0, st, 1);
         if (k2 < best) { best = k2; which = 4; }
       }
+    };
+    for (int iter = 0; iter < max_iter; iter++) {
+      int which, tkind;
+      next_event(which, tkind);
+      // tasks need no partner: a stage runs up to kF1bTasks consecutive
+      // tasks before the send round (its per-device order is unchanged)
+      for (int r = 0; r < kF1bTasks && __any_sync(0xffffffffu, which == 0); r++) {
+        fwd_task(0, which == 0 && tkind == 0);
+        bwd_task(0, which == 0 && tkind == 1);
+        if (which == 0) { jt++; next_event(which, tkind); }
+      }
       if (!__any_sync(0xffffffffu, which >= 0)) break;
       // rendezvous identity (lower stage, direction, microbatch); -1 = none
       const int my_id = which == 1 ? ((st - 1) << 14 | ka_in)
@@ -338,9 +355,6 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       const int dn_id = __shfl_up_sync(0xffffffffu, my_id, 1);
       const double up_c = __shfl_down_sync(0xffffffffu, clk[0], 1);
       const double dn_c = __shfl_up_sync(0xffffffffu, clk[0], 1);
-      fwd_task(0, which == 0 && tkind == 0);                   // all lanes call both:
-      bwd_task(0, which == 0 && tkind == 1);                   // warp-uniform votes
-      if (which == 0) jt++;
       const bool down_link = which == 1 || which == 3;         // partner s - 1
       const bool ready = which > 0 && (down_link ? (sl > 0 && dn_id == my_id)
                                                  : (sl < S - 1 && up_id == my_id));
