@@ -294,8 +294,11 @@ class Simulator:
         return n.value
 
     def workspace(self, n_configs):
+        if getattr(self, "_ws_n", None) == n_configs and self.ws is not None:
+            return self.ws
         b = ctypes.c_size_t()
         _check(lib.distir_workspace_size(self.handle, n_configs, ctypes.byref(b)))
+        self._ws_n = n_configs
         if self.ws is None or self.ws.numel() < b.value:
             self.ws = self.torch.empty(b.value, dtype=self.torch.uint8,
                                        device=self.device)
@@ -311,10 +314,13 @@ class Simulator:
         handle's pinned buffers that the next call overwrites."""
         torch = self.torch
         if grid is not None:
-            key = repr(sorted(grid.items()))
-            if getattr(self, "_spec_key", None) != key:
+            # re-marshal the spec only when the grid changed (dict equality,
+            # against a copy, so in-place edits of the caller's dict count)
+            src = getattr(self, "_spec_src", None)
+            if src is None or grid != src:
                 self._spec_cache = (self.spec(grid), self.grid_size(grid))
-                self._spec_key = key
+                self._spec_src = {k: (list(v) if isinstance(v, list) else v)
+                                  for k, v in grid.items()}
             sp, n = self._spec_cache
             cf, ncf = None, 0
         else:
