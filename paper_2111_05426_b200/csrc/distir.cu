@@ -467,7 +467,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     PlanBudget pb;
     for (int g = 0; g < kGroups; g++)
       pb.warps[g] = (uint32_t)(sim->plan_x * sim->sim_grid[g] * (sim_tpb(g / kModes, g % kModes) / 32));
-    k_plan<<<1, 1024, 0, st>>>(bk, hdr, pb);
+    k_plan<<<1, kPlanThreads, 0, st>>>(bk, hdr, pb);
     k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, perm, items);
     kernels += 3;
   }

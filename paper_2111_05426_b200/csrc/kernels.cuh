@@ -356,7 +356,9 @@ __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
 // warp's time grows with the configs it holds: while a simulate kernel has
 // more resident warps than items, the heaviest classes are split into items
 // of fewer configurations (cpw halved per step, heaviest class first).
-__global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, PlanBudget budget) {
+constexpr int kPlanThreads = 1024;   // k_plan's block size (distir.cu launch)
+__global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
+                                                       PlanBudget budget) {
   __shared__ unsigned int s_items[kGroups][kNumClasses];
   __shared__ unsigned int s_alt[kGroups][kNumClasses][kMaxSplit + 1];   // items at split j
   __shared__ unsigned char s_shift[kGroups][kNumClasses];
@@ -369,9 +371,22 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
   }
   if (threadIdx.x == 0) { s_cfg = 0; s_nb = 0; }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
+  // thread t owns bucket slots t, t + 1024, ...: their count, class, group,
+  // lanes and item offset stay in registers across the passes (no global
+  // re-reads of what this thread just wrote)
+  constexpr int kPer = (kBucketSlots + kPlanThreads - 1) / kPlanThreads;
+  uint32_t cnt[kPer], grp[kPer], cls_[kPer], lanes_[kPer], off[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; u++) {
+    const int b = threadIdx.x + u * kPlanThreads;
+    cnt[u] = b < kBucketSlots ? bk[b].count : 0u;
+    grp[u] = cls_[u] = lanes_[u] = off[u] = 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; u++) {
+    const int b = threadIdx.x + u * kPlanThreads;
+    if (cnt[u] == 0) continue;
     Bucket& B = bk[b];
-    if (B.count == 0) continue;
     uint32_t lanes, cls, group;
     if (b >= kOverflowBucket) {        // mixed shapes: one config per warp
       lanes = 32;
@@ -405,12 +420,13 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
     B.lanes = (uint16_t)lanes;
     B.cls = (uint16_t)cls;
     B.group = (uint16_t)group;
+    lanes_[u] = lanes; cls_[u] = cls; grp[u] = group;
     const uint32_t cpw = 32 / lanes;
     for (int j = 0; j <= kMaxSplit; j++) {
       const uint32_t cj = (cpw >> j) ? (cpw >> j) : 1u;
-      atomicAdd(&s_alt[group][cls][j], (B.count + cj - 1) / cj);
+      atomicAdd(&s_alt[group][cls][j], (cnt[u] + cj - 1) / cj);
     }
-    B.cfg_base = atomicAdd(&s_cfg, B.count);
+    B.cfg_base = atomicAdd(&s_cfg, cnt[u]);
     B.cursor = 0;
     atomicAdd(&s_nb, 1u);
   }
@@ -431,13 +447,14 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
     }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
-    Bucket& B = bk[b];
-    if (B.count == 0) continue;
-    const uint32_t cpw0 = 32u / B.lanes, sh = s_shift[B.group][B.cls];
+#pragma unroll
+  for (int u = 0; u < kPer; u++) {
+    if (cnt[u] == 0) continue;
+    const int b = threadIdx.x + u * kPlanThreads;
+    const uint32_t cpw0 = 32u / lanes_[u], sh = s_shift[grp[u]][cls_[u]];
     const uint32_t cpw = (cpw0 >> sh) ? (cpw0 >> sh) : 1u;
-    B.cpw = (uint16_t)cpw;
-    B.item_off = atomicAdd(&s_items[B.group][B.cls], (B.count + cpw - 1) / cpw);
+    bk[b].cpw = (uint16_t)cpw;
+    off[u] = atomicAdd(&s_items[grp[u]][cls_[u]], (cnt[u] + cpw - 1) / cpw);
   }
   __syncthreads();
   // item numbering: group-major, heaviest class first (per-group prefix by
@@ -465,10 +482,12 @@ __global__ void k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr, Plan
     }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBucketSlots; b += blockDim.x) {
-    Bucket& B = bk[b];
-    if (B.count == 0) continue;
-    B.item_base = s_base[B.group][B.cls] + B.item_off;
+#pragma unroll
+  for (int u = 0; u < kPer; u++) {
+    if (cnt[u] == 0) continue;
+    const int b = threadIdx.x + u * kPlanThreads;
+    bk[b].item_off = off[u];
+    bk[b].item_base = s_base[grp[u]][cls_[u]] + off[u];
   }
 }
 
