@@ -298,3 +298,27 @@ def test_explicit_gpipe_catch_all_buckets():
     assert assert_parity({k: res[k][idx] for k in ref}, ref, "catch-all") == 1.0
     assert res["stats"]["n_buckets"] > 4096
     s.close()
+
+
+def test_interleaved_uploads_and_evals(sim):
+    """The handle's pinned staging block is reused by every upload / eval:
+    back-to-back asynchronous uploads and synchronous evaluations of
+    different grids each see their own spec, and zero-copy results
+    (copy=False) are views that the next call overwrites."""
+    import torch
+    w1 = oracle.grid_result(W.GRIDS["W1"], k=10)
+    n3 = sim.upload(W.GRIDS["W3"])                 # async H2D from the staging block
+    r1 = sim.eval(W.GRIDS["W1"], k=10)             # reuses it before the launch
+    assert (r1["peak"] == w1["peak"]).all() and r1["topk"]["index"].tolist() == w1["topk_index"].tolist()
+    n2 = sim.upload(W.GRIDS["W2"])
+    n2b = sim.upload(W.GRIDS["W2"])                # twice in a row: waits for the first copy
+    assert n2 == n2b == 1860 and n3 == 8680
+    outs = sim.device_outputs(n2, k=10)
+    sim.launch(outs, k=10)
+    torch.cuda.synchronize()
+    ref2 = sim.eval(W.GRIDS["W2"], k=10)
+    assert (outs["peak"].cpu().numpy()[:n2] == ref2["peak"]).all()
+    v = sim.eval(W.GRIDS["W1"], k=10, copy=False)
+    first = v["peak"].copy()
+    sim.eval(W.GRIDS["W2"], k=10, copy=False)
+    assert not np.array_equal(v["peak"], first) or len(first) == 0   # overwritten view
