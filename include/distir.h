@@ -81,7 +81,7 @@ enum {
  * padded vocabulary and an optional LM head.  dtype_bytes = 2 (16-bit values,
  * P:543); id_bytes = bytes per token id.  schedule (MLP training only): the
  * pipeline schedule of the D/T/P transform, DISTIR_SCHED_GPIPE (north_star)
- * or DISTIR_SCHED_1F1B (the paper's synchronous 1F1B; P <= 32).
+ * or DISTIR_SCHED_1F1B (the paper's synchronous 1F1B).
  * recompute / zero (MLP training only, 0 or 1, DESIGN
  * readings R8 / R9): the memory-saving variants of the Appendix --
  *   recompute: gradient checkpointing (Fig. 8): a stage keeps its

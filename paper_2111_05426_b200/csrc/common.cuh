@@ -23,8 +23,9 @@ constexpr int kBucketSlots = kNumBuckets + 4;   // + MLP, GPT-2, MLP-1F1B, MLP-Z
 // modes 3-4: wavefront, one lane per stage (mode 4: two stages per lane,
 // 32 < P <= 64, and the catch-all buckets); mode 5 (MLP only): the 1F1B
 // co-simulation, one lane per stage, P <= 32; mode 6 (MLP only): ZeRO (f4),
-// one lane per (stage, replica), next_pow2(P) * D <= 32.
-constexpr int kModes = 7;
+// one lane per (stage, replica), next_pow2(P) * D <= 32; mode 7 (MLP only):
+// 1F1B with two stages per lane, 32 < P <= 64, and the 1F1B catch-all.
+constexpr int kModes = 8;
 constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr int kMaxSplit = 5;        // configs per item divided by up to 2^5

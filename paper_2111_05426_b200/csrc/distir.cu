@@ -293,16 +293,14 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
   if (g->n_batch < 1 || g->n_batch > 32) return fail(DISTIR_E_INVALID_ARG, "spec.n_batch");
   if (g->n_k < 0 || g->n_k > 16) return fail(DISTIR_E_INVALID_ARG, "spec.n_k");
   if (g->k_mode != 0 && g->k_mode != 1) return fail(DISTIR_E_INVALID_ARG, "spec.k_mode");
-  bool any_1f1b = false, any_zero = false;
+  bool any_zero = false;
   for (int mi = 0; mi < g->n_models; mi++) {
-    any_1f1b |= sim->models[g->models[mi]].sched == 1;
     any_zero |= sim->models[g->models[mi]].kind == 0 && sim->models[g->models[mi]].zero != 0;
   }
   for (int i = 0; i < g->n_world; i++) {
     if (!is_pow2(g->world[i]) || (i && g->world[i] <= g->world[i - 1]))
       return fail(DISTIR_E_INVALID_ARG, "spec.world: ascending powers of two");
     if (g->world[i] > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
-    if (any_1f1b && g->world[i] > 32) return fail(DISTIR_E_UNSUPPORTED, "1F1B with world size > 32");
     if (any_zero && g->world[i] > 32) return fail(DISTIR_E_UNSUPPORTED, "ZeRO with world size > 32");
   }
   for (int i = 0; i < g->n_batch; i++) {
@@ -328,7 +326,7 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     uint32_t m = 0;
     for (int mi = 0; mi < g->n_models; mi++) {
       const DModel& M = sim->models[g->models[mi]];
-      if (M.kind == 0 && M.sched == 1) { m |= gbit(0, 5); continue; }
+      if (M.kind == 0 && M.sched == 1) { m |= gbit(0, 5) | (wmax > 32 ? gbit(0, 7) : 0); continue; }
       m |= gbit(M.kind, 3);
       if (wmax > 32) m |= gbit(M.kind, 4);
       if (M.kind == 0 && M.zero) m |= gbit(0, 6);
@@ -374,8 +372,6 @@ distir_status validate_configs(const distir_sim* sim, const distir_config* cf, i
     if (!is_pow2(c.dp) || !is_pow2(c.tp))
       return fail(DISTIR_E_UNSUPPORTED, "config dp/tp must be powers of two (stage symmetry)");
     if ((int64_t)c.dp * c.tp * c.pp > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
-    if (sim->models[c.model].sched == 1 && c.pp > 32)
-      return fail(DISTIR_E_UNSUPPORTED, "1F1B with more than 32 stages");
     if (sim->models[c.model].kind == 0 && sim->models[c.model].zero && c.dp > 1) {
       int64_t p2 = 1;
       while (p2 < c.pp) p2 <<= 1;
@@ -492,6 +488,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     if (sp.f1b & gbit(0, 4)) { DISTIR_SIM(0, 4); kernels++; }
     if (sp.f1b & gbit(0, 5)) { DISTIR_SIM(0, 5); kernels++; }
     if (sp.f1b & gbit(0, 6)) { DISTIR_SIM(0, 6); kernels++; }
+    if (sp.f1b & gbit(0, 7)) { DISTIR_SIM(0, 7); kernels++; }
     if (sp.f1b & gbit(1, 3)) { DISTIR_SIM(1, 3); kernels++; }
     if (sp.f1b & gbit(1, 4)) { DISTIR_SIM(1, 4); kernels++; }
 #undef DISTIR_SIM
@@ -643,12 +640,13 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
     for (int64_t i = 0; i < n_configs; i++) {
       const DModel& M = sim->models[configs[i].model];
       kinds |= 1u << (M.kind == 0 && M.sched == 1 ? 2 : M.kind == 0 && M.zero && configs[i].dp > 1 ? 3 : M.kind);
-      if (M.kind == 0 && M.sched == 1) m |= gbit(0, 5);
+      if (M.kind == 0 && M.sched == 1) m |= configs[i].pp > 32 ? gbit(0, 7) : gbit(0, 5);
       else if (M.kind == 0 && M.zero && configs[i].dp > 1) m |= gbit(0, 6);
       else m |= gbit(M.kind, configs[i].pp > 32 ? 4 : 3);
     }
     if (n_configs > kNumBuckets / 2)
-      m |= ((kinds & 1) ? gbit(0, 4) : 0) | ((kinds & 2) ? gbit(1, 4) : 0);
+      m |= ((kinds & 1) ? gbit(0, 4) : 0) | ((kinds & 2) ? gbit(1, 4) : 0) |
+           ((kinds & 4) ? gbit(0, 7) : 0);
     sp.f1b = m;
   }
   sp.n_total = n_total;
@@ -749,9 +747,9 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   const void* fns[kGroups] = {
       (const void*)k_simulate<0, 0>, (const void*)k_simulate<0, 1>, (const void*)k_simulate<0, 2>,
       (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<0, 5>,
-      (const void*)k_simulate<0, 6>,
+      (const void*)k_simulate<0, 6>, (const void*)k_simulate<0, 7>,
       (const void*)k_simulate<1, 0>, (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>,
-      (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr, nullptr};
+      (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr, nullptr, nullptr};
   for (int g = 0; g < kGroups && e == cudaSuccess; g++) {
     if (!fns[g]) continue;
     const int smem = sim_smem(g / kModes, g % kModes);

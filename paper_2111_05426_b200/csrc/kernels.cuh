@@ -392,10 +392,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, 
       lanes = 32;
       cls = kNumClasses - 1;
       // MLP / GPT-2 catch-alls run two stages per lane (any P <= 64); the
-      // 1F1B catch-all (P <= 32 by validation) one stage per lane; the ZeRO
+      // 1F1B catch-all two stages per lane (mode 7, any P <= 64); the ZeRO
       // catch-all one (stage, replica) per lane
       group = b == kOverflowBucket + 3 ? 6
-            : b == kOverflowBucket + 2 ? 5 : (uint32_t)(b - kOverflowBucket) * kModes + 4;
+            : b == kOverflowBucket + 2 ? 7 : (uint32_t)(b - kOverflowBucket) * kModes + 4;
     } else {
       const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, K = (B.key >> 17) & 255;
       uint32_t mode;
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, 
         est = (2ull * K + P) * 4;
       } else {
         lanes = P < 32 ? pow2ceil32(P) : 32;
-        mode = (B.key >> 25) & 1 ? 5 : P > 32 ? 4 : 3;
+        mode = (B.key >> 25) & 1 ? (P > 32 ? 7 : 5) : P > 32 ? 4 : 3;
         est = (2ull * K + P) * (kind ? 1ull : 2ull) * 2;
       }
       cls = 63 - __clzll(est + 1);
@@ -517,7 +517,7 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
 // Persistent simulate kernel for one group (model kind x stages per lane):
 // each warp pulls work items of its group, heaviest weight class first.
 __host__ __device__ constexpr int sim_v(int mode) {
-  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : mode == 4 ? 2 : 1;
+  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : (mode == 4 || mode == 7) ? 2 : 1;
 }
 __host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per lane row
   return kind == 1 ? 19 + 6 * sim_v(mode) : mode == 6 ? 43 : 15 + 20 * sim_v(mode);
@@ -601,9 +601,9 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
     if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk);
     else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk);
     else if (warp_max_int(has ? c.M.rc : 0))          // bucket key: warp-uniform
-      run_mlp<V, SEQ, MODE == 5, true>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+      run_mlp<V, SEQ, MODE == 5 || MODE == 7, true>(c, tp, has, sl, S, lane, row, tab, ms, pk);
     else
-      run_mlp<V, SEQ, MODE == 5, false>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+      run_mlp<V, SEQ, MODE == 5 || MODE == 7, false>(c, tp, has, sl, S, lane, row, tab, ms, pk);
 #ifdef DISTIR_INSTR
     if (lane == 0) {
       const unsigned long long dt = (unsigned long long)(clock64() - t0);

@@ -273,8 +273,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     DISTIR_SLOW_T1(any)
   };
   if constexpr (F1B) {
-    static_assert(V == 1 && !SEQ, "1F1B: one stage per lane");
-    // (validation keeps 1F1B configurations at P <= 32)
+    static_assert(!SEQ, "1F1B: wavefront lanes");
     // ---- synchronous 1F1B (NEXT row f1).  Stage s's ops are the
     // PipeDream-flush sequence (w = min(P-1-s, K) warm-up forwards, then
     // F(w+i), B(i) pairs, then the remaining backwards) interleaved with its
@@ -282,12 +281,11 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     // that schedule F(k, s) starts at s + k (k <= w) or 2k + s, B(k, s) at
     // 2P - 1 - s + 2k, and a Send happens when its producer finishes; Sends
     // precede tasks at equal times, then by lower stage, forward first.  The
-    // warp co-simulates the stages (lane = stage): a lane whose next event is
-    // a task runs it; a Send runs when both ends have it next (rendezvous,
-    // P:119).  This is exactly the per-device order of the oracle's program.
-    const int st = s[0];
+    // warp co-simulates the stages (lane = stage; with V = 2, 32 < P <= 64,
+    // a lane holds stages sl and sl + 32): a stage whose next event is a task
+    // runs it; a Send runs when both ends have it next (rendezvous).
+    // This is exactly the per-device order of the oracle's program.
     const int Pi = (int)P, Ki = (int)K;
-    const int w = Pi - 1 - st < Ki ? Pi - 1 - st : Ki;
     auto fstart = [&](int k, int ss) {
       const int ww = Pi - 1 - ss < Ki ? Pi - 1 - ss : Ki;
       return k <= ww ? ss + k : 2 * k + ss;
@@ -301,73 +299,100 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 #define DISTIR_F1B_TASKS 2
 #endif
     constexpr int kF1bTasks = DISTIR_F1B_TASKS;
-    int jt = 0, ka_in = 0, ka_out = 0, kg_out = 0, kg_in = 0;
-    const int n_tasks = ok[0] ? 2 * Ki : 0;
+    int wu[V], jt[V], ka_in[V], ka_out[V], kg_out[V], kg_in[V], n_tasks[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      wu[q] = Pi - 1 - s[q] < Ki ? Pi - 1 - s[q] : Ki;
+      jt[q] = ka_in[q] = ka_out[q] = kg_out[q] = kg_in[q] = 0;
+      n_tasks[q] = ok[q] ? 2 * Ki : 0;
+    }
     // every iteration runs >= 1 event of each configuration (its globally
     // first one); the guard only bounds a broken schedule
     const int max_iter = warp_max_int(has ? 4 * Pi * Ki + 64 : 0);
-    // next event of this stage's five streams (task, recv act, send act,
+    // next event of stage slot q's five streams (task, recv act, send act,
     // send grad, recv grad), by the unit-time keys
-    auto next_event = [&](int& which, int& tkind) {
+    auto next_event = [&](int q, int& which, int& tkind) {
+      const int st = s[q];
       int64_t best = kDone;
       int tk = 0;
       which = -1;
       tkind = 0;
-      if (jt < n_tasks) {
-        if (jt < w) { tkind = 0; tk = jt; }
-        else if (jt < 2 * Ki - w) { const int jj = jt - w; tkind = jj & 1; tk = (jj >> 1) + (tkind ? 0 : w); }
-        else { tkind = 1; tk = jt - Ki; }
+      if (jt[q] < n_tasks[q]) {
+        const int w = wu[q];
+        if (jt[q] < w) { tkind = 0; tk = jt[q]; }
+        else if (jt[q] < 2 * Ki - w) { const int jj = jt[q] - w; tkind = jj & 1; tk = (jj >> 1) + (tkind ? 0 : w); }
+        else { tkind = 1; tk = jt[q] - Ki; }
         const int t = tkind ? 2 * Pi - 1 - st + 2 * tk : fstart(tk, st);
         best = key(t, 1, st, tkind);
         which = 0;
       }
-      if (ok[0] && st > 0 && ka_in < Ki) {
-        const int64_t k2 = key(fstart(ka_in, st - 1) + 1, 0, st - 1, 0);
+      if (ok[q] && st > 0 && ka_in[q] < Ki) {
+        const int64_t k2 = key(fstart(ka_in[q], st - 1) + 1, 0, st - 1, 0);
         if (k2 < best) { best = k2; which = 1; }
       }
-      if (ok[0] && st < Pi - 1 && ka_out < Ki) {
-        const int64_t k2 = key(fstart(ka_out, st) + 1, 0, st, 0);
+      if (ok[q] && st < Pi - 1 && ka_out[q] < Ki) {
+        const int64_t k2 = key(fstart(ka_out[q], st) + 1, 0, st, 0);
         if (k2 < best) { best = k2; which = 2; }
       }
-      if (ok[0] && st > 0 && kg_out < Ki) {
-        const int64_t k2 = key(2 * Pi - st + 2 * kg_out, 0, st - 1, 1);
+      if (ok[q] && st > 0 && kg_out[q] < Ki) {
+        const int64_t k2 = key(2 * Pi - st + 2 * kg_out[q], 0, st - 1, 1);
         if (k2 < best) { best = k2; which = 3; }
       }
-      if (ok[0] && st < Pi - 1 && kg_in < Ki) {
-        const int64_t k2 = key(2 * Pi - (st + 1) + 2 * kg_in, 0, st, 1);
+      if (ok[q] && st < Pi - 1 && kg_in[q] < Ki) {
+        const int64_t k2 = key(2 * Pi - (st + 1) + 2 * kg_in[q], 0, st, 1);
         if (k2 < best) { best = k2; which = 4; }
       }
     };
     for (int iter = 0; iter < max_iter; iter++) {
-      int which, tkind;
-      next_event(which, tkind);
+      int which[V], tkind[V];
+#pragma unroll
+      for (int q = 0; q < V; q++) next_event(q, which[q], tkind[q]);
       // tasks need no partner: a stage runs up to kF1bTasks consecutive
       // tasks before the send round (its per-device order is unchanged)
-      for (int r = 0; r < kF1bTasks && __any_sync(0xffffffffu, which == 0); r++) {
-        fwd_task(0, which == 0 && tkind == 0);
-        bwd_task(0, which == 0 && tkind == 1);
-        if (which == 0) { jt++; next_event(which, tkind); }
+      for (int r = 0; r < kF1bTasks; r++) {
+        bool anyt = false;
+#pragma unroll
+        for (int q = 0; q < V; q++) anyt |= which[q] == 0;
+        if (!__any_sync(0xffffffffu, anyt)) break;
+#pragma unroll
+        for (int q = 0; q < V; q++) {
+          fwd_task(q, which[q] == 0 && tkind[q] == 0);
+          bwd_task(q, which[q] == 0 && tkind[q] == 1);
+          if (which[q] == 0) { jt[q]++; next_event(q, which[q], tkind[q]); }
+        }
       }
-      if (!__any_sync(0xffffffffu, which >= 0)) break;
+      bool anye = false;
+#pragma unroll
+      for (int q = 0; q < V; q++) anye |= which[q] >= 0;
+      if (!__any_sync(0xffffffffu, anye)) break;
       // rendezvous identity (lower stage, direction, microbatch); -1 = none
-      const int my_id = which == 1 ? ((st - 1) << 14 | ka_in)
-                      : which == 2 ? (st << 14 | ka_out)
-                      : which == 3 ? ((st - 1) << 14 | 1 << 13 | kg_out)
-                      : which == 4 ? (st << 14 | 1 << 13 | kg_in) : -1;
-      const int up_id = __shfl_down_sync(0xffffffffu, my_id, 1);
-      const int dn_id = __shfl_up_sync(0xffffffffu, my_id, 1);
-      const double up_c = __shfl_down_sync(0xffffffffu, clk[0], 1);
-      const double dn_c = __shfl_up_sync(0xffffffffu, clk[0], 1);
-      const bool down_link = which == 1 || which == 3;         // partner s - 1
-      const bool ready = which > 0 && (down_link ? (sl > 0 && dn_id == my_id)
-                                                 : (sl < S - 1 && up_id == my_id));
-      if (ready) {
-        const double other = down_link ? dn_c : up_c;
-        clk[0] = dadd(fmax(clk[0], other), down_link ? sendb[0] : sendf[0]);
-        if (which == 1) { MEM(0, m * kin[lo[0] & 1] * e, 0); ka_in++; }        // recv act
-        else if (which == 2) { ka_out++; }                                    // send act
-        else if (which == 3) { live[0] -= m * kin[lo[0] & 1] * e; kg_out++; } // send grad
-        else { MEM(0, m * dout[(hi[0] - 1) & 1] * e, 0); kg_in++; }           // recv grad
+      double my_id[V], up_id[V], dn_id[V], up_c[V], dn_c[V];
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        const int st = s[q];
+        my_id[q] = which[q] == 1 ? (double)((st - 1) << 14 | ka_in[q])
+                 : which[q] == 2 ? (double)(st << 14 | ka_out[q])
+                 : which[q] == 3 ? (double)((st - 1) << 14 | 1 << 13 | kg_out[q])
+                 : which[q] == 4 ? (double)(st << 14 | 1 << 13 | kg_in[q]) : -1.0;
+      }
+      Nbr<V>::up_stage(my_id, up_id, lane);
+      Nbr<V>::down_stage(my_id, dn_id, lane);
+      Nbr<V>::up_stage(clk, up_c, lane);
+      Nbr<V>::down_stage(clk, dn_c, lane);
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        const int st = s[q];
+        const bool down_link = which[q] == 1 || which[q] == 3;      // partner s - 1
+        const bool ready = which[q] > 0 && (down_link ? (st > 0 && dn_id[q] == my_id[q])
+                                                      : (st < Pi - 1 && up_id[q] == my_id[q]));
+        if (ready) {
+          const double other = down_link ? dn_c[q] : up_c[q];
+          clk[q] = dadd(fmax(clk[q], other), down_link ? sendb[q] : sendf[q]);
+          if (which[q] == 1) { MEM(q, m * kin[lo[q] & 1] * e, 0); ka_in[q]++; }        // recv act
+          else if (which[q] == 2) { ka_out[q]++; }                                    // send act
+          else if (which[q] == 3) { live[q] -= m * kin[lo[q] & 1] * e; kg_out[q]++; } // send grad
+          else { MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0); kg_in[q]++; }              // recv grad
+        }
       }
     }
   } else if constexpr (SEQ) {

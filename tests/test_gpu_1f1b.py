@@ -34,8 +34,9 @@ def test_w2_1f1b(sim):
 
 
 def test_w4_1f1b(sim):
-    """Deep pipelines: 64-layer MLP, P up to 32, K up to 128."""
-    g = W.grid_with("W4", models=["mlp_w4_1f1b"], world=[1, 2, 4, 8, 16, 32])
+    """Deep pipelines: 64-layer MLP, P up to 64 (two stages per lane beyond
+    32), K up to 128."""
+    g = W.grid_with("W4", models=["mlp_w4_1f1b"])
     assert full_grid_check(sim, g) == 1.0
 
 
@@ -80,12 +81,18 @@ def test_explicit_1f1b_all_shapes(sim):
     s.close()
 
 
-def test_1f1b_beyond_32_stages_rejected(sim):
-    from paper_2111_05426_b200 import DistirError
+def test_1f1b_beyond_32_stages(sim):
+    """32 < P <= 64 runs two stages per lane (k_simulate mode 7): explicit
+    configurations (non-power-of-two P too) against the oracle."""
     mi = list(W.MODELS).index("mlp_w4_1f1b")
-    with pytest.raises(DistirError, match="1F1B"):
-        sim.eval(configs=[(mi, 0, 1, 1, 64, 64, 64)], k=1)
-    with pytest.raises(DistirError, match="1F1B"):
-        sim.eval(W.grid_with("W4", models=["mlp_w4_1f1b"]), k=1)
-    # GPipe on the same shape stays supported
-    sim.eval(configs=[(list(W.MODELS).index("mlp_w4"), 0, 1, 1, 64, 64, 64)], k=1)
+    cfgs = [(mi, 0, 1, 1, P, K, 64 * K) for P in (33, 40, 47, 64) for K in (1, 2, 5, 16)]
+    res = sim.eval(configs=cfgs, k=4)
+    ref = {"makespan": [], "peak": [], "reason": []}
+    for (m_, ti, D, T, P, K, B) in cfgs:
+        r = oracle.eval_config(W.MODELS["mlp_w4_1f1b"], W.TOPOLOGIES[list(W.TOPOLOGIES)[ti]],
+                               D, T, P, K, B)
+        for k in ref:
+            ref[k].append(r[k])
+    ref = {k: np.array(v) for k, v in ref.items()}
+    ref["reason"] = ref["reason"].astype(np.uint32)
+    assert assert_parity(res, ref, "1f1b P > 32") == 1.0
