@@ -41,7 +41,9 @@
  *     create.  The caller owns every output buffer and the device workspace
  *     (e.g. a torch uint8 tensor of distir_workspace_size() bytes).
  *   * Limits (DISTIR_E_UNSUPPORTED beyond them): world size <= 64, n_layer
- *     <= 1024, microbatches <= 4096, node_size a power of two, k <= 64.
+ *     <= 1024, microbatches <= 4096, node_size a power of two, k <= 64,
+ *     dp and tp powers of two in explicit configs (stage symmetry); ZeRO
+ *     models: GPipe only and next_pow2(pp) * dp <= 32 (distir_model).
  */
 #ifndef DISTIR_H_
 #define DISTIR_H_
