@@ -77,6 +77,7 @@ def main():
              ("PM_1B", W.GRIDS["PM_1B"]), ("PM_17B", W.GRIDS["PM_17B"]),
              ("PM_103B", W.GRIDS["PM_103B"]), ("PG", W.GRIDS["PG"]),
              ("W2-1F1B", W.grid_with("W2", models=["mlp_1b_1f1b"])),
+             ("W4-1F1B", W.grid_with("W4", models=["mlp_w4_1f1b"])),
              ("W2-ckpt", W.grid_with("W2", models=["mlp_1b_ckpt"])),
              ("W2-ZeRO", W.grid_with("W2", models=["mlp_1b_zero"])),
              ("W2-TB200R", W.grid_with("W2", topos=["TB200R"])),
