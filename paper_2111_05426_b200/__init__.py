@@ -14,29 +14,29 @@ from __future__ import annotations
 
 import ctypes
 import os
-import subprocess
 
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
 SO_PATH = os.path.join(_HERE, "libdistir.so")
-SOURCES = [os.path.join(_HERE, "csrc", f)
-           for f in ("distir.cu", "kernels.cuh", "common.cuh")] + [
-    os.path.join(ROOT, "include", "distir.h")]
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
-              "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+
+def _build_lib():
+    """csrc/build_lib.py, loaded by path (importing this package needs the
+    library it builds)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "distir_build_lib", os.path.join(_HERE, "csrc", "build_lib.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libdistir.so for sm_100a in-tree (nvcc cross-compiles here)."""
-    newest = max(os.path.getmtime(s) for s in SOURCES)
-    if force or not os.path.exists(SO_PATH) or os.path.getmtime(SO_PATH) < newest:
-        cmd = ["nvcc"] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + [
-            "-o", SO_PATH, os.path.join(_HERE, "csrc", "distir.cu"), "-ldl"]
-        subprocess.check_call(cmd)
-    return SO_PATH
+    """Compile libdistir.so for sm_100a in-tree (nvcc cross-compiles here);
+    without `force`, only when a csrc/ source or include/distir.h is newer."""
+    return _build_lib().build(out=SO_PATH, verbose=verbose, force=force)
 
 
 # ------------------------------------------------------------ C structs -----

@@ -19,8 +19,10 @@
 #include <vector>
 
 #include "../../include/distir.h"
+#define DISTIR_HOST_TU 1   // k_simulate lives in sim_inst.cu (one TU per instantiation)
 #include "kernels.cuh"
 #include "raw.cuh"
+#include "sim_launch.cuh"
 
 using namespace distir;
 
@@ -469,8 +471,9 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   }
   CUDA_TRY(mark(1));
   if (n > 0) {
+    const SimArgs sa{dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv};
 #define DISTIR_SIM(KD, MD) \
-  k_simulate<KD, MD><<<sim->sim_grid[KD * kModes + MD], sim_tpb(KD, MD), sim_smem(KD, MD), st>>>(dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv)
+  CUDA_TRY(sim_launch_##KD##_##MD(sim->sim_grid[KD * kModes + MD], sim_tpb(KD, MD), sim_smem(KD, MD), st, sa))
 #if DISTIR_SEQ_MAXP >= 1
     DISTIR_SIM(0, 0); DISTIR_SIM(1, 0);
     kernels += 2;
@@ -745,11 +748,9 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sim->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   int per_sm[kGroups] = {};
   const void* fns[kGroups] = {
-      (const void*)k_simulate<0, 0>, (const void*)k_simulate<0, 1>, (const void*)k_simulate<0, 2>,
-      (const void*)k_simulate<0, 3>, (const void*)k_simulate<0, 4>, (const void*)k_simulate<0, 5>,
-      (const void*)k_simulate<0, 6>, (const void*)k_simulate<0, 7>,
-      (const void*)k_simulate<1, 0>, (const void*)k_simulate<1, 1>, (const void*)k_simulate<1, 2>,
-      (const void*)k_simulate<1, 3>, (const void*)k_simulate<1, 4>, nullptr, nullptr, nullptr};
+      sim_fn_0_0(), sim_fn_0_1(), sim_fn_0_2(), sim_fn_0_3(), sim_fn_0_4(), sim_fn_0_5(),
+      sim_fn_0_6(), sim_fn_0_7(), sim_fn_1_0(), sim_fn_1_1(), sim_fn_1_2(), sim_fn_1_3(),
+      sim_fn_1_4(), nullptr, nullptr, nullptr};
   for (int g = 0; g < kGroups && e == cudaSuccess; g++) {
     if (!fns[g]) continue;
     const int smem = sim_smem(g / kModes, g % kModes);
@@ -995,13 +996,17 @@ distir_status distir_nccl_comm_destroy(void* comm) {
 
 #ifdef DISTIR_INSTR
 // Debug: read and reset the instrumentation counters (not part of distir.h).
+// The counters live per translation unit (one per simulate kernel); maxima
+// ([8], [11]) are combined by max, the rest summed.
 int distir_debug_counters(unsigned long long* out, int n) {
-  unsigned long long h[16];
-  if (cudaMemcpyFromSymbol(h, g_distir_instr, sizeof(h)) != cudaSuccess) return -1;
-  for (int i = 0; i < n && i < 16; i++) out[i] = h[i];
-  unsigned long long z[16] = {0};
-  cudaMemcpyToSymbol(g_distir_instr, z, sizeof(z));
-  return 0;
+  for (int i = 0; i < n; i++) out[i] = 0;
+  int r = 0;
+  r |= sim_counters_0_0(out, n); r |= sim_counters_0_1(out, n); r |= sim_counters_0_2(out, n);
+  r |= sim_counters_0_3(out, n); r |= sim_counters_0_4(out, n); r |= sim_counters_0_5(out, n);
+  r |= sim_counters_0_6(out, n); r |= sim_counters_0_7(out, n); r |= sim_counters_1_0(out, n);
+  r |= sim_counters_1_1(out, n); r |= sim_counters_1_2(out, n); r |= sim_counters_1_3(out, n);
+  r |= sim_counters_1_4(out, n);
+  return r;
 }
 #endif
 

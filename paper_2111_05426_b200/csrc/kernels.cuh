@@ -29,7 +29,7 @@
 #include <climits>
 #ifdef DISTIR_INSTR
 // Debug instrumentation (tools/probe_instr.py): warp-aggregated event counts.
-__device__ unsigned long long g_distir_instr[16];
+static __device__ unsigned long long g_distir_instr[16];   // per translation unit
 __device__ __forceinline__ void distir_count(int i) {
   const unsigned m_ = __activemask();
   if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));
@@ -191,7 +191,7 @@ __device__ __forceinline__ double cost_compute(int64_t flops, const DTopo& t) {
 }
 // Compute op with `flops` FLOPs touching `bytes` of tensors (C.5; row f2:
 // the regression form of P:518-520 when the topology selects it).
-__device__ __noinline__ double cost_regression(int64_t flops, int64_t bytes, bool mm, const DTopo& t) {
+static __device__ __noinline__ double cost_regression(int64_t flops, int64_t bytes, bool mm, const DTopo& t) {
   const double c0 = mm ? t.mm_c0 : t.ew_c0, cf = mm ? t.mm_flop : t.ew_flop,
                cb = mm ? t.mm_byte : t.ew_byte;
   return __dadd_rn(__dadd_rn(c0, __dmul_rn(cf, __ll2double_rn(flops))),
@@ -275,10 +275,13 @@ struct Par {
   __device__ __forceinline__ T operator[](int p) const { return p ? b : a; }
 };
 
+#ifndef DISTIR_HOST_TU   // the simulate kernels are compiled in sim_inst.cu, one TU each
 #include "simulate.cuh"
+#endif
 #undef MEM
 
 // ------------------------------------------------------------- kernels ------
+#ifndef DISTIR_SIM_TU   // sim_inst.cu compiles only k_simulate
 
 __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* __restrict__ ex,
                             Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
@@ -514,6 +517,8 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
   }
 }
 
+#endif  // DISTIR_SIM_TU
+
 // Persistent simulate kernel for one group (model kind x stages per lane):
 // each warp pulls work items of its group, heaviest weight class first.
 __host__ __device__ constexpr int sim_v(int mode) {
@@ -537,6 +542,7 @@ __host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic sme
               (sim_tpb(kind, mode) / 32) * kTabCfgs * sim_tab(kind, mode));
 }
 
+#ifndef DISTIR_HOST_TU
 template <int KIND, int MODE>
 __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecBlock* __restrict__ spp,
                                                   const DExplicit* __restrict__ ex,
@@ -634,6 +640,9 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
   if (lane == 0 && feas) atomicAdd(&hdr->n_feasible, feas);
 }
 
+#endif  // DISTIR_HOST_TU
+
+#ifndef DISTIR_SIM_TU
 // ------------------------------------------------------------ top-k ---------
 // The C.8 total order -- throughput desc, peak asc, index asc -- as an
 // unsigned lexicographic key (larger = better): a = bits of the throughput
@@ -688,7 +697,7 @@ __device__ __forceinline__ int warp_best_lane(const Key& k) {
 // and offers the best of their heads; k rounds of a block-wide best (warp
 // winners in shared memory, then warp 0); the owner of the winner advances.
 // Pads `out` to k.
-__device__ void merge_lists(const TopkRec* __restrict__ lists, const int* __restrict__ list_n,
+static __device__ void merge_lists(const TopkRec* __restrict__ lists, const int* __restrict__ list_n,
                             int n_lists, int k_in, int k, TopkRec* __restrict__ out,
                             int* __restrict__ out_n) {
   constexpr int kLPT = 4;                                      // lists per thread
@@ -845,5 +854,6 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_merge(const TopkRec* __re
                                                             int* __restrict__ out_n) {
   merge_lists(lists, list_n, n_lists, k_in, k, out, out_n);
 }
+#endif  // DISTIR_SIM_TU
 
 }  // namespace distir

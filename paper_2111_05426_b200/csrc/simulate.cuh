@@ -64,10 +64,10 @@ __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int
 #error "DISTIR_CROSS1 uses warp votes inside the slow path: build with DISTIR_VOTE=1"
 #endif
 // Segment -> distinct-op-list maps of the task caches (BinTab).
-__device__ constexpr int kMapId3[3] = {0, 1, 2};
+static __device__ constexpr int kMapId3[3] = {0, 1, 2};
 // MLP backward: LossGrad, recompute (the forward lists), layers (desc)
-__device__ constexpr int kMapMlpBwd[7] = {3, 0, 1, 2, 4, 5, 6};
-__device__ constexpr int kMapMlpBwd4[4] = {3, 4, 5, 6};          // without checkpointing
+static __device__ constexpr int kMapMlpBwd[7] = {3, 0, 1, 2, 4, 5, 6};
+static __device__ constexpr int kMapMlpBwd4[4] = {3, 4, 5, 6};          // without checkpointing
 
 __device__ __forceinline__ MemProf mem_alt(MemProf A, MemProf B, int p0, int n) {
   if (n <= 0) return mem_id();
@@ -795,7 +795,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
 // each Reduce waits for the previous owner's Add (max(x + add, x) = x + add,
 // RN is monotone) -- up to the final Add, which only its owner performs.
 // Sends pair replica i of neighbouring stages (lanes D apart).
-__device__ constexpr int kMapZeroBwd[9] = {3, 0, 1, 2, 4, 5, 6, 7, 8};
+static __device__ constexpr int kMapZeroBwd[9] = {3, 0, 1, 2, 4, 5, 6, 7, 8};
 
 __device__ __forceinline__ double cost_chain(int64_t g, int64_t bytes, bool intra, const DTopo& t) {
   // Broadcast from / Reduce to the owner: a pipelined chain over the g
@@ -804,7 +804,7 @@ __device__ __forceinline__ double cost_chain(int64_t g, int64_t bytes, bool intr
   return __dadd_rn(__dmul_rn(__ll2double_rn(g - 1), a), __ddiv_rn(__ll2double_rn(bytes), bw));
 }
 
-__device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
+static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                              double* row, double* tab, double& ms_out, int64_t& peak_out) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
   const int64_t m = has ? c.B / (D * K) : 0;
