@@ -16,7 +16,13 @@ round-robin over the ranks, so per-GPU work stays fixed ("scaling": "weak").
   e2e         the same metric through the public API with host buffers
               (spec H2D, per-config results + top-k D2H inside the timing)
   roofline    k_simulate (the dominant kernel) against the SM issue ceiling
-  cpu_baseline the CPU oracle on a bounded sample of the same grid (rank 0, N=1)
+              (warp instructions per launch from the committed ncu capture of
+              this source tree), with the HBM-equivalent logical rate and the
+              measured DRAM bytes beside it
+  strong      fixed grids (W3 x 8 topologies, W5) dealt over the N ranks:
+              strong scaling, time = max over ranks
+  cpu_baseline the CPU oracle on a bounded sample of the same grid (rank 0,
+              N=1): all host threads and one thread, CPU model
 
 `--impl reference` times the CPU oracle (the reference arm of this tier).
 """
@@ -39,7 +45,6 @@ import workloads as W  # noqa: E402
 
 METRIC = "simulated op-events/sec (GPT-2 inference grid W3, DistIR simulator pass)"
 UNIT = "op-events/s"
-ISSUE_PEAK_NOTE = "148 SMs x 4 SMSPs x 32 lanes x 1 instr/clk x sm_max_mhz"
 
 
 def parse():
@@ -54,6 +59,11 @@ def parse():
                     help="end-to-end steps (default: min(steps, 50))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--nccl", action="store_true",
+                    help="N=1: run row a8 (NCCL all-gather of the top-k + device merge) "
+                         "through a 1-rank communicator inside the timed loop")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the fixed-grid (strong-scaling) legs")
     return ap.parse_args()
 
 
@@ -140,26 +150,44 @@ class ClockSampler:
 
 # --------------------------------------------------------- CPU baseline -----
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_oracle_rate(grid, seconds, seed=20211105426, threads=None):
-    """Time the oracle (as it stands) on seeded random configs of the grid
-    until `seconds` of wall time, on all host threads (each thread owns
-    whole configurations); op-events/s."""
+    """Time the oracle (as it stands) on a seeded random sample of the grid
+    for about `seconds` of wall time on `threads` host threads (configs are
+    handed out one at a time); op-events/s.  A first call on 2 configs per
+    thread sizes the sample; the rest is ONE call, so the threads never wait
+    for each other between chunks."""
     import oracle
     oracle.build()
     threads = threads or os.cpu_count() or 1
     n = len(oracle.enumerate_grid(grid)) if grid["synth_count"] == 0 else grid["synth_count"]
-    rng = np.random.default_rng(seed)
-    order = rng.permutation(n)
-    done, ops, cfgs, t0 = 0, 0, 0, time.perf_counter()
-    chunk = max(16, 8 * threads)
-    while time.perf_counter() - t0 < seconds and done < n:
-        idx = np.sort(order[done:done + chunk])
+    order = np.random.default_rng(seed).permutation(n)
+    ops, cfgs, dt, pos = 0, 0, 0.0, 0
+    for part in range(2):
+        if part == 0:
+            m = min(n, 2 * threads)
+        else:
+            rate = cfgs / max(dt, 1e-9)
+            m = int(min(n - pos, max(0.0, seconds - dt) * rate))
+            if m <= 0:
+                break
+        idx = np.sort(order[pos:pos + m])
+        pos += m
+        t = time.perf_counter()
         r = oracle.grid_eval(grid, indices=idx, threads=threads)
-        valid = (r["reason"] & 0x1F) == 0
-        ops += int(r["n_ops"][valid].sum())
+        dt += time.perf_counter() - t
+        ops += int(r["n_ops"][(r["reason"] & 0x1F) == 0].sum())
         cfgs += len(idx)
-        done += chunk
-    dt = time.perf_counter() - t0
     return dict(value=ops / dt, ops=ops, configs=cfgs, seconds=dt, threads=threads)
 
 
@@ -219,7 +247,118 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------- roofline -----
+
+def source_sha():
+    """sha256 over the library's sources (csrc/*.cu*, include/distir.h): the
+    key under which an ncu capture of k_simulate is valid for this build."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2111_05426_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        if f.endswith((".cu", ".cuh")):
+            with open(os.path.join(csrc, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    with open(os.path.join(ROOT, "include", "distir.h"), "rb") as fh:
+        h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_capture():
+    """The committed `ncu --set full` summary of the dominant kernel
+    (profiles/ncu_simulate_summary.json, written by tools/ncu_capture.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_simulate_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
+def roofline(prof, stats, n_sm, sm_mhz, peaks, peak_kind):
+    """k_simulate (the dominant kernel) against the bound that binds it: SM
+    instruction issue.  It is a latency-/issue-bound integer + fp64 scalar
+    kernel (no tensor cores: nothing on the path is a dense contraction; HBM
+    traffic is ~150 KB per launch).  achieved = warp instructions per launch
+    (ncu capture of this source tree) / its live CUDA-event time; peak = SMs x
+    4 schedulers x 1 warp instruction / clock.  Beside it: north_star's
+    HBM-equivalent rate (16 B per op-event, SURVEY D.3 -- a LOGICAL rate: the
+    kernel never moves those bytes, exact aggregation skips the per-op work)
+    and the DRAM bytes ncu measured."""
+    sim_ms = prof["ms_simulate"] / max(prof["launches"], 1)
+    sim_s = sim_ms / 1e3
+    cap = ncu_capture()
+    sha = source_sha()
+    fresh = cap is not None and cap.get("source_sha") == sha
+    inst = cap.get("inst_executed_per_launch") if cap else None
+    dram = cap.get("dram_bytes_per_launch") if cap else None
+    issue_peak = n_sm * 4 * sm_mhz * 1e6
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = inst / sim_s if inst else None
+    logical = 16.0 * stats["op_events"] / sim_s / 1e9
+    return {
+        "bound": "alu", "unit": "warp-instructions/s",
+        "achieved": achieved, "peak": issue_peak,
+        "frac": achieved / issue_peak if achieved else None,
+        "traffic": dram,
+        "kernel": "k_simulate (a2-a6)", "kernel_ms": sim_ms,
+        "instructions_per_launch": inst,
+        "capture": {"file": "profiles/ncu_simulate_summary.json",
+                    "source_sha": cap.get("source_sha") if cap else None,
+                    "this_source_sha": sha, "fresh": fresh,
+                    "workload": cap.get("workload") if cap else None},
+        "peak_note": "%d SMs x 4 SMSPs x 1 warp-instr/clk x %.0f MHz (SM clock under load)"
+                     % (n_sm, sm_mhz),
+        "dram": {"bytes_per_launch": dram,
+                 "GBps": dram / sim_s / 1e9 if dram else None,
+                 "frac_of_hbm": dram / sim_s / 1e9 / hbm if dram else None},
+        "hbm_equivalent": {"bytes_per_op_event": 16, "GBps": logical,
+                           "peak_GBps": hbm, "frac": logical / hbm,
+                           "peak_kind": peak_kind,
+                           "note": "logical rate (op-events x 16 B / k_simulate time); "
+                                   "not traffic -- see dram"},
+    }
+
+
 # --------------------------------------------------------------- main -------
+
+def timed(sim, outs, k, comm, steps, flush, stream, barrier):
+    """Device time per launch (ms, CUDA events on the library's stream, L2
+    flushed before each launch)."""
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    barrier()
+    for i in range(steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        sim.launch(outs, k=k, comm=comm)
+        evs[i][1].record(stream)
+    barrier()
+    return sum(a.elapsed_time(b) for a, b in evs) / steps
+
+
+def strong_leg(sim, name, grid, k, comm, rank, world, steps, warmup, flush, stream, barrier,
+               reduce_max, reduce_sum):
+    """A FIXED grid dealt round-robin over the `world` ranks (strong scaling):
+    op-events/s of the whole grid, time = max over ranks."""
+    n_total = sim.grid_size(grid)
+    n_local = sim.upload(grid, rank=rank, n_ranks=world)
+    outs = sim.device_outputs(n_local, k=k)
+    for _ in range(warmup):
+        sim.launch(outs, k=k, comm=comm)
+    barrier()
+    ops = float(sim.last_stats()["op_events"])
+    ms = reduce_max(timed(sim, outs, k, comm, steps, flush, stream, barrier))
+    ops = reduce_sum(ops)
+    return {"workload": "%s: %d configs (%s x %s)" % (
+                name, n_total, "+".join(grid["models"]) or "synthetic",
+                "+".join(grid["topos"])),
+            "value": ops / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "n_gpus": world,
+            "steps": steps, "configs_per_s": n_total / (ms / 1e3)}
+
+
+STRONG = [("W3x8", dict(W.GRIDS["W3"], topos=["TB200"] + W.TM[:7])), ("W5", W.GRIDS["W5"])]
+
 
 def main():
     args = parse()
@@ -241,10 +380,14 @@ def main():
     grid = bench_grid(args.workload, n_gpus)
     sim = Simulator(W.MODELS, W.TOPOLOGIES, device=local)
     comm = None
-    if world > 1:
-        obj = [distir_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        comm = distir_nccl_comm_init(obj[0], world, rank, local)
+    if world > 1 or args.nccl:
+        if world > 1:
+            obj = [distir_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        else:
+            uid = distir_nccl_unique_id()
+        comm = distir_nccl_comm_init(uid, world, rank, local)
     k = args.k
     n_total = sim.grid_size(grid)
     n_local = sim.upload(grid, rank=rank, n_ranks=world)
@@ -257,6 +400,20 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def reduce_max(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def reduce_sum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     # warm-up
     for _ in range(args.warmup):
         sim.launch(outs, k=k, comm=comm)
@@ -265,21 +422,11 @@ def main():
 
     # ---- device-timed region (inputs resident in HBM)
     K = args.steps
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(K)]
     sim.profile(True)
     with ClockSampler(local) as clk:
-        barrier()
-        for i in range(K):
-            flush.zero_()
-            evs[i][0].record(stream)
-            sim.launch(outs, k=k, comm=comm)
-            evs[i][1].record(stream)
-        barrier()
+        ms_step = timed(sim, outs, k, comm, K, flush, stream, barrier)
     prof = sim.profile(False)
     clocks = clk.summary()
-    t_ms = sum(a.elapsed_time(b) for a, b in evs)
-    ms_step = t_ms / K
     tk_dev = outs["topk"].cpu()
     ntk = int(outs["ntopk"].item())
 
@@ -296,60 +443,60 @@ def main():
     barrier()
     e2e_ms = 1e3 * (time.perf_counter() - t0) / E
     est = res["stats"]
-
-    # ---- reduce over ranks
-    vals = torch.tensor([ms_step, e2e_ms, float(stats["op_events"]),
-                         float(stats["stage_steps"]), float(est["h2d_bytes"]),
-                         float(est["d2h_bytes"])], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = vals[:2].clone()
-        sm = vals[2:].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        vals = torch.cat([mx, sm])
-    ms_step, e2e_ms, ops_all, steps_all, h2d_all, d2h_all = vals.tolist()
     assert res["topk"]["index"].tolist() == \
         tk_dev.numpy()[:ntk].view(np.int64).reshape(-1, 4)[:, 0].tolist()
 
+    # ---- fixed-grid legs (strong scaling: the same grid at every N)
+    strong = []
+    if not args.no_strong:
+        for name, g in STRONG:
+            strong.append(strong_leg(sim, name, g, k, comm, rank, world,
+                                     min(K, 50 if name == "W5" else 200), 3, flush, stream,
+                                     barrier, reduce_max, reduce_sum))
+
+    # ---- reduce over ranks
+    ms_step = reduce_max(ms_step)
+    e2e_ms = reduce_max(e2e_ms)
+    ops_all = reduce_sum(float(stats["op_events"]))
+    steps_all = reduce_sum(float(stats["stage_steps"]))
+    h2d_all = reduce_sum(float(est["h2d_bytes"]))
+    d2h_all = reduce_sum(float(est["d2h_bytes"]))
+
     if rank == 0:
         peaks, peak_kind = measured_peaks()
-        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        issue_peak = n_sm * 4 * 32 * sm_max * 1e6
-        sim_ms = prof["ms_simulate"] / max(prof["launches"], 1)
-        achieved = stats["stage_steps"] / (sim_ms / 1e3)
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_simulate_summary.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+        sm_mhz = clocks["sm_mhz"] or float(peaks.get("sm_max_mhz", 1965.0))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             c = cpu_oracle_rate(grid, args.cpu_seconds)
+            c1 = cpu_oracle_rate(grid, args.cpu_seconds / 3, seed=7, threads=1)
             cpu = {"value": c["value"], "unit": UNIT, "cores": c["threads"],
-                   "kind": "oracle",
+                   "kind": "oracle", "cpu_model": cpu_model(),
                    "sample": "seeded random %d of %d %s configs (%d op-events), %.1f s, "
-                             "%d threads" % (c["configs"], n_total, args.workload, c["ops"],
-                                             c["seconds"], c["threads"])}
+                             "%d threads (configs handed out one at a time)"
+                             % (c["configs"], n_total, args.workload, c["ops"],
+                                c["seconds"], c["threads"]),
+                   "one_thread": {"value": c1["value"], "unit": UNIT, "cores": 1,
+                                  "sample": "seeded random %d configs (%d op-events), %.1f s"
+                                            % (c1["configs"], c1["ops"], c1["seconds"])}}
         value = ops_all / (ms_step / 1e3)
+        cfg = bench_config(args.workload, grid, n_total, k, n_gpus)
+        cfg["nccl_merge"] = comm is not None
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
             "steps": K, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": bench_config(args.workload, grid, n_total, k, n_gpus),
+            "config": cfg,
             "configs_per_s": n_total / (ms_step / 1e3),
             "time_to_best_ms": e2e_ms,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": issue_peak,
-                         "unit": "stage-steps/s", "frac": achieved / issue_peak,
-                         "traffic": traffic,
-                         "kernel": "k_simulate", "kernel_ms": sim_ms,
-                         "peak_note": ISSUE_PEAK_NOTE + " (%s sm_max_mhz)" % peak_kind},
+            "roofline": roofline(prof, stats, n_sm, sm_mhz, peaks, peak_kind),
             "kernel_ms_per_step": {x: prof[x] / max(prof["launches"], 1) for x in
                                    ("ms_prepare", "ms_simulate", "ms_topk", "ms_merge")},
             "cpu_baseline": cpu,
             "e2e": {"value": ops_all / (e2e_ms / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all)},
+            "strong": strong,
             "gpu_launches": int(prof["kernels"]),
             "clocks": clocks,
             "stats": {"op_events": int(ops_all), "stage_steps": int(steps_all),

@@ -284,6 +284,27 @@ distir_status distir_grid_eval_sharded(distir_sim* sim, const distir_grid_spec* 
                                        uint32_t* reason_out, distir_topk_entry* topk_out,
                                        int32_t* n_topk_out, distir_stats* stats_out);
 
+/* Device merge of top-k lists (row a8: the step distir_grid_launch /
+ * distir_grid_eval_sharded run after the NCCL all-gather of the per-rank
+ * lists; north_star "only the final top-k merged").  Selects the first k
+ * records of the union of n_lists sorted lists by the C.8 order --
+ * throughput descending, then peak_bytes ascending, then index ascending
+ * -- on this handle's device, asynchronously on its stream.
+ *   d_lists   DEVICE, n_lists x k_in records, list l at d_lists[l * k_in],
+ *             each sorted by the C.8 order (as distir_grid_launch writes its
+ *             d_topk); records are identified by index, which must be
+ *             distinct across the lists.
+ *   d_list_n  DEVICE, n_lists counts (clamped to k_in), or NULL: then list
+ *             l's records are its leading entries with index >= 0 (the
+ *             padding distir_grid_launch writes past *d_n_topk is index -1).
+ *   d_out     DEVICE, k records: the merged list, padded with index -1;
+ *   d_n_out   DEVICE, the number of real records, min(k, sum of counts).
+ * Limits: 1 <= n_lists <= 1024, 0 <= k_in, k <= 64.  d_out must not overlap
+ * d_lists.  Errors: INVALID_ARG, CUDA. */
+distir_status distir_topk_merge(distir_sim* sim, const distir_topk_entry* d_lists,
+                                const int32_t* d_list_n, int32_t n_lists, int32_t k_in,
+                                int32_t k, distir_topk_entry* d_out, int32_t* d_n_out);
+
 /* NCCL bootstrap helpers (NCCL is loaded at run time with dlopen, so the
  * library itself has no link-time NCCL dependency).  The unique id is 128
  * opaque bytes to broadcast from rank 0 (e.g. through torch.distributed). */
@@ -312,7 +333,12 @@ int64_t distir_shard_indices(int64_t n_configs, int32_t rank, int32_t n_ranks,
  *   returned: never freed), bytes.
  * Outputs (host; any but makespan_out may be NULL): makespan per program,
  * final clock and peak live bytes per device, start and end time per op.
- * Synchronous.  Errors: INVALID_ARG for out-of-range ids/offsets. */
+ * Programs are checked on the host before any GPU work: every op input
+ * must be a parameter or an earlier op's output, every value is defined at
+ * most once, an op's outputs must live on one of its devices, and the
+ * programs' op, value and output ranges must not overlap.
+ * Synchronous.  Errors: INVALID_ARG for out-of-range ids/offsets or a
+ * program that breaks these rules. */
 typedef struct {
   int32_t n_dev, dev_off, n_in, in_off, n_out, out_off;
   double cost;

@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstring>
 #include <limits>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -1021,7 +1022,7 @@ int64_t oracle_enumerate(int32_t n_model_table, const int64_t* model_table,
 }
 
 // Evaluate the configs at the given canonical indices (or all when
-// idx == NULL), with n_threads worker threads owning static chunks.
+// idx == NULL), with n_threads worker threads taking configs one at a time.
 // Outputs are indexed like idx.  Returns the number of configs that failed a
 // self-check (0 expected).
 int64_t oracle_grid_eval(int32_t n_model_table, const int64_t* model_table,
@@ -1048,12 +1049,14 @@ int64_t oracle_grid_eval(int32_t n_model_table, const int64_t* model_table,
   if (n_threads <= 1) {
     work(0, 0, n_idx);
   } else {
+    // configurations differ in size by orders of magnitude: threads take
+    // them one at a time from a shared counter (dynamic distribution)
+    std::atomic<int64_t> next{0};
+    auto worker = [&](int tid) {
+      for (int64_t q; (q = next.fetch_add(1)) < n_idx;) work(tid, q, q + 1);
+    };
     std::vector<std::thread> th;
-    const int64_t chunk = (n_idx + n_threads - 1) / n_threads;
-    for (int t = 0; t < n_threads; t++) {
-      int64_t a = std::min<int64_t>(n_idx, t * chunk), b = std::min<int64_t>(n_idx, a + chunk);
-      th.emplace_back(work, t, a, b);
-    }
+    for (int t = 0; t < n_threads; t++) th.emplace_back(worker, t);
     for (auto& x : th) x.join();
   }
   int64_t nb = 0;

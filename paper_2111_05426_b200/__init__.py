@@ -129,7 +129,8 @@ EXPORTS = ("distir_sim_create", "distir_sim_destroy", "distir_grid_size",
            "distir_grid_eval_sharded", "distir_nccl_unique_id",
            "distir_nccl_comm_init", "distir_nccl_comm_destroy",
            "distir_shard_indices", "distir_raw_workspace_size",
-           "distir_raw_eval", "distir_last_error", "distir_version")
+           "distir_raw_eval", "distir_topk_merge", "distir_last_error",
+           "distir_version")
 
 
 class DistirError(RuntimeError):
@@ -173,6 +174,7 @@ def _load():
     L.distir_raw_eval.argtypes = [vp, P(distir_raw_program), i32, P(distir_raw_op), i64,
                                   P(i32), i64, P(distir_raw_value), i64, i64, vp,
                                   ctypes.c_size_t, vp, vp, vp, vp, vp]
+    L.distir_topk_merge.argtypes = [vp, vp, vp, i32, i32, i32, vp, vp]
     L.distir_shard_indices.restype = i64
     for f in EXPORTS:
         if f not in ("distir_sim_destroy", "distir_last_error", "distir_version",
@@ -401,6 +403,24 @@ class Simulator:
             _ptr(outs["peak"]) if per_config else None,
             _ptr(outs["reason"]) if per_config else None,
             _ptr(outs["topk"]), _ptr(outs["ntopk"])))
+
+    def merge_topk(self, lists, counts=None, k=10):
+        """Device merge of sorted top-k lists (row a8, distir_topk_merge).
+        lists: int64 CUDA tensor (n_lists, k_in, 4) of records as
+        distir_grid_launch writes them; counts: int32 CUDA tensor (n_lists,)
+        or None (records with index >= 0).  Returns (topk (k, 4) int64
+        tensor, n (1,) int32 tensor), asynchronously on the handle's stream."""
+        torch = self.torch
+        assert lists.is_cuda and lists.dtype == torch.int64 and lists.dim() == 3
+        lists = lists.contiguous()
+        out = torch.empty((max(k, 1), 4), dtype=torch.int64, device=lists.device)
+        n = torch.zeros(1, dtype=torch.int32, device=lists.device)
+        if counts is not None:
+            counts = counts.to(torch.int32).contiguous()
+        _check(lib.distir_topk_merge(self.handle, _ptr(lists),
+                                     _ptr(counts) if counts is not None else None,
+                                     lists.shape[0], lists.shape[1], k, _ptr(out), _ptr(n)))
+        return out, n
 
     # -- raw-program mode (f3)
     def eval_raw(self, programs, per_op=True):

@@ -35,13 +35,16 @@ struct PlanBudget {                 // resident warps of each simulate kernel
 };
 // Binade tables (exact_add.cuh BinTab) of the wavefront simulate kernels:
 // the first kTabCfgs configurations of a warp get one.
-constexpr int kTabCfgs = 4;
-constexpr int kTabBinadesGpt2 = 32;   // 3 task segments
+constexpr int kTabCfgs = 4;          // MLP kernels: tables for the first 4 configurations
+constexpr int kTabCfgsGpt2 = 16;     // GPT-2 kernels: every configuration of a warp (S >= 2)
+constexpr int kTabBinadesGpt2 = 16;   // 3 task segments; from the binade below the
+                                      // first task to the makespan bound
 constexpr int kTabBinadesMlp = 24;    // 3 forward + 4 backward task segments
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
 constexpr int kTopkBlocks = 1024;   // max partial top-k blocks (<= 4 lists per merge thread)
 constexpr int kTopkThreads = 256;   // threads per partial top-k block
+constexpr int kMergeMaxLists = 4 * kTopkThreads;   // distir_topk_merge: 4 lists per thread
 constexpr int kTopkIPT = 2;         // candidates per thread held in registers
 
 enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <new>
 #include <string>
@@ -35,6 +37,10 @@ static_assert(sizeof(distir_raw_program) == sizeof(RawProgram), "raw program lay
 namespace {
 
 thread_local std::string g_err;
+// bumped by every NCCL communicator create / destroy: a cached graph that
+// captured an all-gather on a communicator is replayed only while no
+// communicator changed since
+std::atomic<uint64_t> g_comm_gen{0};
 
 distir_status fail(distir_status s, const std::string& msg) {
   g_err = msg;
@@ -143,6 +149,8 @@ struct GraphCache {
   int* ntopk = nullptr;
   int k = -1;
   void* comm = nullptr;
+  uint64_t comm_gen = 0;         // g_comm_gen at capture (a freed communicator's
+                                 // address may be reused by a new one)
   int64_t n_local = -1, n_total = -1;
   int32_t mode = -1;
   uint32_t f1b = 0xFFFFFFFFu;
@@ -412,6 +420,14 @@ __global__ void k_reset(Bucket* bk, WsHeader* hdr) {
   }
 }
 
+// Merge n_lists sorted top-k lists on the device (k_topk_merge): one warp
+// covers up to 128 lists (4 per lane), a full block up to kMergeMaxLists.
+void enqueue_merge(cudaStream_t st, const TopkRec* lists, const int* list_n, int n_lists, int k_in,
+                   int k, TopkRec* out, int* out_n) {
+  const int threads = n_lists <= 4 * 32 ? 32 : kTopkThreads;
+  k_topk_merge<<<1, threads, 0, st>>>(lists, list_n, n_lists, k_in, k, out, out_n);
+}
+
 // Fold the recorded launch events into the accumulated totals.
 distir_status prof_fold(distir_sim* sim) {
   if (sim->ev_used == 0) return DISTIR_OK;
@@ -510,7 +526,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
       k_topk<<<nblk, kTopkThreads, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n, hdr, loc, loc_n);
       kernels++;
     } else {
-      k_topk_merge<<<1, 32, 0, st>>>(part, part_n, 0, k, k, loc, loc_n);
+      enqueue_merge(st, part, part_n, 0, k, k, loc, loc_n);
       kernels++;
     }
   }
@@ -524,7 +540,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     if (r != ncclSuccess)
       return fail(DISTIR_E_NCCL, std::string("ncclAllGather: ") +
                                      (api.getErrorString ? api.getErrorString(r) : "error"));
-    k_topk_merge<<<1, 32, 0, st>>>(gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
+    enqueue_merge(st, gath, nullptr, sp.n_ranks, k, k, topk, ntopk);
     kernels++;
   }
   CUDA_TRY(mark(4));
@@ -544,6 +560,7 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
   GraphCache& G = sim->graph;
   const bool key_ok = G.exec && G.ws == ws && G.ms == ms && G.pk == pk && G.rs == rs &&
                       G.topk == topk && G.ntopk == ntopk && G.k == k && G.comm == comm &&
+                      (comm == nullptr || G.comm_gen == g_comm_gen.load()) &&
                       G.n_local == sim->spec.n_local && G.n_total == sim->spec.n_total &&
                       G.mode == sim->spec.mode && G.f1b == sim->spec.f1b;
   if (sim->use_graph && !key_ok) {
@@ -581,7 +598,7 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
       G.graph = g;
       CUDA_TRY(e);
       G.ws = ws; G.ms = ms; G.pk = pk; G.rs = rs; G.topk = topk; G.ntopk = ntopk; G.k = k;
-      G.comm = comm; G.n_local = sim->spec.n_local; G.n_total = sim->spec.n_total;
+      G.comm = comm; G.comm_gen = g_comm_gen.load(); G.n_local = sim->spec.n_local; G.n_total = sim->spec.n_total;
       G.mode = sim->spec.mode; G.f1b = sim->spec.f1b; G.kernels = kern; G.ev_ring = false;
     }
   }
@@ -954,6 +971,28 @@ distir_status distir_grid_eval(distir_sim* sim, const distir_grid_spec* spec,
                                   n_topk_out, stats_out);
 }
 
+distir_status distir_topk_merge(distir_sim* sim, const distir_topk_entry* d_lists,
+                                const int32_t* d_list_n, int32_t n_lists, int32_t k_in,
+                                int32_t k, distir_topk_entry* d_out, int32_t* d_n_out) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (n_lists < 1 || n_lists > kMergeMaxLists)
+    return fail(DISTIR_E_INVALID_ARG, "n_lists in [1, 1024]");
+  if (k_in < 0 || k_in > kMaxK || k < 0 || k > kMaxK)
+    return fail(DISTIR_E_INVALID_ARG, "k_in / k in [0, 64]");
+  if (!d_lists || !d_out || !d_n_out) return fail(DISTIR_E_INVALID_ARG, "NULL device buffer");
+  const char* lo = reinterpret_cast<const char*>(d_lists);
+  const char* oo = reinterpret_cast<const char*>(d_out);
+  if (oo < lo + (size_t)n_lists * k_in * sizeof(TopkRec) && lo < oo + (size_t)k * sizeof(TopkRec))
+    return fail(DISTIR_E_INVALID_ARG, "d_out overlaps d_lists");
+  CUDA_TRY(cudaSetDevice(sim->device));
+  enqueue_merge(sim->stream, reinterpret_cast<const TopkRec*>(d_lists), d_list_n, n_lists, k_in, k,
+                reinterpret_cast<TopkRec*>(d_out), d_n_out);
+  CUDA_TRY(cudaGetLastError());
+  return DISTIR_OK;
+}
+
 distir_status distir_nccl_unique_id(uint8_t id_out[128]) {
   g_err.clear();
   if (!id_out) return fail(DISTIR_E_INVALID_ARG, "id_out is NULL");
@@ -981,6 +1020,7 @@ distir_status distir_nccl_comm_init(const uint8_t id[128], int32_t n_ranks, int3
   if (r != ncclSuccess)
     return fail(DISTIR_E_NCCL, std::string("ncclCommInitRank: ") +
                                    (api.getErrorString ? api.getErrorString(r) : "error"));
+  g_comm_gen.fetch_add(1);
   *comm_out = comm;
   return DISTIR_OK;
 }
@@ -990,6 +1030,7 @@ distir_status distir_nccl_comm_destroy(void* comm) {
   if (!comm) return DISTIR_OK;
   NcclApi& api = nccl();
   if (!api.ok) return fail(DISTIR_E_NCCL, api.why);
+  g_comm_gen.fetch_add(1);
   api.commDestroy(static_cast<ncclComm_t>(comm));
   return DISTIR_OK;
 }
@@ -1086,6 +1127,44 @@ distir_status distir_raw_eval(distir_sim* sim, const distir_raw_program* program
       for (int j = 0; j < o.n_out; j++)
         if (idx[o.out_off + j] < 0 || idx[o.out_off + j] >= pr.n_values) return bad("op output id");
     }
+    // program semantics the kernel relies on: every input
+    // is a parameter or an earlier op's output, every value is defined once,
+    // and an output lives on one of its op's devices
+    std::vector<uint8_t> defined(pr.n_values);
+    for (int32_t v = 0; v < pr.n_values; v++) defined[v] = values[pr.value_base + v].flags & 1;
+    for (int32_t i = 0; i < pr.n_ops; i++) {
+      const distir_raw_op& o = ops[pr.op_base + i];
+      for (int j = 0; j < o.n_in; j++)
+        if (!defined[idx[o.in_off + j]]) return bad("op input used before it is defined");
+      for (int j = 0; j < o.n_out; j++) {
+        const int32_t v = idx[o.out_off + j];
+        if (defined[v]) return bad("value defined twice (a parameter or an earlier output)");
+        defined[v] = 1;
+        bool on = false;
+        for (int t = 0; t < o.n_dev; t++) on |= idx[o.dev_off + t] == values[pr.value_base + v].dev;
+        if (!on) return bad("output value not on one of its op's devices");
+      }
+    }
+  }
+  // one thread per program writes its value, output and op ranges: they
+  // must not overlap across programs
+  {
+    auto disjoint = [&](auto base, auto len) {
+      std::vector<std::pair<int64_t, int64_t>> r;
+      for (int32_t p = 0; p < n_programs; p++)
+        if (len(programs[p]) > 0) r.push_back({base(programs[p]), len(programs[p])});
+      std::sort(r.begin(), r.end());
+      for (size_t i = 1; i < r.size(); i++)
+        if (r[i - 1].first + r[i - 1].second > r[i].first) return false;
+      return true;
+    };
+    if (!disjoint([](const distir_raw_program& q) { return (int64_t)q.value_base; },
+                  [](const distir_raw_program& q) { return (int64_t)q.n_values; }) ||
+        !disjoint([](const distir_raw_program& q) { return (int64_t)q.out_base; },
+                  [](const distir_raw_program& q) { return (int64_t)q.n_dev; }) ||
+        !disjoint([](const distir_raw_program& q) { return (int64_t)q.op_base; },
+                  [](const distir_raw_program& q) { return (int64_t)q.n_ops; }))
+      return fail(DISTIR_E_INVALID_ARG, "programs' op / value / output ranges overlap");
   }
   const RawLayout L = raw_layout(n_programs, n_ops, n_idx, n_values, n_out);
   if ((s = check_ws(d_workspace, ws_bytes, L.total)) != DISTIR_OK) return s;

@@ -419,6 +419,83 @@ DISTIR_HD bool task_cross1(double& x, const Seg (&sg)[NS], TaskCache& c, const B
   return true;
 }
 
+// Straight-line slow path of a three-segment task p x A + n x B + e x C
+// (p, e in {0, 1}; A, B, C the first three lists of the binade table, B the
+// repeated one -- a GPT-2 stage: prologue, blocks, epilogue), for the two
+// common cases, when the table covers x's binade E (and E + 1) and the lists
+// have no ties there (their per-pass increments do not depend on parity):
+//   (i)  a stale cache -- x moved into E between tasks (a Send) and the whole
+//        task fits E: x <- x + (p*A + n*B + e*C) ulps;
+//   (ii) one crossing inside the B passes: the fitting passes in closed form,
+//        the crossing pass op by op, the rest of the task in closed form in
+//        E + 1, which must hold it.
+// Returns false with x untouched in every other case (add_task handles it).
+// The cache follows x into its new binade, per-segment increments included
+// (segment i is table list i: the identity map).
+DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const BinTab& t) {
+  const int64_t xb = d2bits(x);
+  const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+  const int32_t b = ef - t.e0;
+  if (!(x > 0.0) || b < 0 || b >= t.nb || ef > 1992) return false;
+  const int64_t* r0 = t.tab + (int64_t)b * 6;
+  const int64_t A0 = r0[0], A0b = r0[1], B0 = r0[2], B0b = r0[3], C0 = r0[4], C0b = r0[5];
+  const int64_t p = sg[0].reps, n = sg[1].reps, e = sg[2].reps;
+  if (!(B0 == B0b && B0 < kNeverI && (!p || (A0 == A0b && A0 < kNeverI)) &&
+        (!e || (C0 == C0b && C0 < kNeverI))))
+    return false;
+  // (products saturate at 2^53: n <= 2^10 and increments < 2^53, so n * B
+  // fits int64 and saturated sums cannot overflow)
+  auto sat = [](int64_t v) { return v > kTwo53 ? kTwo53 : v; };
+  const int64_t M = (xb & kMant) | kHidden, avail = kTwo53 - 1 - M;
+  const int64_t Cp = p * A0, CpB = Cp + sat(n * B0);
+  const int64_t tot = CpB + e * C0;
+  if (tot <= avail) {                                   // (i) the task fits E
+    x = bits2d(((int64_t)ef << 52) | ((M + tot) & kMant));
+    c.R[0] = A0; c.R[1] = A0b; c.R[2] = B0; c.R[3] = B0b; c.R[4] = C0; c.R[5] = C0b;
+    c.ef = ef;
+    c.lo = ef << 20;
+    c.hi = (ef + 1) << 20;
+    c.Su0 = c.Su1 = xmul((double)tot, bits2d((int64_t)(ef - 52) << 52));
+    return true;
+  }
+  if (Cp > avail || CpB <= avail || b + 1 >= t.nb) return false;   // not (ii)
+  const int64_t* r1 = r0 + 6;
+  const int64_t A1 = r1[0], A1b = r1[1], B1 = r1[2], B1b = r1[3], C1 = r1[4], C1b = r1[5];
+  if (!(B1 == B1b && B1 < kNeverI && (!p || (A1 == A1b && A1 < kNeverI)) &&
+        (!e || (C1 == C1b && C1 < kNeverI))))
+    return false;
+  // passes of B that still fit E: fit = floor(room / B0) < n (estimate with
+  // relative error ~2^-21 and fit < 2^10, corrected exactly)
+  const int64_t room = avail - Cp;
+  int64_t fit = (int64_t)fdiv_approx((float)room, (float)B0);
+  fit = fit < 0 ? 0 : (fit > n - 1 ? n - 1 : fit);
+  if (fit * B0 > room) fit--;
+  if (fit + 1 < n && (fit + 1) * B0 <= room) fit++;
+  double y = bits2d(((int64_t)ef << 52) | ((M + Cp + fit * B0) & kMant));   // exact, in E
+  {
+    const double* a = sg[1].a;
+    double v[kSegMax];
+#pragma unroll
+    for (int j = 0; j < kSegMax; j++) v[j] = j < sg[1].n ? a[j] : 0.0;     // loads first
+#pragma unroll
+    for (int j = 0; j < kSegMax; j++)
+      if (j < sg[1].n) y = xadd(y, v[j]);
+  }
+  const int64_t yb = d2bits(y);
+  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) return false;
+  const int64_t rest = sat((n - fit - 1) * B1) + e * C1;
+  const int64_t M1 = (yb & kMant) | kHidden;
+  if (M1 + rest > kTwo53 - 1) return false;
+  x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
+  const int64_t tot1 = p * A1 + sat(n * B1) + e * C1;
+  c.R[0] = A1; c.R[1] = A1b; c.R[2] = B1; c.R[3] = B1b; c.R[4] = C1; c.R[5] = C1b;
+  c.ef = ef + 1;
+  c.lo = (ef + 1) << 20;
+  c.hi = (ef + 2) << 20;
+  c.Su0 = c.Su1 = tot1 < kTwo53 ? xmul((double)tot1, bits2d((int64_t)(ef + 1 - 52) << 52)) : kInf();
+  return true;
+}
+
 // x <- every addition of the task, in order, computed exactly: the cache is
 // moved to x's binade and the fast path retried; otherwise each segment
 // advances by whole passes while they fit (closed form, or a short parity

@@ -29,7 +29,7 @@
 #include <climits>
 #ifdef DISTIR_INSTR
 // Debug instrumentation (tools/probe_instr.py): warp-aggregated event counts.
-static __device__ unsigned long long g_distir_instr[16];   // per translation unit
+static __device__ unsigned long long g_distir_instr[32];   // per translation unit
 __device__ __forceinline__ void distir_count(int i) {
   const unsigned m_ = __activemask();
   if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));
@@ -537,9 +537,12 @@ __host__ __device__ constexpr int sim_tab(int kind, int mode) {   // doubles per
   return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3
                      : kTabBinadesMlp * 2 * (mode == 6 ? 9 : 7);
 }
+__host__ __device__ constexpr int sim_tab_cfgs(int kind) {     // configurations with a table
+  return kind == 1 ? kTabCfgsGpt2 : kTabCfgs;
+}
 __host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic smem bytes
   return 8 * (sim_tpb(kind, mode) * sim_row(kind, mode) +
-              (sim_tpb(kind, mode) / 32) * kTabCfgs * sim_tab(kind, mode));
+              (sim_tpb(kind, mode) / 32) * sim_tab_cfgs(kind) * sim_tab(kind, mode));
 }
 
 #ifndef DISTIR_HOST_TU
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
   constexpr int TAB = sim_tab(KIND, MODE);
   extern __shared__ double s_dyn[];
   double* row = s_dyn + threadIdx.x * ROW;
-  double* wtab = s_dyn + sim_tpb(KIND, MODE) * ROW + (threadIdx.x >> 5) * kTabCfgs * TAB;
+  double* wtab = s_dyn + sim_tpb(KIND, MODE) * ROW + (threadIdx.x >> 5) * sim_tab_cfgs(KIND) * TAB;
   unsigned long long feas = 0;
   while (true) {
     unsigned int id;
@@ -598,7 +601,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
       c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
     }
     const DTopo& tp = sp.topos[c.topo];
-    double* tab = (TAB > 0 && S >= 2 && seg < kTabCfgs) ? wtab + seg * TAB : nullptr;
+    double* tab = (TAB > 0 && S >= 2 && seg < sim_tab_cfgs(KIND)) ? wtab + seg * TAB : nullptr;
     double ms;
     int64_t pk;
 #ifdef DISTIR_INSTR

@@ -18,7 +18,7 @@
 // work, doubled for rounding slack), capped at nb_max binades.  `work` is
 // this lane's total work; the max runs over the configuration's S lanes.
 __device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, int nu, double cmin,
-                                               double work, int64_t P, int S) {
+                                               double work, int64_t P, int S, double slack = 2.0) {
   for (int o = S >> 1; o > 0; o >>= 1) {
     work = fmax(work, __shfl_xor_sync(0xffffffffu, work, o));
     cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
@@ -26,7 +26,7 @@ __device__ __forceinline__ BinTab bintab_range(double* tab, int nb_max, int nu, 
   BinTab t{reinterpret_cast<int64_t*>(tab), 0, 0, nu};
   if (tab != nullptr && cmin > 0.0 && cmin < kInf()) {
     const int32_t e0 = exp_field(cmin);
-    const int32_t e1 = exp_field(__dmul_rn(work, 2.0 * (double)P)) + 1;
+    const int32_t e1 = exp_field(__dmul_rn(work, slack * (double)P)) + 1;
     t.e0 = e0 < 53 ? 53 : e0;
     const int32_t nb = e1 - t.e0 + 1;
     t.nb = nb < 0 ? 0 : (nb > nb_max ? nb_max : nb);
@@ -55,6 +55,9 @@ __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int
 #endif
 #ifndef DISTIR_PLAIN_AFTER_MLP
 #define DISTIR_PLAIN_AFTER_MLP 1   // MLP kernels: walk the rest of a task op by op after N binade crossings (W5 -16%, W2 +2%, W4 +4%)
+#endif
+#ifndef DISTIR_QUICK3
+#define DISTIR_QUICK3 1     // GPT-2: straight-line stale-cache / single-crossing slow path
 #endif
 #ifndef DISTIR_CROSS1
 #define DISTIR_CROSS1 0     // straight-line single-binade-crossing slow path (task_cross1):
@@ -668,18 +671,24 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   BinTab bt{nullptr, 0, 0, 0};
   if constexpr (!SEQ) {
     // binade table of the task segments, filled by the configuration's lanes
+    // Range: every task but stage 0's first starts at a clock >= stage 0's
+    // task duration t0 (after stage 0's first task), so the table starts one
+    // binade below t0 (rounding slack); the makespan is at most the sum of
+    // all op costs <= P x the busiest stage's K tasks and Sends.  Clocks
+    // outside the table fall back to computing increments on the fly.
     double cmin = kInf(), work = 0.0;
-    for (int j = 0; j < 19; j++) cmin = min_pos(cmin, row[j]);
 #pragma unroll
     for (int q = 0; q < V; q++) {
       if (!ok[q]) continue;
-      cmin = min_pos(cmin, sendf[q]);
       double w = nb[q] * (row[2] + row[3] + row[4] + row[5] + row[6] + row[7] + row[8] + row[9] +
                           row[10] + row[11] + row[12] + row[13] + row[14] + row[15]);
-      w = w + row[0] + row[1] + row[16] + row[17] + row[18] + sendf[q];
+      if (s[q] == 0) w = w + row[0] + row[1];
+      if (s[q] == P - 1) w = w + row[16] + row[17] + row[18];
+      if (s[q] == 0) cmin = min_pos(cmin, __dmul_rn(w, 0.5));
+      w = w + sendf[q] + sendf[q];
       work = fmax(work, w * (double)K);
     }
-    bt = bintab_range(has ? tab : nullptr, kTabBinadesGpt2, 3, cmin, work, P, S);
+    bt = bintab_range(has ? tab : nullptr, kTabBinadesGpt2, 3, cmin, work, P, S, 1.0);
     Seg sg[3];
     segs(0, sg);
     bintab_fill(bt, sg, sl, S);
@@ -700,6 +709,13 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       bool s2 = slow;
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], tc[q], bt)))
         s2 = slow && !task_cross1(clk[q], sg, tc[q], bt, kMapId3);
+#if DISTIR_QUICK3
+      if (s2) {
+        DISTIR_COUNT(16);
+        s2 = !task3_quick(clk[q], sg, tc[q], bt);
+        if (!s2) DISTIR_COUNT(17);
+      }
+#endif
       if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3);
     }
     DISTIR_SLOW_T1(any)
@@ -739,6 +755,9 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   // max(their clocks) + cost; each computes it from the other's clock
   // (both neighbours' clocks are shuffled independently), bit-identically.
   const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+#ifdef DISTIR_INSTR
+  const long long t_wave = clock64();
+#endif
   bool up[V], dn[V];
   int kk[V];
   double recvc[V];
@@ -772,6 +791,9 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       clk[q] = (sd || rcv[q]) ? nc : clk[q];
     }
   }
+#ifdef DISTIR_INSTR
+  if (lane == 0) distir_clk_add(19, t_wave);
+#endif
   }  // wavefront
   double msx = 0.0;
   int64_t pkx = 0;

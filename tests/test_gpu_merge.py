@@ -1,0 +1,191 @@
+"""GPU parity of row a8, the device merge of per-GPU top-k lists
+(distir_topk_merge, the step distir_grid_launch runs after the NCCL
+all-gather): virtual shards of a grid evaluated on one GPU, their local top-k
+lists merged ON THE DEVICE, against the oracle's full-grid top-k (P:544,
+P:637: the top 10 of the filtered grid; C.8 order throughput desc, peak asc,
+index asc) -- including forced ties on throughput and on (throughput, peak).
+Also the 1-rank NCCL path in the timed loop shape bench.py uses."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sim():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2111_05426_b200 import Simulator
+    s = Simulator(W.MODELS, W.TOPOLOGIES, device=0)
+    yield s
+    s.close()
+
+
+def shard_lists(s, G, k, grid=None, configs=None):
+    """Evaluate shards 0..G-1 of the grid (or explicit list) one after another
+    on one GPU; returns the (G, k, 4) device tensor of their padded local
+    top-k lists and the (G,) device tensor of their counts."""
+    import torch
+    lists = torch.full((G, max(k, 1), 4), -7, dtype=torch.int64, device="cuda")
+    counts = torch.zeros(G, dtype=torch.int32, device="cuda")
+    for g in range(G):
+        n = s.upload(grid=grid, configs=configs, rank=g, n_ranks=G)
+        outs = s.device_outputs(n, k=k)
+        s.launch(outs, k=k)
+        lists[g].copy_(outs["topk"])
+        counts[g:g + 1].copy_(outs["ntopk"])
+    torch.cuda.synchronize()
+    return lists, counts
+
+
+def merged(s, lists, counts, k):
+    import torch
+    from paper_2111_05426_b200 import topk_from_device
+    out, n = s.merge_topk(lists, counts, k=k)
+    torch.cuda.synchronize()
+    nn = int(n.item())
+    rec = topk_from_device(out, nn)
+    pad = out.cpu().numpy()[nn:]
+    assert (pad[:, 0] == -1).all(), "merged list padded with index -1"
+    return rec
+
+
+def oracle_topk_grid(grid, k):
+    ref = oracle.grid_result(grid, k=k, threads=8)
+    i = ref["topk_index"]
+    return dict(index=i, throughput=ref["topk_throughput"], makespan=ref["makespan"][i],
+                peak=ref["peak"][i])
+
+
+def assert_same(rec, ref):
+    assert rec["index"].tolist() == ref["index"].tolist()
+    assert (rec["throughput"] == ref["throughput"]).all()
+    assert (rec["makespan_s"] == ref["makespan"]).all()
+    assert (rec["peak_bytes"] == ref["peak"]).all()
+
+
+@pytest.mark.parametrize("name", ["W1", "W3"])
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_device_merge_of_virtual_shards_equals_oracle_topk(sim, name, G):
+    grid = W.GRIDS[name]
+    for k in (1, 10, 64):
+        ref = oracle_topk_grid(grid, k)
+        lists, counts = shard_lists(sim, G, k, grid=grid)
+        assert_same(merged(sim, lists, counts, k), ref)          # explicit counts
+        assert_same(merged(sim, lists, None, k), ref)            # index >= 0 (padding)
+
+
+def tie_case():
+    """An explicit list whose top-k is decided by the tie-breaks: the same
+    configuration repeated (equal throughput and peak: index decides) and two
+    models that differ only in dtype_bytes at D = T = P = 1 (no
+    communication, so equal makespans; the 4-byte copies have the larger
+    peak: peak decides)."""
+    models = {"a": W.mlp(4, 256, dtype_bytes=2), "b": W.mlp(4, 256, dtype_bytes=4),
+              "c": W.mlp(8, 512)}
+    topos = {"TB200": W.TOPOLOGIES["TB200"]}
+    cfgs = []
+    for B in (64, 128):
+        for m in (1, 0, 1, 0):                     # b before a in the list
+            cfgs.append((m, 0, 1, 1, 1, 1, B))
+        cfgs += [(2, 0, 2, 1, 2, 2, B)] * 3
+        cfgs += [(0, 0, 1, 1, 1, 1, B)] * 5       # duplicates of an a-config
+    return models, topos, cfgs
+
+
+def oracle_topk_configs(models, topos, cfgs, k):
+    ms, pk, rs, bt = [], [], [], []
+    for (mi, ti, D, T, P, K, B) in cfgs:
+        r = oracle.eval_config(models[list(models)[mi]], topos[list(topos)[ti]], D, T, P, K, B)
+        ms.append(r["makespan"]); pk.append(r["peak"]); rs.append(r["reason"]); bt.append(B)
+    ms, pk, rs = np.array(ms), np.array(pk, np.int64), np.array(rs, np.uint32)
+    pos, tp = oracle.topk(np.arange(len(cfgs)), np.array(bt, np.int64), ms, pk, rs, k)
+    return dict(index=pos, throughput=tp, makespan=ms[pos], peak=pk[pos])
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+def test_device_merge_tie_breaks(G):
+    from paper_2111_05426_b200 import Simulator
+    models, topos, cfgs = tie_case()
+    s = Simulator(models, topos, device=0)
+    try:
+        k = len(cfgs)
+        ref = oracle_topk_configs(models, topos, cfgs, k)
+        # the case really has ties of both kinds among the ranked records
+        tp = ref["throughput"]
+        eq = np.nonzero(tp[1:] == tp[:-1])[0]
+        assert len(eq) > 0
+        assert any(ref["peak"][i] != ref["peak"][i + 1] for i in eq), "peak tie-break exercised"
+        assert any(ref["peak"][i] == ref["peak"][i + 1] for i in eq), "index tie-break exercised"
+        lists, counts = shard_lists(s, G, min(k, 64), configs=cfgs)
+        assert_same(merged(s, lists, counts, min(k, 64)), ref)
+        # the single-launch top-k (k_topk) agrees as well
+        res = s.eval(configs=cfgs, k=min(k, 64))
+        assert res["topk"]["index"].tolist() == ref["index"].tolist()
+    finally:
+        s.close()
+
+
+def test_device_merge_edges(sim):
+    import torch
+    from paper_2111_05426_b200 import DistirError
+    # all lists empty: n = 0, everything padded
+    empty = torch.full((5, 10, 4), -1, dtype=torch.int64, device="cuda")
+    out, n = sim.merge_topk(empty, None, k=10)
+    torch.cuda.synchronize()
+    assert int(n.item()) == 0 and (out[:, 0] == -1).all()
+    # one list: a copy truncated to k
+    lists, counts = shard_lists(sim, 1, 10, grid=W.GRIDS["W1"])
+    rec = merged(sim, lists, counts, 4)
+    assert rec["index"].tolist() == oracle_topk_grid(W.GRIDS["W1"], 4)["index"].tolist()
+    # k = 0
+    out, n = sim.merge_topk(lists, counts, k=0)
+    torch.cuda.synchronize()
+    assert int(n.item()) == 0
+    # many lists (block-wide merge path): 300 lists of which few are non-empty
+    big = torch.full((300, 10, 4), -1, dtype=torch.int64, device="cuda")
+    big[7] = lists[0]
+    big[299] = lists[0]
+    big[299, :, 0] += 1000                       # distinct indices
+    out, n = sim.merge_topk(big, None, k=10)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()[:int(n.item())]
+    assert int(n.item()) == 10
+    ref = np.concatenate([lists[0].cpu().numpy(), big[299].cpu().numpy()])
+    ref = ref[ref[:, 0] >= 0]
+    tpv = ref[:, 2].view(np.float64)
+    order = sorted(range(len(ref)), key=lambda i: (-tpv[i], ref[i, 3], ref[i, 0]))[:10]
+    assert got[:, 0].tolist() == ref[order, 0].tolist()
+    # invalid arguments
+    with pytest.raises(DistirError):
+        sim.merge_topk(lists, counts, k=65)
+    with pytest.raises(DistirError):
+        sim.merge_topk(torch.empty((0, 10, 4), dtype=torch.int64, device="cuda"), None, k=10)
+
+
+def test_nccl_one_rank_in_timed_loop(sim):
+    """The device-resident launch with a 1-rank NCCL communicator, replayed
+    as bench.py's timed loop does (graph capture of the all-gather + merge),
+    gives the oracle's top-k every step; a new communicator after destroying
+    the old one is not served a stale graph."""
+    import torch
+    import paper_2111_05426_b200 as pkg
+    from paper_2111_05426_b200 import topk_from_device
+    grid = W.GRIDS["W3"]
+    ref = oracle_topk_grid(grid, 10)
+    for _ in range(2):
+        comm = pkg.distir_nccl_comm_init(pkg.distir_nccl_unique_id(), 1, 0, 0)
+        try:
+            n = sim.upload(grid)
+            outs = sim.device_outputs(n, k=10)
+            for _ in range(5):
+                outs["ntopk"].zero_()
+                sim.launch(outs, k=10, comm=comm)
+                torch.cuda.synchronize()
+                rec = topk_from_device(outs["topk"], int(outs["ntopk"].item()))
+                assert_same(rec, ref)
+        finally:
+            pkg.distir_nccl_comm_destroy(comm)

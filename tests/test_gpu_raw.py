@@ -67,3 +67,37 @@ def test_invalid_program_rejected(sim):
     from paper_2111_05426_b200 import DistirError
     with pytest.raises(DistirError):
         sim.eval_raw([(2, [([0, 5], 1.0)], [])])       # device 5 of 2
+
+
+def test_program_rules_rejected(sim):
+    """distir_raw_eval checks the program rules the kernel relies on (P:301-306,
+    P:506): inputs defined before use, each value defined once, outputs on one
+    of the op's devices, non-overlapping per-program ranges."""
+    import ctypes
+    import paper_2111_05426_b200 as pkg
+    from paper_2111_05426_b200 import DistirError
+    p = (1, 16, True, False)                     # a parameter on device 1
+    # input used before it is defined (value 1 is produced by the second op)
+    with pytest.raises(DistirError, match="before"):
+        sim.eval_raw([(2, [([0], 1.0, [1], []), ([0], 1.0, [], [1])], [p, (0, 8, False, False)])])
+    # defined twice
+    with pytest.raises(DistirError, match="twice"):
+        sim.eval_raw([(2, [([1], 1.0, [], [0])], [p])])
+    # output off the op's devices
+    with pytest.raises(DistirError, match="devices"):
+        sim.eval_raw([(2, [([0], 1.0, [0], [1])], [p, (1, 8, False, False)])])
+    # the accepted form of the same program
+    r = sim.eval_raw([(2, [([0, 1], 1.0, [0], [1])], [p, (0, 8, False, True)])])[0]
+    assert r["makespan"] == 1.0 and r["peak"].tolist() == [8, 16]
+    # two programs sharing a value range
+    progs = (pkg.distir_raw_program * 2)(pkg.distir_raw_program(1, 0, 0, 1, 0, 0),
+                                         pkg.distir_raw_program(1, 0, 0, 1, 0, 1))
+    vals = (pkg.distir_raw_value * 1)(pkg.distir_raw_value(0, 1, 8))
+    ms = (ctypes.c_double * 2)()
+    b = ctypes.c_size_t()
+    pkg.lib.distir_raw_workspace_size(2, 0, 0, 1, 2, ctypes.byref(b))
+    ws = sim.torch.empty(b.value, dtype=sim.torch.uint8, device=sim.device)
+    st = pkg.lib.distir_raw_eval(sim.handle, progs, 2, None, 0, None, 0, vals, 1, 2,
+                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), ms, None, None,
+                                 None, None)
+    assert st == 1 and b"overlap" in pkg.lib.distir_last_error()

@@ -12,12 +12,13 @@ import paper_2111_05426_b200 as pkg
 from paper_2111_05426_b200 import Simulator
 
 NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles",
-         "slow_cycles", "slow_entries", "max_item_tag", "refresh_cyc", "cross_cyc", "-", "addtask_cyc"]
+         "slow_cycles", "slow_entries", "max_item_tag", "refresh_cyc", "cross_cyc", "-", "addtask_cyc",
+         "quick_try", "quick_ok", "-", "wave_cycles"] + ["-"] * 12
 
 
 def counters():
-    buf = (ctypes.c_ulonglong * 16)()
-    pkg.lib.distir_debug_counters(buf, 16)
+    buf = (ctypes.c_ulonglong * 32)()
+    pkg.lib.distir_debug_counters(buf, 32)
     return list(buf)
 
 
@@ -57,6 +58,8 @@ def main():
         print("   lane-cycles in add_task %d: refresh %d, crossing passes %d (per add_task call: %.0f / %.0f / %.0f)" % (
             d["addtask_cyc"], d["refresh_cyc"], d["cross_cyc"], d["addtask_cyc"] / max(d["tasks"], 1),
             d["refresh_cyc"] / max(d["tasks"], 1), d["cross_cyc"] / max(d["tasks"], 1)))
+        print("   quick path: %d tries, %d ok; wavefront cycles (lane 0, summed over items) %d = %.0f%% of item cycles" % (
+            d["quick_try"], d["quick_ok"], d["wave_cycles"], 100.0 * d["wave_cycles"] / max(d["item_cycles"], 1)))
         tag = d["max_item_tag"]
         key = (tag >> 5) & 0x7FFFF
         print("   slowest item: %d cycles, kind %d P %d L %d, %d configs" % (
