@@ -501,7 +501,12 @@ def main():
             "clocks": clocks,
             "stats": {"op_events": int(ops_all), "stage_steps": int(steps_all),
                       "n_valid": stats["n_valid"], "n_feasible": stats["n_feasible"],
-                      "n_buckets": stats["n_buckets"], "n_items": stats["n_items"]},
+                      "n_buckets": stats["n_buckets"], "n_items": stats["n_items"],
+                      "tasks": stats["tasks"], "slow_tasks": stats["slow_tasks"],
+                      "wave_steps": stats["wave_steps"],
+                      "note": "op_events: logical program ops; tasks / slow_tasks / "
+                              "wave_steps: work k_simulate performed (a fast-path task "
+                              "is one add + one binade test)"},
             "top1": {"index": int(res["topk"]["index"][0]),
                      "throughput": float(res["topk"]["throughput"][0])} if len(res["topk"]) else None,
         }

@@ -185,6 +185,12 @@ typedef struct {
   int64_t n_items;        /* warp work items                                 */
   int64_t h2d_bytes;      /* host->device bytes the last eval/upload copied   */
   int64_t d2h_bytes;      /* device->host bytes the last eval copied          */
+  /* work the simulate kernels actually performed (physical companions of  */
+  /* op_events, which count the logical program):                          */
+  int64_t tasks;          /* (microbatch, stage) tasks of the valid configs   */
+  int64_t slow_tasks;     /* tasks that left the one-add fast path (a binade  */
+                          /* crossing or a stale increment cache)            */
+  int64_t wave_steps;     /* warp-level wavefront / co-simulation steps       */
 } distir_stats;
 
 typedef struct distir_sim distir_sim;

@@ -96,7 +96,8 @@ class distir_profile_data(ctypes.Structure):
 class distir_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "n_configs", "n_valid", "n_feasible", "op_events", "stage_steps",
-        "n_buckets", "n_items", "h2d_bytes", "d2h_bytes")]
+        "n_buckets", "n_items", "h2d_bytes", "d2h_bytes", "tasks", "slow_tasks",
+        "wave_steps")]
 
 
 class distir_raw_op(ctypes.Structure):

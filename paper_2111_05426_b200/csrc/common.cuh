@@ -103,6 +103,9 @@ struct WsHeader {
   unsigned long long stage_steps;
   unsigned long long n_valid;
   unsigned long long n_feasible;
+  unsigned long long tasks;           // (microbatch, stage) tasks of the valid configs
+  unsigned long long slow_tasks;      // lane-level slow-path entries (k_simulate)
+  unsigned long long wave_steps;      // warp-level wavefront steps (k_simulate)
   unsigned int cfg_total;
   unsigned int topk_ticket;           // partial top-k blocks done (last one merges)
 };

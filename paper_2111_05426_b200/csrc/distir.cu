@@ -715,6 +715,9 @@ distir_status fetch_stats(distir_sim* sim, void* ws, distir_stats* out) {
   out->n_items = h.n_items;
   out->h2d_bytes = sim->h2d;
   out->d2h_bytes = sim->d2h + (int64_t)sizeof(WsHeader);
+  out->tasks = (int64_t)h.tasks;
+  out->slow_tasks = (int64_t)h.slow_tasks;
+  out->wave_steps = (int64_t)h.wave_steps;
   return DISTIR_OK;
 }
 
@@ -954,6 +957,9 @@ distir_status distir_grid_eval_sharded(distir_sim* sim, const distir_grid_spec* 
       stats_out->n_items = h.n_items;
       stats_out->h2d_bytes = sim->h2d;
       stats_out->d2h_bytes = sim->d2h + (int64_t)sizeof(WsHeader);
+      stats_out->tasks = (int64_t)h.tasks;
+      stats_out->slow_tasks = (int64_t)h.slow_tasks;
+      stats_out->wave_steps = (int64_t)h.wave_steps;
     } else if ((s = fetch_stats(sim, d_workspace, stats_out)) != DISTIR_OK) {
       return s;
     }

@@ -458,32 +458,47 @@ DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bi
     c.Su0 = c.Su1 = xmul((double)tot, bits2d((int64_t)(ef - 52) << 52));
     return true;
   }
-  if (Cp > avail || CpB <= avail || b + 1 >= t.nb) return false;   // not (ii)
+  if (b + 1 >= t.nb) return false;
   const int64_t* r1 = r0 + 6;
   const int64_t A1 = r1[0], A1b = r1[1], B1 = r1[2], B1b = r1[3], C1 = r1[4], C1b = r1[5];
   if (!(B1 == B1b && B1 < kNeverI && (!p || (A1 == A1b && A1 < kNeverI)) &&
         (!e || (C1 == C1b && C1 < kNeverI))))
     return false;
-  // passes of B that still fit E: fit = floor(room / B0) < n (estimate with
-  // relative error ~2^-21 and fit < 2^10, corrected exactly)
-  const int64_t room = avail - Cp;
-  int64_t fit = (int64_t)fdiv_approx((float)room, (float)B0);
-  fit = fit < 0 ? 0 : (fit > n - 1 ? n - 1 : fit);
-  if (fit * B0 > room) fit--;
-  if (fit + 1 < n && (fit + 1) * B0 <= room) fit++;
-  double y = bits2d(((int64_t)ef << 52) | ((M + Cp + fit * B0) & kMant));   // exact, in E
+  // (ii) the segment that leaves E: A (whole task from x), B (the passes that
+  // still fit, then one), or C (after A and every B pass); that pass is walked
+  // op by op from the exact value where it starts, the rest of the task is
+  // added in E + 1
+  int64_t pre, rest;
+  const double* a;
+  int na;
+  if (Cp > avail) {                                           // crossing in A
+    pre = 0; a = sg[0].a; na = sg[0].n;
+    rest = sat(n * B1) + e * C1;
+  } else if (CpB > avail) {                                   // crossing in B
+    // fit = floor(room / B0) < n: estimate (relative error ~2^-21, fit <
+    // 2^10), corrected exactly
+    const int64_t room = avail - Cp;
+    int64_t fit = (int64_t)fdiv_approx((float)room, (float)B0);
+    fit = fit < 0 ? 0 : (fit > n - 1 ? n - 1 : fit);
+    if (fit * B0 > room) fit--;
+    if (fit + 1 < n && (fit + 1) * B0 <= room) fit++;
+    pre = Cp + fit * B0; a = sg[1].a; na = sg[1].n;
+    rest = sat((n - fit - 1) * B1) + e * C1;
+  } else {                                                    // crossing in C
+    pre = CpB; a = sg[2].a; na = sg[2].n;
+    rest = 0;
+  }
+  double y = bits2d(((int64_t)ef << 52) | ((M + pre) & kMant));   // exact, in E
   {
-    const double* a = sg[1].a;
     double v[kSegMax];
 #pragma unroll
-    for (int j = 0; j < kSegMax; j++) v[j] = j < sg[1].n ? a[j] : 0.0;     // loads first
+    for (int j = 0; j < kSegMax; j++) v[j] = j < na ? a[j] : 0.0;   // loads first
 #pragma unroll
     for (int j = 0; j < kSegMax; j++)
-      if (j < sg[1].n) y = xadd(y, v[j]);
+      if (j < na) y = xadd(y, v[j]);
   }
   const int64_t yb = d2bits(y);
   if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) return false;
-  const int64_t rest = sat((n - fit - 1) * B1) + e * C1;
   const int64_t M1 = (yb & kMant) | kHidden;
   if (M1 + rest > kTwo53 - 1) return false;
   x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
@@ -494,6 +509,22 @@ DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bi
   c.hi = (ef + 2) << 20;
   c.Su0 = c.Su1 = tot1 < kTwo53 ? xmul((double)tot1, bits2d((int64_t)(ef + 1 - 52) << 52)) : kInf();
   return true;
+}
+
+// A three-segment task (as task3_quick) walked op by op -- for a clock at
+// zero (stage 0's first task), where the sum climbs through many binades:
+// the repeated segment's costs are held in registers.
+DISTIR_HD void task3_plain(double& x, const Seg (&sg)[3]) {
+  for (int64_t r = 0; r < sg[0].reps; r++) seq_plain(x, sg[0].a, sg[0].n);
+  double v[kSegMax];
+#pragma unroll
+  for (int j = 0; j < kSegMax; j++) v[j] = j < sg[1].n ? sg[1].a[j] : 0.0;
+  for (int64_t r = 0; r < sg[1].reps; r++) {
+#pragma unroll
+    for (int j = 0; j < kSegMax; j++)
+      if (j < sg[1].n) x = xadd(x, v[j]);
+  }
+  for (int64_t r = 0; r < sg[2].reps; r++) seq_plain(x, sg[2].a, sg[2].n);
 }
 
 // x <- every addition of the task, in order, computed exactly: the cache is

@@ -275,6 +275,13 @@ struct Par {
   __device__ __forceinline__ T operator[](int p) const { return p ? b : a; }
 };
 
+// Work the simulate kernels actually performed (physical companions of the
+// logical op-event count): lane-level task slow-path entries (a binade
+// crossing or a stale cache) and warp-level wavefront / co-simulation steps.
+struct WorkCount {
+  unsigned int slow, steps;
+};
+
 #ifndef DISTIR_HOST_TU   // the simulate kernels are compiled in sim_inst.cu, one TU each
 #include "simulate.cuh"
 #endif
@@ -290,7 +297,7 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
                             WsHeader* __restrict__ hdr) {
   const SpecBlock& sp = *spp;
   const int64_t nloc = sp.n_local;
-  unsigned long long ev = 0, st = 0, nv = 0;
+  unsigned long long ev = 0, st = 0, nv = 0, tk = 0;
   // the decode table, staged in shared memory (a binary search per config)
   __shared__ DEntry s_ent[kMaxEntries];
   for (int j = threadIdx.x; j < sp.n_entries; j += blockDim.x) s_ent[j] = sp.entries[j];
@@ -312,6 +319,7 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
     int64_t events, steps;
     op_counts(c, events, steps);
     ev += events; st += steps; nv += 1;
+    tk += (unsigned long long)(c.K * c.P * (c.M.kind == 0 ? 2 : 1));
     const uint32_t key = bucket_key(c);
     uint32_t slot = (key * 2654435761u) >> 20;                 // 12-bit hash
     uint32_t found = kOverflowBucket + (is_zero(c) ? 3u : c.M.sched ? 2u : (uint32_t)c.M.kind);
@@ -329,8 +337,10 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
     ev += __shfl_xor_sync(0xffffffffu, ev, o);
     st += __shfl_xor_sync(0xffffffffu, st, o);
     nv += __shfl_xor_sync(0xffffffffu, nv, o);
+    tk += __shfl_xor_sync(0xffffffffu, tk, o);
   }
   if ((threadIdx.x & 31) == 0 && nv) {
+    atomicAdd(&hdr->tasks, tk);
     atomicAdd(&hdr->op_events, ev);
     atomicAdd(&hdr->stage_steps, st);
     atomicAdd(&hdr->n_valid, nv);
@@ -576,6 +586,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
   double* row = s_dyn + threadIdx.x * ROW;
   double* wtab = s_dyn + sim_tpb(KIND, MODE) * ROW + (threadIdx.x >> 5) * sim_tab_cfgs(KIND) * TAB;
   unsigned long long feas = 0;
+  WorkCount wc{0u, 0u};
   while (true) {
     unsigned int id;
     if (first_item) {
@@ -607,12 +618,12 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
 #ifdef DISTIR_INSTR
     const long long t0 = clock64();
 #endif
-    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk);
-    else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk);
+    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+    else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
     else if (warp_max_int(has ? c.M.rc : 0))          // bucket key: warp-uniform
-      run_mlp<V, SEQ, MODE == 5 || MODE == 7, true>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+      run_mlp<V, SEQ, MODE == 5 || MODE == 7, true>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
     else
-      run_mlp<V, SEQ, MODE == 5 || MODE == 7, false>(c, tp, has, sl, S, lane, row, tab, ms, pk);
+      run_mlp<V, SEQ, MODE == 5 || MODE == 7, false>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
 #ifdef DISTIR_INSTR
     if (lane == 0) {
       const unsigned long long dt = (unsigned long long)(clock64() - t0);
@@ -639,8 +650,16 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
       feas += r == 0;
     }
   }
-  for (int o = 16; o > 0; o >>= 1) feas += __shfl_xor_sync(0xffffffffu, feas, o);
-  if (lane == 0 && feas) atomicAdd(&hdr->n_feasible, feas);
+  unsigned long long slow = wc.slow;
+  for (int o = 16; o > 0; o >>= 1) {
+    feas += __shfl_xor_sync(0xffffffffu, feas, o);
+    slow += __shfl_xor_sync(0xffffffffu, slow, o);
+  }
+  if (lane == 0) {
+    if (feas) atomicAdd(&hdr->n_feasible, feas);
+    if (slow) atomicAdd(&hdr->slow_tasks, slow);
+    if (wc.steps) atomicAdd(&hdr->wave_steps, (unsigned long long)wc.steps);
+  }
 }
 
 #endif  // DISTIR_HOST_TU

@@ -56,6 +56,11 @@ __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int
 #ifndef DISTIR_PLAIN_AFTER_MLP
 #define DISTIR_PLAIN_AFTER_MLP 1   // MLP kernels: walk the rest of a task op by op after N binade crossings (W5 -16%, W2 +2%, W4 +4%)
 #endif
+#ifndef DISTIR_PLAIN_BLOCKS
+#define DISTIR_PLAIN_BLOCKS 12
+#endif
+constexpr int kPlainBlocks = DISTIR_PLAIN_BLOCKS;   // GPT-2: walk tasks of <= 12 blocks op by op
+                                                    // when the quick path cannot take them
 #ifndef DISTIR_QUICK3
 #define DISTIR_QUICK3 1     // GPT-2: straight-line stale-cache / single-crossing slow path
 #endif
@@ -95,7 +100,7 @@ __device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, in
 
 template <int V, bool SEQ, bool F1B, bool RC>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                        double* row, double* tab, double& ms_out, int64_t& peak_out) {
+                        double* row, double* tab, double& ms_out, int64_t& peak_out, WorkCount& wc) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
   const int64_t m = has ? c.B / (D * K) : 0;
   const int32_t ns = tp.node_size;
@@ -239,6 +244,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       if (act) mem_apply(live[q], peak[q], pf[q]);
     }
     const bool slow = task_fast_or_slow(clk[q], cf[q], act);
+    wc.slow += slow;
     DISTIR_SLOW_T0
     const bool any = DISTIR_ANY(slow);
     if (any) {
@@ -258,6 +264,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       if (act) mem_apply(live[q], peak[q], pb[q]);
     }
     const bool slow = task_fast_or_slow(clk[q], cb[q], act);
+    wc.slow += slow;
     DISTIR_SLOW_T0
     const bool any = DISTIR_ANY(slow);
     if (any) {
@@ -351,6 +358,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       }
     };
     for (int iter = 0; iter < max_iter; iter++) {
+      wc.steps++;
       int which[V], tkind[V];
 #pragma unroll
       for (int q = 0; q < V; q++) next_event(q, which[q], tkind[q]);
@@ -417,6 +425,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     // ---- program order (one lane owns all P <= V stages)
     const int K_ = warp_max_int(has ? (int)K : 0);
     for (int k = 0; k < K_; k++) {
+      wc.steps++;
 #pragma unroll
       for (int q = 0; q < V; q++) {
         fwd_task(q, ok[q] && k < K);
@@ -429,6 +438,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       }
     }
     for (int k = 0; k < K_; k++) {
+      wc.steps++;
 #pragma unroll
       for (int q = V - 1; q >= 0; q--) {
         bwd_task(q, ok[q] && k < K);
@@ -478,6 +488,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 #pragma unroll
     for (int q = 0; q < V; q++) kk[q] = -s[q];
     for (int w = 0; w < nsteps; w++) {
+      wc.steps++;
       bool act[V], rcv[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
@@ -503,6 +514,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 #pragma unroll
     for (int q = 0; q < V; q++) kk[q] = -(int)(P - 1 - s[q]);
     for (int w = 0; w < nsteps; w++) {
+      wc.steps++;
       bool act[V], rcv[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
@@ -557,7 +569,10 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 // ------------------------------------------------ GPT-2 inference (C.4) -----
 template <int V, bool SEQ>
 __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                         double* row, double* tab, double& ms_out, int64_t& peak_out) {
+                         double* row, double* tab, double& ms_out, int64_t& peak_out, WorkCount& wc) {
+#ifdef DISTIR_INSTR
+  const long long t_entry = clock64();
+#endif
   const int64_t L = c.M.L, d = c.M.d, h = c.M.h, Sq = c.M.S, Vp = c.M.V, e = c.M.e,
                 ide = c.M.ide, nctx = c.M.nctx;
   const bool lm = c.M.lm != 0;
@@ -691,14 +706,22 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     bt = bintab_range(has ? tab : nullptr, kTabBinadesGpt2, 3, cmin, work, P, S, 1.0);
     Seg sg[3];
     segs(0, sg);
+#ifdef DISTIR_INSTR
+    const long long t_fill = clock64();
+    if (lane == 0) distir_clk_add(18, t_entry);
+#endif
     bintab_fill(bt, sg, sl, S);
     __syncwarp();
+#ifdef DISTIR_INSTR
+    if (lane == 0) distir_clk_add(20, t_fill);
+#endif
   }
   auto task = [&](int q, bool act, bool last) {
     if constexpr (SEQ) {
       if (act) mem_apply(live[q], peak[q], last ? ptask1[q] : ptask0[q]);
     }
     const bool slow = task_fast_or_slow(clk[q], tc[q], act);
+    wc.slow += slow;
     DISTIR_SLOW_T0
     const bool any = DISTIR_ANY(slow);
     if (any) {
@@ -710,10 +733,20 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], tc[q], bt)))
         s2 = slow && !task_cross1(clk[q], sg, tc[q], bt, kMapId3);
 #if DISTIR_QUICK3
+      // op by op: stage 0's first task (from zero, it climbs many binades),
+      // and short tasks (few blocks) the quick path cannot take (ties)
+      if (s2 && clk[q] == 0.0) {
+        task3_plain(clk[q], sg);
+        s2 = false;
+      }
       if (s2) {
         DISTIR_COUNT(16);
         s2 = !task3_quick(clk[q], sg, tc[q], bt);
         if (!s2) DISTIR_COUNT(17);
+      }
+      if (s2 && nb[q] <= kPlainBlocks) {
+        task3_plain(clk[q], sg);
+        s2 = false;
       }
 #endif
       if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3);
@@ -724,6 +757,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     // ---- program order (one lane owns all P <= V stages)
     const int K_ = warp_max_int(has ? (int)K : 0);
     for (int k = 0; k < K_; k++) {
+      wc.steps++;
 #pragma unroll
       for (int q = 0; q < V; q++) {
         task(q, ok[q] && k < K, k == K - 1);
@@ -771,6 +805,7 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     recvc[q] = dn[q] ? cost_send(nde, group_intra(r0 - T * D, r0, ns), tp) : 0.0;  // Send s-1 -> s
   }
   for (int w = 0; w < nsteps; w++) {
+      wc.steps++;
     if (lane == 0) DISTIR_COUNT(4);
     bool act[V], rcv[V];
 #pragma unroll
@@ -827,7 +862,7 @@ __device__ __forceinline__ double cost_chain(int64_t g, int64_t bytes, bool intr
 }
 
 static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
-                             double* row, double* tab, double& ms_out, int64_t& peak_out) {
+                             double* row, double* tab, double& ms_out, int64_t& peak_out, WorkCount& wc) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
   const int64_t m = has ? c.B / (D * K) : 0;
   const int32_t ns = tp.node_size;
@@ -961,6 +996,7 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
     const double mx = segmax(clk);
     if (act) clk = mx;
     const bool slow = task_fast_or_slow(clk, cf, act);
+    wc.slow += slow;
     const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[3];
@@ -977,6 +1013,7 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
     const double mx = segmax(clk);
     if (act) clk = mx;
     const bool slow = task_fast_or_slow(clk, cb, act);
+    wc.slow += slow;
     const bool any = DISTIR_ANY(slow);
     if (any) {
       Seg sg[9];
@@ -999,6 +1036,7 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
   {   // forward wavefront: task (k, s) at step 2k + s, then Send s -> s+1
     int kk = -st;
     for (int wv = 0; wv < nsteps; wv++) {
+      wc.steps++;
       const bool act = ok && (unsigned int)kk < K2 && !(kk & 1);
       const bool rcv = dn && (unsigned int)(kk + 1) < K2 && (kk & 1);
       kk++;
@@ -1013,6 +1051,7 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
   {   // backward wavefront: task (k, s) at step 2k + (P-1-s), then Send s -> s-1
     int kk = -(int)(P - 1 - st);
     for (int wv = 0; wv < nsteps; wv++) {
+      wc.steps++;
       const bool act = ok && (unsigned int)kk < K2 && !(kk & 1);
       const bool rcv = up && (unsigned int)(kk + 1) < K2 && (kk & 1);
       kk++;
