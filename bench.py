@@ -164,23 +164,22 @@ def cpu_model():
 def cpu_oracle_rate(grid, seconds, seed=20211105426, threads=None):
     """Time the oracle (as it stands) on a seeded random sample of the grid
     for about `seconds` of wall time on `threads` host threads (configs are
-    handed out one at a time); op-events/s.  A first call on 2 configs per
-    thread sizes the sample; the rest is ONE call, so the threads never wait
-    for each other between chunks."""
+    handed out one at a time); op-events/s.  Calls grow geometrically, each
+    sized to about half the remaining time at the rate measured so far, so
+    the threads rarely wait for each other at a call's end and the total
+    stays near `seconds` (configs differ in size by orders of magnitude)."""
     import oracle
     oracle.build()
     threads = threads or os.cpu_count() or 1
     n = len(oracle.enumerate_grid(grid)) if grid["synth_count"] == 0 else grid["synth_count"]
     order = np.random.default_rng(seed).permutation(n)
     ops, cfgs, dt, pos = 0, 0, 0.0, 0
-    for part in range(2):
-        if part == 0:
-            m = min(n, 2 * threads)
+    while pos < n and dt < 0.9 * seconds:
+        if cfgs == 0:
+            m = threads
         else:
-            rate = cfgs / max(dt, 1e-9)
-            m = int(min(n - pos, max(0.0, seconds - dt) * rate))
-            if m <= 0:
-                break
+            m = max(threads, int(0.5 * (seconds - dt) * cfgs / dt))
+        m = min(m, n - pos)
         idx = np.sort(order[pos:pos + m])
         pos += m
         t = time.perf_counter()

@@ -125,11 +125,26 @@ struct Bucket {          // per hash slot (plus one overflow slot)
 };
 
 struct Item {            // one warp's worth of configs of one bucket
-  uint32_t first;        // position in perm
+  uint32_t first;        // position in the permuted config list
   uint16_t bucket;
   uint8_t n;             // configs in this item
+  uint8_t lg_lanes;      // log2(lanes per config)
+};
+
+// A decoded configuration as k_enumerate packs it and k_scatter permutes it
+// into warp order, so k_simulate reads each config with one load instead of
+// re-decoding (the grid decode is a binary search over a table in HBM).
+struct PCfg {
+  int64_t B;
+  uint32_t q;            // shard position (output index)
+  uint16_t K;
+  uint8_t P;
+  uint8_t model;         // index into SpecBlock.models; kSynthModel: synthetic
+  uint8_t topo;
+  uint8_t lgD, lgT;
   uint8_t pad;
 };
+constexpr uint8_t kSynthModel = 0xFF;   // model drawn by the synthetic sweep (re-decoded)
 
 struct TopkRec {         // == distir_topk_entry
   int64_t index;

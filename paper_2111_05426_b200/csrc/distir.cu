@@ -64,7 +64,7 @@ int ilog2(int64_t x) {
 
 // ------------------------------------------------------------ layout -------
 struct Layout {
-  size_t hdr, spec, ex, bk, cfg_bucket, perm, items, ms, pk, rs, tp, part, part_n, gath, fin,
+  size_t hdr, spec, ex, bk, cfg_bucket, pc, perm, items, ms, pk, rs, tp, part, part_n, gath, fin,
       fin_n, out, out_n, total;
 };
 
@@ -82,7 +82,8 @@ Layout layout(int64_t n_local, int64_t n_explicit) {
   L.ex = take((size_t)(n_explicit > 0 ? n_explicit : 1) * sizeof(DExplicit));
   L.bk = take(kBucketSlots * sizeof(Bucket));
   L.cfg_bucket = take(n * 4);
-  L.perm = take(n * 4);
+  L.pc = take(n * sizeof(PCfg));
+  L.perm = take(n * sizeof(PCfg));
   L.items = take(n * sizeof(Item));
   L.ms = take(n * 8);
   L.pk = take(n * 8);
@@ -469,7 +470,8 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   Bucket* bk = at<Bucket>(ws, L.bk);
   WsHeader* hdr = at<WsHeader>(ws, L.hdr);
   uint32_t* cb = at<uint32_t>(ws, L.cfg_bucket);
-  uint32_t* perm = at<uint32_t>(ws, L.perm);
+  PCfg* pc = at<PCfg>(ws, L.pc);
+  PCfg* perm = at<PCfg>(ws, L.perm);
   Item* items = at<Item>(ws, L.items);
   double* tpv = at<double>(ws, L.tp);
   k_reset<<<(kBucketSlots + 255) / 256, 256, 0, st>>>(bk, hdr);
@@ -477,12 +479,12 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   const int64_t n = sp.n_local;
   if (n > 0) {
     const int eg = (int)std::min<int64_t>((n + 255) / 256, sim->enum_grid);
-    k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, hdr);
+    k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, pc, hdr);
     PlanBudget pb;
     for (int g = 0; g < kGroups; g++)
       pb.warps[g] = (uint32_t)(sim->plan_x * sim->sim_grid[g] * (sim_tpb(g / kModes, g % kModes) / 32));
     k_plan<<<1, kPlanThreads, 0, st>>>(bk, hdr, pb);
-    k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, perm, items);
+    k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, pc, perm, items);
     kernels += 3;
   }
   CUDA_TRY(mark(1));

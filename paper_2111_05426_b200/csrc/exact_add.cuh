@@ -125,19 +125,23 @@ DISTIR_HD void seq_plain(double& x, const double* a, int n) {
 // such a double are exact, and sums of integers below 2^53 are exact.
 DISTIR_HD bool seg_pass_d(const double* a, int n, int32_t ef, double& R0, double& R1) {
   const double inv_u = bits2d((int64_t)(2098 - ef) << 52);    // 2^(52-E)
-  double R = 0.0;
+  // the ops are independent: two partial sums halve the dependent chain (the
+  // integers add exactly while below 2^53; a total >= 2^53 fails below
+  // either way, rounding being monotone)
+  double Ra = 0.0, Rb = 0.0;
   bool tie = false, never = false;
-#if DISTIR_UNROLL_SEG
 #pragma unroll
-#endif
-  for (int j = 0; j < kSegMax; j++) {             // the ops are independent
-    if (j >= n) break;
-    const double q = xmul(a[j], inv_u);
-    never |= !(q < kTwo53d);
-    tie |= (xadd(q, -xfloor(q)) == 0.5);
-    R = xadd(R, xrint(q));
+  for (int j = 0; j < kSegMax; j++) {
+    if (j < n) {
+      const double q = xmul(a[j], inv_u);
+      never |= !(q < kTwo53d);
+      tie |= (xadd(q, -xfloor(q)) == 0.5);
+      if (j & 1) Rb = xadd(Rb, xrint(q));
+      else Ra = xadd(Ra, xrint(q));
+    }
   }
   if (never) return false;
+  const double R = xadd(Ra, Rb);
   R0 = R1 = R;
   if (tie) {                      // resolve ties by the running parity
     R0 = R1 = 0.0;
@@ -320,10 +324,15 @@ DISTIR_HD bool task_fast(double& x, const TaskCache& c) {
 // The same, for a lane that runs the task only when `act`: evaluated
 // unconditionally (no divergent branch), applied under `act`; true when the
 // task still has to be performed (act and not fast).
+#ifndef DISTIR_FAST_LO
+#define DISTIR_FAST_LO 0
+#endif
 DISTIR_HD bool task_fast_or_slow(double& x, const TaskCache& c, bool act) {
   const double Su = (loword(x) & 1) ? c.Su1 : c.Su0;
   const double y = xadd(x, Su);
-  const bool ok = act && hiword(x) >= c.lo && hiword(y) < c.hi;
+  // (clocks never decrease and the cache is only ever set for the binade x
+  // is in, so with DISTIR_FAST_LO=0 the lower bound is implied)
+  const bool ok = act && (!DISTIR_FAST_LO || hiword(x) >= c.lo) && hiword(y) < c.hi;
   x = ok ? y : x;
   return act && !ok;
 }
@@ -387,7 +396,7 @@ DISTIR_HD bool task_cross1(double& x, const Seg (&sg)[NS], TaskCache& c, const B
   double y = bits2d(((int64_t)ef << 52) | ((M + C + fit * rj) & kMant));   // exact, in E
   seq_plain(y, aj, naj);
   const int64_t yb = d2bits(y);
-  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) return false;
+  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) { DISTIR_COUNT(25); return false; }
   // the rest of the task in E+1
   int64_t rest = 0, T1 = 0;                           // both capped at 2^53
   auto cap_add = [](int64_t a, int64_t b) { return (a >= kTwo53 || b >= kTwo53) ? kTwo53 : a + b; };
@@ -400,7 +409,7 @@ DISTIR_HD bool task_cross1(double& x, const Seg (&sg)[NS], TaskCache& c, const B
     else if (i > j) rest = cap_add(rest, sg[i].reps * r1);
   }
   const int64_t M1 = (yb & kMant) | kHidden;
-  if (M1 + rest > kTwo53 - 1) return false;
+  if (M1 + rest > kTwo53 - 1) { DISTIR_COUNT(26); return false; }
   x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
   // the cache follows x into E+1 (no ties: the total does not depend on parity)
 #pragma unroll
@@ -419,30 +428,169 @@ DISTIR_HD bool task_cross1(double& x, const Seg (&sg)[NS], TaskCache& c, const B
   return true;
 }
 
-// Straight-line slow path of a three-segment task p x A + n x B + e x C
+// Slow path of a three-segment task p x A + n x B + e x C
 // (p, e in {0, 1}; A, B, C the first three lists of the binade table, B the
-// repeated one -- a GPT-2 stage: prologue, blocks, epilogue), for the two
-// common cases, when the table covers x's binade E (and E + 1) and the lists
-// have no ties there (their per-pass increments do not depend on parity):
+// repeated one -- a GPT-2 stage: prologue, blocks, epilogue), when the table
+// covers x's binade E (and E + 1):
 //   (i)  a stale cache -- x moved into E between tasks (a Send) and the whole
-//        task fits E: x <- x + (p*A + n*B + e*C) ulps;
-//   (ii) one crossing inside the B passes: the fitting passes in closed form,
-//        the crossing pass op by op, the rest of the task in closed form in
-//        E + 1, which must hold it.
+//        task fits E: x <- x + its ulps;
+//   (ii) one crossing: the passes that fit E in closed form, the pass that
+//        leaves E op by op, the rest of the task in closed form in E + 1,
+//        which must hold it.
+// Ties are handled exactly: a pass adds R0 ulps from an even significand and
+// R1 from an odd one, so n passes add the closed form of reps_total and the
+// parity after them is the start parity xor the total's low bit.
 // Returns false with x untouched in every other case (add_task handles it).
 // The cache follows x into its new binade, per-segment increments included
 // (segment i is table list i: the identity map).
-DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const BinTab& t) {
+DISTIR_HD int64_t task3_total(const int64_t* r, int64_t p, int64_t n, int64_t e, int par) {
+  // r = {A0, A1, B0, B1, C0, C1} (even / odd start) of one binade; capped at 2^53
+  int64_t t = 0;
+  if (p) {
+    const int64_t a = par ? r[1] : r[0];
+    t = a;
+    par ^= (int)(a & 1);
+  }
+  if (n > 0) {
+    const int64_t b = reps_total(r[2], r[3], par, n);
+    if (b >= kTwo53) return kTwo53;
+    t += b;
+    par ^= (int)(b & 1);
+  }
+  if (e) t += par ? r[5] : r[4];
+  return t < kTwo53 ? t : kTwo53;
+}
+
+#if defined(DISTIR_TIES) && DISTIR_TIES == 2 && defined(__CUDACC__)
+__host__ __device__ __noinline__
+#else
+DISTIR_HD
+#endif
+bool task3_quick_ties(double& x, const Seg (&sg)[3], TaskCache& c, const BinTab& t) {
   const int64_t xb = d2bits(x);
   const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
   const int32_t b = ef - t.e0;
-  if (!(x > 0.0) || b < 0 || b >= t.nb || ef > 1992) return false;
+  if (!(x > 0.0) || b < 0 || b >= t.nb || ef > 1992) { DISTIR_COUNT(29); return false; }
+  const int64_t* r0 = t.tab + (int64_t)b * 6;
+  const int64_t p = sg[0].reps, n = sg[1].reps, e = sg[2].reps;
+  int64_t q0[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) q0[i] = r0[i];
+  if (q0[2] >= kNeverI || (p && q0[0] >= kNeverI) || (e && q0[4] >= kNeverI)) {
+    DISTIR_COUNT(29);
+    return false;
+  }
+  const int64_t M = (xb & kMant) | kHidden, avail = kTwo53 - 1 - M;
+  const int par0 = (int)(M & 1);
+  const int64_t tot = task3_total(q0, p, n, e, par0);
+  if (tot <= avail) {                                   // (i) the task fits E
+    x = bits2d(((int64_t)ef << 52) | ((M + tot) & kMant));
+    const double u = bits2d((int64_t)(ef - 52) << 52);
+    const int64_t T0 = par0 ? task3_total(q0, p, n, e, 0) : tot;
+    const int64_t T1 = par0 ? tot : task3_total(q0, p, n, e, 1);
+#pragma unroll
+    for (int i = 0; i < 6; i++) c.R[i] = q0[i];
+    c.ef = ef;
+    c.lo = ef << 20;
+    c.hi = (ef + 1) << 20;
+    c.Su0 = T0 < kTwo53 ? xmul((double)T0, u) : kInf();
+    c.Su1 = T1 < kTwo53 ? xmul((double)T1, u) : kInf();
+    return true;
+  }
+  if (b + 1 >= t.nb) { DISTIR_COUNT(29); return false; }
+  const int64_t* r1 = r0 + 6;
+  int64_t q1[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) q1[i] = r1[i];
+  if (q1[2] >= kNeverI || (p && q1[0] >= kNeverI) || (e && q1[4] >= kNeverI)) {
+    DISTIR_COUNT(29);
+    return false;
+  }
+  // (ii) the segment that leaves E: A (from x), B (the passes that still fit,
+  // then one) or C (after A and every B pass); that pass is walked op by op
+  // from the exact value where it starts, the rest of the task (B passes
+  // left, C) is added in E + 1 from the parity the walk ends on
+  int par = par0;
+  int64_t Cp = 0;
+  if (p) {
+    Cp = par ? q0[1] : q0[0];
+    par ^= (int)(Cp & 1);
+  }
+  int64_t pre, nrest, erest;
+  const double* a;
+  int na;
+  if (Cp > avail) {                                           // crossing in A
+    pre = 0; a = sg[0].a; na = sg[0].n;
+    nrest = n; erest = e;
+  } else {
+    const int64_t room = avail - Cp;
+    const int64_t CB = reps_total(q0[2], q0[3], par, n);     // capped (kNeverI)
+    if (CB > room) {                                          // crossing in B
+      // passes add Ra, then (Ra odd) Rb, ...: cum(j) below; fit = the most
+      // whole passes (< n) with cum(fit) <= room
+      const int64_t Ra = par ? q0[3] : q0[2], Rb = par ? q0[2] : q0[3];
+      const int kind = !(Ra & 1) ? 0 : (!(Rb & 1) ? 1 : 2);
+      auto cum = [&](int64_t j) -> int64_t {                  // j <= 2^10: no overflow
+        if (j <= 0) return 0;
+        if (kind == 0) return j * Ra;
+        if (kind == 1) return Ra + (j - 1) * Rb;
+        return ((j + 1) >> 1) * Ra + (j >> 1) * Rb;
+      };
+      const float avg = kind == 0 ? (float)Ra : kind == 1 ? (float)Rb : 0.5f * ((float)Ra + (float)Rb);
+      int64_t fit = avg > 0.0f ? (int64_t)fdiv_approx((float)room, avg) : n - 1;
+      fit = fit < 0 ? 0 : (fit > n - 1 ? n - 1 : fit);
+      while (fit > 0 && cum(fit) > room) fit--;
+      while (fit + 1 < n && cum(fit + 1) <= room) fit++;
+      pre = Cp + cum(fit); a = sg[1].a; na = sg[1].n;
+      nrest = n - fit - 1; erest = e;
+    } else {                                                  // crossing in C
+      pre = Cp + CB; a = sg[2].a; na = sg[2].n;
+      nrest = 0; erest = 0;
+    }
+  }
+  double y = bits2d(((int64_t)ef << 52) | ((M + pre) & kMant));   // exact, in E
+  {
+    double v[kSegMax];
+#pragma unroll
+    for (int j = 0; j < kSegMax; j++) v[j] = j < na ? a[j] : 0.0;   // loads first
+#pragma unroll
+    for (int j = 0; j < kSegMax; j++)
+      if (j < na) y = xadd(y, v[j]);
+  }
+  const int64_t yb = d2bits(y);
+  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) { DISTIR_COUNT(29); return false; }
+  const int64_t M1 = (yb & kMant) | kHidden;
+  const int64_t rest = task3_total(q1, 0, nrest, erest, (int)(M1 & 1));
+  if (M1 + rest > kTwo53 - 1) { DISTIR_COUNT(29); return false; }
+  x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
+  const double u1 = bits2d((int64_t)(ef + 1 - 52) << 52);
+  const int64_t T0 = task3_total(q1, p, n, e, 0), T1 = task3_total(q1, p, n, e, 1);
+#pragma unroll
+  for (int i = 0; i < 6; i++) c.R[i] = q1[i];
+  c.ef = ef + 1;
+  c.lo = (ef + 1) << 20;
+  c.hi = (ef + 2) << 20;
+  c.Su0 = T0 < kTwo53 ? xmul((double)T0, u1) : kInf();
+  c.Su1 = T1 < kTwo53 ? xmul((double)T1, u1) : kInf();
+  return true;
+}
+
+// The no-tie case in straight-line code: 1 when done, 2 when a list has a tie
+// in E (or, crossing, in E + 1) -- task3_quick_ties then applies -- and 0
+// otherwise (x untouched in both).
+DISTIR_HD int task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const BinTab& t) {
+  const int64_t xb = d2bits(x);
+  const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+  const int32_t b = ef - t.e0;
+  if (!(x > 0.0) || b < 0 || b >= t.nb || ef > 1992) { DISTIR_COUNT(21); return 0; }
   const int64_t* r0 = t.tab + (int64_t)b * 6;
   const int64_t A0 = r0[0], A0b = r0[1], B0 = r0[2], B0b = r0[3], C0 = r0[4], C0b = r0[5];
   const int64_t p = sg[0].reps, n = sg[1].reps, e = sg[2].reps;
   if (!(B0 == B0b && B0 < kNeverI && (!p || (A0 == A0b && A0 < kNeverI)) &&
-        (!e || (C0 == C0b && C0 < kNeverI))))
-    return false;
+        (!e || (C0 == C0b && C0 < kNeverI)))) {
+    DISTIR_COUNT(22);
+    return 2;
+  }
   // (products saturate at 2^53: n <= 2^10 and increments < 2^53, so n * B
   // fits int64 and saturated sums cannot overflow)
   auto sat = [](int64_t v) { return v > kTwo53 ? kTwo53 : v; };
@@ -456,14 +604,16 @@ DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bi
     c.lo = ef << 20;
     c.hi = (ef + 1) << 20;
     c.Su0 = c.Su1 = xmul((double)tot, bits2d((int64_t)(ef - 52) << 52));
-    return true;
+    return 1;
   }
-  if (b + 1 >= t.nb) return false;
+  if (b + 1 >= t.nb) { DISTIR_COUNT(23); return 0; }
   const int64_t* r1 = r0 + 6;
   const int64_t A1 = r1[0], A1b = r1[1], B1 = r1[2], B1b = r1[3], C1 = r1[4], C1b = r1[5];
   if (!(B1 == B1b && B1 < kNeverI && (!p || (A1 == A1b && A1 < kNeverI)) &&
-        (!e || (C1 == C1b && C1 < kNeverI))))
-    return false;
+        (!e || (C1 == C1b && C1 < kNeverI)))) {
+    DISTIR_COUNT(24);
+    return 2;
+  }
   // (ii) the segment that leaves E: A (whole task from x), B (the passes that
   // still fit, then one), or C (after A and every B pass); that pass is walked
   // op by op from the exact value where it starts, the rest of the task is
@@ -498,9 +648,9 @@ DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bi
       if (j < na) y = xadd(y, v[j]);
   }
   const int64_t yb = d2bits(y);
-  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) return false;
+  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) { DISTIR_COUNT(25); return 0; }
   const int64_t M1 = (yb & kMant) | kHidden;
-  if (M1 + rest > kTwo53 - 1) return false;
+  if (M1 + rest > kTwo53 - 1) { DISTIR_COUNT(26); return 0; }
   x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
   const int64_t tot1 = p * A1 + sat(n * B1) + e * C1;
   c.R[0] = A1; c.R[1] = A1b; c.R[2] = B1; c.R[3] = B1b; c.R[4] = C1; c.R[5] = C1b;
@@ -508,7 +658,7 @@ DISTIR_HD bool task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bi
   c.lo = (ef + 1) << 20;
   c.hi = (ef + 2) << 20;
   c.Su0 = c.Su1 = tot1 < kTwo53 ? xmul((double)tot1, bits2d((int64_t)(ef + 1 - 52) << 52)) : kInf();
-  return true;
+  return 1;
 }
 
 // A three-segment task (as task3_quick) walked op by op -- for a clock at

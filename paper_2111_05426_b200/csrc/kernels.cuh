@@ -65,6 +65,7 @@ namespace distir {
 struct Cfg {
   DModel M;
   int32_t topo;
+  int32_t mi;            // index of M in SpecBlock.models, -1 when synthetic
   int64_t D, T, P, K, B;
 };
 
@@ -81,6 +82,7 @@ __device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t 
   if (sp.mode == MODE_EXPLICIT) {
     const DExplicit x = ex[i];
     c.M = sp.models[x.model];
+    c.mi = x.model;
     c.topo = x.topo;
     c.D = x.dp; c.T = x.tp; c.P = x.pp; c.K = x.K; c.B = x.B;
     return;
@@ -107,6 +109,7 @@ __device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t 
       c.M = DModel{1, L, d, h, 8, 50304, 1024, 2, 8, 1, 0, 0, 0};
     }
     c.topo = sp.topo_ids[r[7] % (uint64_t)sp.n_topos];
+    c.mi = -1;
     return;
   }
   const int64_t mt = i / sp.per_mt;
@@ -122,6 +125,7 @@ __device__ inline void decode(const SpecBlock& sp, const DExplicit* ex, int64_t 
   const int64_t r2 = r - en.cum;
   const int64_t kq = r2 / sp.n_batch, bq = r2 - kq * sp.n_batch;
   c.M = sp.models[sp.model_ids[mi]];
+  c.mi = sp.model_ids[mi];
   c.topo = sp.topo_ids[ti];
   c.D = en.D; c.T = en.T; c.P = en.P;
   c.K = (sp.k_mode == 0 && en.P == 1) ? 1 : sp.k_set[kq];
@@ -294,7 +298,7 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
                             Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
                             double* __restrict__ ms_out, int64_t* __restrict__ pk_out,
                             uint32_t* __restrict__ rs_out, double* __restrict__ tp_out,
-                            WsHeader* __restrict__ hdr) {
+                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr) {
   const SpecBlock& sp = *spp;
   const int64_t nloc = sp.n_local;
   unsigned long long ev = 0, st = 0, nv = 0, tk = 0;
@@ -331,6 +335,10 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
     }
     atomicAdd(&bk[found].count, 1u);
     cfg_bucket[q] = found;
+    pc_out[q] = PCfg{c.B, (uint32_t)q, (uint16_t)c.K, (uint8_t)c.P,
+                     c.mi < 0 ? kSynthModel : (uint8_t)c.mi, (uint8_t)c.topo,
+                     (uint8_t)(63 - __clzll((unsigned long long)c.D)),
+                     (uint8_t)(63 - __clzll((unsigned long long)c.T)), 0};
   }
   // warp-aggregated statistics
   for (int o = 16; o > 0; o >>= 1) {
@@ -505,8 +513,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, 
 }
 
 __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
-                          const uint32_t* __restrict__ cfg_bucket, uint32_t* __restrict__ perm,
-                          Item* __restrict__ items) {
+                          const uint32_t* __restrict__ cfg_bucket, const PCfg* __restrict__ pc,
+                          PCfg* __restrict__ perm, Item* __restrict__ items) {
   const int64_t nloc = spp->n_local;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nloc;
        q += (int64_t)gridDim.x * blockDim.x) {
@@ -514,14 +522,14 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
     if (b == kEmptyKey) continue;
     const uint32_t pos = atomicAdd(&bk[b].cursor, 1u);
     const uint32_t cpw = bk[b].cpw;
-    perm[bk[b].cfg_base + pos] = (uint32_t)q;
+    perm[bk[b].cfg_base + pos] = pc[q];
     if (pos % cpw == 0) {
       const uint32_t cnt = bk[b].count;
       Item it;
       it.first = bk[b].cfg_base + pos;
       it.bucket = (uint16_t)b;
       it.n = (uint8_t)(cnt - pos < cpw ? cnt - pos : cpw);
-      it.pad = 0;
+      it.lg_lanes = (uint8_t)(31 - __clz((int)bk[b].lanes));
       items[bk[b].item_base + pos / cpw] = it;
     }
   }
@@ -557,11 +565,14 @@ __host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic sme
 
 #ifndef DISTIR_HOST_TU
 template <int KIND, int MODE>
-__global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecBlock* __restrict__ spp,
+#ifndef DISTIR_SIM_MINB
+#define DISTIR_SIM_MINB 1      // min resident blocks per SM asked of ptxas (register cap)
+#endif
+__global__ void __launch_bounds__(sim_tpb(KIND, MODE), DISTIR_SIM_MINB) k_simulate(const SpecBlock* __restrict__ spp,
                                                   const DExplicit* __restrict__ ex,
                                                   const Bucket* __restrict__ bk,
                                                   const Item* __restrict__ items,
-                                                  const uint32_t* __restrict__ perm,
+                                                  const PCfg* __restrict__ perm,
                                                   WsHeader* __restrict__ hdr,
                                                   double* __restrict__ ms_out,
                                                   int64_t* __restrict__ pk_out,
@@ -599,17 +610,22 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
     }
     if (id >= end) break;
     const Item it = items[id];
-    const Bucket& B = bk[it.bucket];
-    const int S = (int)B.lanes;
+    const int S = 1 << it.lg_lanes;
     const int seg = lane / S, sl = lane - seg * S;
     const bool has = seg < it.n;
-    const uint32_t q = has ? perm[it.first + seg] : 0u;
+    const PCfg pc = has ? perm[it.first + seg] : PCfg{1, 0u, 1, 1, 0, 0, 0, 0, 0};
+    const uint32_t q = pc.q;
     Cfg c;
-    if (has) {
-      decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);
+    if (has && pc.model == kSynthModel) {
+      decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);     // arithmetic only
+    } else if (has) {
+      c.M = sp.models[pc.model];
+      c.mi = pc.model;
+      c.topo = pc.topo;
+      c.D = 1ll << pc.lgD; c.T = 1ll << pc.lgT; c.P = pc.P; c.K = pc.K; c.B = pc.B;
     } else {
       c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0};
-      c.topo = 0; c.D = c.T = c.P = c.K = c.B = 1;
+      c.topo = 0; c.mi = 0; c.D = c.T = c.P = c.K = c.B = 1;
     }
     const DTopo& tp = sp.topos[c.topo];
     double* tab = (TAB > 0 && S >= 2 && seg < sim_tab_cfgs(KIND)) ? wtab + seg * TAB : nullptr;
@@ -631,7 +647,7 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), 1) k_simulate(const SpecB
       atomicAdd(&g_distir_instr[7], 1ull);
       atomicMax(&g_distir_instr[8], dt);
       // slowest item: cycles and its bucket key / configs (for probe_instr)
-      atomicMax(&g_distir_instr[11], (dt << 24) | ((unsigned long long)(B.key & 0x7FFFF) << 5) |
+      atomicMax(&g_distir_instr[11], (dt << 24) | ((unsigned long long)(bk[it.bucket].key & 0x7FFFF) << 5) |
                                          (unsigned long long)(it.n & 31));
     }
 #endif
@@ -849,6 +865,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(
         if (lane == wl) { s_acc[cur ^ 1][r] = mine; ptr++; }
         o++;
       }
+      __syncwarp();                    // every lane has read s_acc_n
       if (lane == 0) s_acc_n = o;
     }
     cur ^= 1;

@@ -14,7 +14,7 @@ struct SimArgs {
   const DExplicit* ex;
   const Bucket* bk;
   const Item* items;
-  const uint32_t* perm;
+  const PCfg* perm;
   WsHeader* hdr;
   double* ms;
   int64_t* pk;

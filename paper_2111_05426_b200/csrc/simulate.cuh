@@ -61,6 +61,9 @@ __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int
 #endif
 constexpr int kPlainBlocks = DISTIR_PLAIN_BLOCKS;   // GPT-2: walk tasks of <= 12 blocks op by op
                                                     // when the quick path cannot take them
+#ifndef DISTIR_TIES
+#define DISTIR_TIES 0       // GPT-2 tasks of > kPlainBlocks blocks with ties: closed forms
+#endif                      // (task3_quick_ties) instead of add_task; measured equal on W3 (r02j), off
 #ifndef DISTIR_QUICK3
 #define DISTIR_QUICK3 1     // GPT-2: straight-line stale-cache / single-crossing slow path
 #endif
@@ -612,6 +615,10 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   row[16] = c_ln;                                                                    // ln_f
   row[17] = lm ? cost_op(2 * n * d * VT, nde + VT * d * e + n * VT * e, true, tp) : 0.0;  // LM head
   row[18] = (lm && T > 1) ? cost_allgather(T, n * Vp * e, tp_intra, tp) : 0.0;  // AllGather
+#ifdef DISTIR_INSTR
+  if (lane == 0) distir_clk_add(27, t_entry);
+  const long long t_mem = clock64();
+#endif
   // live-memory profiles (C.7), for a normal and for the last microbatch
   // (whose ops free the parameters at their last use)
   const int64_t arb = T > 1 ? nde : 0;
@@ -675,6 +682,9 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
     }
     tc[q] = task_cache_make(i64(row + 19 + 6 * q));       // 3 segments
   }
+#ifdef DISTIR_INSTR
+  if (lane == 0) distir_clk_add(28, t_mem);
+#endif
 
   // the task's segments: prologue (stage 0), blocks, epilogue (stage P-1);
   // the op lists are the same on every lane of the configuration
@@ -741,12 +751,20 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       }
       if (s2) {
         DISTIR_COUNT(16);
-        s2 = !task3_quick(clk[q], sg, tc[q], bt);
+        const int r = task3_quick(clk[q], sg, tc[q], bt);
+        s2 = r != 1;
         if (!s2) DISTIR_COUNT(17);
-      }
-      if (s2 && nb[q] <= kPlainBlocks) {
-        task3_plain(clk[q], sg);
-        s2 = false;
+        // ties: short tasks op by op, long ones by the parity-exact closed forms
+        if (s2 && nb[q] <= kPlainBlocks) {
+          task3_plain(clk[q], sg);
+          s2 = false;
+        }
+#if DISTIR_TIES
+        if (s2 && r == 2) {
+          s2 = !task3_quick_ties(clk[q], sg, tc[q], bt);
+          if (!s2) DISTIR_COUNT(30);
+        }
+#endif
       }
 #endif
       if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, tc[q], bt, kMapId3);

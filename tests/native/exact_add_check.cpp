@@ -2,13 +2,16 @@
 // exact_add.cuh): add_task(x, segments) must equal every plain IEEE addition
 // of the task, in order, bit for bit -- over random, tie-heavy dyadic and
 // zero costs, clocks starting at zero or anywhere, binade crossings, a
-// cache reused across tasks, with and without a precomputed binade table -- and MemProf composition must equal the
+// cache reused across tasks, with and without a precomputed binade table,
+// including the GPT-2 kernels' quick / plain slow paths -- and MemProf composition must equal the
 // op-by-op live/peak walk.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <random>
+static long g_cnt[32];
+#define DISTIR_COUNT(i) (g_cnt[i]++)
 #include "../../paper_2111_05426_b200/csrc/exact_add.cuh"
 
 using namespace distir;
@@ -68,6 +71,59 @@ static long check(std::mt19937_64& g, int trials, int mode) {
   return bad;
 }
 
+// The GPT-2 kernels' slow-path order (simulate.cuh run_gpt2): a task of
+// prologue (0/1 pass) + blocks (n passes) + epilogue (0/1 pass) with an
+// identity-map binade table; fast path, else op by op from a zero clock,
+// else task3_quick, else op by op (short tasks) or add_task.
+static long g_quick_ok = 0, g_ties_ok = 0;
+static long check_gpt2(std::mt19937_64& g, int trials, int mode) {
+  long bad = 0;
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  for (int t = 0; t < trials; t++) {
+    double store[3][14];
+    Seg sg[3];
+    const int ns[3] = {2, 14, 3};
+    for (int i = 0; i < 3; i++) {
+      for (int j = 0; j < ns[i]; j++) store[i][j] = draw_cost(g, mode);
+      sg[i] = Seg{store[i], ns[i], i == 1 ? 1 + (int64_t)(g() % ((g() & 3) ? 48 : 1024))
+                                          : (int64_t)(g() & 1)};
+    }
+    double x = (g() % 5 == 0) ? 0.0 : std::ldexp(U(g), -(int)(g() % 30));
+    double y = x;
+    int64_t cstore[6];
+    TaskCache c = task_cache_make(cstore);
+    static int64_t tstore[64 * 6];
+    BinTab tb{tstore, 0, 0, 3};
+    const int map[3] = {0, 1, 2};
+    if (g() % 8) {
+      tb.e0 = 1023 - 45 + (int)(g() % 40);
+      tb.nb = 1 + (int)(g() % 24);
+      bintab_fill(tb, sg, 0, 1);
+    }
+    const int tasks = 1 + (int)(g() % 60);
+    for (int k = 0; k < tasks; k++) {
+      for (int i = 0; i < 3; i++)
+        for (int64_t r = 0; r < sg[i].reps; r++)
+          for (int j = 0; j < sg[i].n; j++) x = x + sg[i].a[j];
+      if (task_fast_or_slow(y, c, true)) {
+        int r;
+        if (y == 0.0) task3_plain(y, sg);
+        else if (!(g() & 3) && task3_quick_ties(y, sg, c, tb)) g_ties_ok++;   // also without ties
+        else if ((r = task3_quick(y, sg, c, tb)) == 1) g_quick_ok++;
+        else if (r == 2 && task3_quick_ties(y, sg, c, tb)) g_ties_ok++;
+        else if (g() & 1) task3_plain(y, sg);
+        else add_task(y, sg, c, tb, map);
+      }
+      if (std::memcmp(&x, &y, 8) != 0) {
+        if (bad < 5) std::printf("gpt2 mismatch mode=%d task=%d plain=%a agg=%a\n", mode, k, x, y);
+        bad++;
+        break;
+      }
+    }
+  }
+  return bad;
+}
+
 static long check_mem(std::mt19937_64& g, int trials) {
   long bad = 0;
   for (int t = 0; t < trials; t++) {
@@ -96,8 +152,13 @@ int main(int argc, char** argv) {
     bad += check<2>(g, trials, mode);
     bad += check<3>(g, trials, mode);
     bad += check<4>(g, trials, mode);
+    bad += check_gpt2(g, 2 * trials, mode);
   }
   bad += check_mem(g, trials * 5);
+  std::printf("task3_quick_ties: %ld taken\n", g_ties_ok);
+  std::printf("task3_quick: %ld taken; misses: outside table %ld, never-fitting lists %ld / %ld, "
+              "crossing beyond E+1 %ld, rest beyond E+1 %ld\n", g_quick_ok, g_cnt[21], g_cnt[22],
+              g_cnt[24], g_cnt[25], g_cnt[26]);
   std::printf("bad=%ld\n", bad);
   return bad ? 1 : 0;
 }

@@ -20,7 +20,7 @@ if [ "$3" != "skip-ncu" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file "$OUT/launches.csv" python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-strong \
     --e2e-steps 1 > "$OUT/ncu_launch_bench.log" 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on \
+  timeout 900 ncu --set full --clock-control none --import-source on --warp-sampling-interval 2 \
     --kernel-name-base demangled -k "regex:k_simulate<.int.1, .int.3>" --launch-skip 2 --launch-count 2 -o "$OUT/simulate_full" \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-strong --e2e-steps 1 \
     > "$OUT/ncu_full.log" 2>&1

@@ -13,7 +13,8 @@ from paper_2111_05426_b200 import Simulator
 
 NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles",
          "slow_cycles", "slow_entries", "max_item_tag", "refresh_cyc", "cross_cyc", "-", "addtask_cyc",
-         "quick_try", "quick_ok", "setup_cycles", "wave_cycles", "fill_cycles"] + ["-"] * 11
+         "quick_try", "quick_ok", "setup_cycles", "wave_cycles", "fill_cycles", "q_range", "q_tieE", "q_range1", "q_tieE1",
+         "q_twice", "q_rest", "cost_cycles", "mem_cycles"] + ["-"] * 3
 
 
 def counters():
@@ -60,8 +61,12 @@ def main():
             d["refresh_cyc"] / max(d["tasks"], 1), d["cross_cyc"] / max(d["tasks"], 1)))
         print("   quick path: %d tries, %d ok; wavefront cycles (lane 0, summed over items) %d = %.0f%% of item cycles" % (
             d["quick_try"], d["quick_ok"], d["wave_cycles"], 100.0 * d["wave_cycles"] / max(d["item_cycles"], 1)))
-        print("   setup (costs, memory) %d cycles/item, table fill %d cycles/item" % (
-            d["setup_cycles"] / max(d["items"], 1), d["fill_cycles"] / max(d["items"], 1)))
+        print("   setup (costs, memory) %d cycles/item [costs %d, memory profiles %d], table fill %d cycles/item" % (
+            d["setup_cycles"] / max(d["items"], 1), d["cost_cycles"] / max(d["items"], 1),
+            d["mem_cycles"] / max(d["items"], 1), d["fill_cycles"] / max(d["items"], 1)))
+        print("   quick-path misses: x outside table %d, ties in E %d, E+1 outside table %d, ties in E+1 %d, "
+              "crossing pass beyond E+1 %d, rest overflows E+1 %d" % tuple(d[k] for k in (
+                  "q_range", "q_tieE", "q_range1", "q_tieE1", "q_twice", "q_rest")))
         tag = d["max_item_tag"]
         key = (tag >> 5) & 0x7FFFF
         print("   slowest item: %d cycles, kind %d P %d L %d, %d configs" % (
