@@ -42,10 +42,11 @@ constexpr int kTabBinadesGpt2 = 16;   // 3 task segments; from the binade below 
 constexpr int kTabBinadesMlp = 24;    // 3 forward + 4 backward task segments
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kCapacityBit = 1u << 5;   // DISTIR_R_CAPACITY
-constexpr int kTopkBlocks = 1024;   // max partial top-k blocks (<= 4 lists per merge thread)
-constexpr int kTopkThreads = 256;   // threads per partial top-k block
+constexpr int kTopkThreads = 256;   // threads of a block-wide top-k merge (k_topk_merge)
 constexpr int kMergeMaxLists = 4 * kTopkThreads;   // distir_topk_merge: 4 lists per thread
-constexpr int kTopkIPT = 2;         // candidates per thread held in registers
+constexpr int kPartLists = 8192;     // simulate blocks' partial top-k lists per launch
+constexpr int kSelectThreads = 256;  // k_topk_select: one block
+constexpr int kSelectCap = 1024;     // candidates it selects from in shared memory
 
 enum Mode : int32_t { MODE_GRID = 0, MODE_SYNTH = 1, MODE_EXPLICIT = 2 };
 
@@ -107,7 +108,7 @@ struct WsHeader {
   unsigned long long slow_tasks;      // lane-level slow-path entries (k_simulate)
   unsigned long long wave_steps;      // warp-level wavefront steps (k_simulate)
   unsigned int cfg_total;
-  unsigned int topk_ticket;           // partial top-k blocks done (last one merges)
+  unsigned long long topk_thresh;      // max over simulate blocks of their k-th throughput bits
 };
 
 struct Bucket {          // per hash slot (plus one overflow slot)
@@ -151,6 +152,19 @@ struct TopkRec {         // == distir_topk_entry
   double makespan;
   double throughput;
   int64_t peak;
+};
+
+// Row a7 inside the simulate kernels: each warp keeps a running top-k, each
+// block merges its warps' lists into part[blockIdx] (k records, count in
+// part_n) and, when that list is full, raises *thresh to its k-th key's
+// throughput bits; k_topk_select then picks the top k of the records at or
+// above the threshold (every global top-k record is: the block holding the
+// largest k-th throughput alone has k records at least that good).
+struct SimTopk {
+  int k;
+  TopkRec* part;        // this kernel's gridDim.x lists of k records
+  int* part_n;
+  unsigned long long* thresh;
 };
 
 }  // namespace distir

@@ -89,8 +89,8 @@ Layout layout(int64_t n_local, int64_t n_explicit) {
   L.pk = take(n * 8);
   L.rs = take(n * 4);
   L.tp = take(n * 8);
-  L.part = take((size_t)kTopkBlocks * kMaxK * sizeof(TopkRec));
-  L.part_n = take((size_t)kTopkBlocks * 4);
+  L.part = take((size_t)kPartLists * kMaxK * sizeof(TopkRec));
+  L.part_n = take((size_t)kPartLists * 4);
   L.gath = take((size_t)kMaxRanks * kMaxK * sizeof(TopkRec));
   L.fin = take((size_t)kMaxK * sizeof(TopkRec));
   L.fin_n = take(16);
@@ -176,7 +176,7 @@ struct distir_sim {
   size_t ev_used = 0;            // launches recorded in ev
   distir_profile_data acc{};     // totals folded in from ev
   int64_t kernels = 0, launches = 0;
-  GraphCache graph;
+  GraphCache graph[2];            // [0] plain, [1] with the profiling event nodes
   bool use_graph = true;
   // pinned host staging of the per-call small copies (spec H2D; top-k,
   // its count and the statistics header D2H), so they are true async DMA
@@ -193,11 +193,13 @@ struct distir_sim {
     if (pin) cudaFreeHost(pin);
     if (pin_ev) cudaEventDestroy(pin_ev);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
-    if (graph.exec) cudaGraphExecDestroy(graph.exec);
-    if (graph.graph) cudaGraphDestroy(graph.graph);
-    for (cudaEvent_t e : graph.ph)
-      if (e) cudaEventDestroy(e);
-    if (graph.cap) cudaStreamDestroy(graph.cap);
+    for (GraphCache& g : graph) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.graph) cudaGraphDestroy(g.graph);
+      for (cudaEvent_t e : g.ph)
+        if (e) cudaEventDestroy(e);
+      if (g.cap) cudaStreamDestroy(g.cap);
+    }
   }
 };
 
@@ -488,49 +490,58 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     kernels += 3;
   }
   CUDA_TRY(mark(1));
-  if (n > 0) {
-    const SimArgs sa{dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv};
-#define DISTIR_SIM(KD, MD) \
-  CUDA_TRY(sim_launch_##KD##_##MD(sim->sim_grid[KD * kModes + MD], sim_tpb(KD, MD), sim_smem(KD, MD), st, sa))
-#if DISTIR_SEQ_MAXP >= 1
-    DISTIR_SIM(0, 0); DISTIR_SIM(1, 0);
-    kernels += 2;
-#endif
-#if DISTIR_SEQ_MAXP >= 2
-    DISTIR_SIM(0, 1); DISTIR_SIM(1, 1);
-    kernels += 2;
-#endif
-#if DISTIR_SEQ_MAXP >= 3
-    DISTIR_SIM(0, 2); DISTIR_SIM(1, 2);
-    kernels += 2;
-#endif
-    // only the simulate kernels the grid can need (SpecBlock.f1b mask)
-    if (sp.f1b & gbit(0, 3)) { DISTIR_SIM(0, 3); kernels++; }
-    if (sp.f1b & gbit(0, 4)) { DISTIR_SIM(0, 4); kernels++; }
-    if (sp.f1b & gbit(0, 5)) { DISTIR_SIM(0, 5); kernels++; }
-    if (sp.f1b & gbit(0, 6)) { DISTIR_SIM(0, 6); kernels++; }
-    if (sp.f1b & gbit(0, 7)) { DISTIR_SIM(0, 7); kernels++; }
-    if (sp.f1b & gbit(1, 3)) { DISTIR_SIM(1, 3); kernels++; }
-    if (sp.f1b & gbit(1, 4)) { DISTIR_SIM(1, 4); kernels++; }
-#undef DISTIR_SIM
-  }
-  CUDA_TRY(mark(2));
   TopkRec* fin = at<TopkRec>(ws, L.fin);
   int* fin_n = at<int>(ws, L.fin_n);
   TopkRec* loc = comm ? fin : topk;   // local list (padded) when merging
   int* loc_n = comm ? fin_n : ntopk;
-  if (k > 0) {
-    TopkRec* part = at<TopkRec>(ws, L.part);
-    int* part_n = at<int>(ws, L.part_n);
-    if (n > 0) {
-      const int64_t per = (int64_t)kTopkThreads * kTopkIPT;
-      const int nblk = (int)std::min<int64_t>(kTopkBlocks, (n + per - 1) / per);
-      k_topk<<<nblk, kTopkThreads, 0, st>>>(dsp, ms, pk, rs, tpv, k, part, part_n, hdr, loc, loc_n);
-      kernels++;
-    } else {
-      enqueue_merge(st, part, part_n, 0, k, k, loc, loc_n);
-      kernels++;
+  TopkRec* part = at<TopkRec>(ws, L.part);
+  int* part_n = at<int>(ws, L.part_n);
+  // the simulate kernels the grid can need (SpecBlock.f1b mask, plus the
+  // program-order variants when built in); a7 runs inside them, the last one
+  // launched merging the per-kernel top-k lists
+  int groups[kGroups], ng = 0;
+  if (n > 0) {
+    for (int g = 0; g < kGroups; g++) {
+      const int md = g % kModes;
+      const bool seq = md < 3 && md < DISTIR_SEQ_MAXP && g / kModes <= 1;
+      if (seq || (md >= 3 && (sp.f1b & (1u << g)))) groups[ng++] = g;
     }
+  }
+  int n_lists = 0;                    // partial top-k lists (one per simulate block)
+  for (int i = 0; i < ng; i++) {
+    const int g = groups[i];
+    if (n_lists + sim->sim_grid[g] > kPartLists)
+      return fail(DISTIR_E_UNSUPPORTED, "simulate grids exceed the partial top-k lists");
+    SimArgs sa{dsp, dex, bk, items, perm, hdr, ms, pk, rs, tpv,
+               SimTopk{k, part + (int64_t)n_lists * (k > 0 ? k : 1), part_n + n_lists,
+                       &hdr->topk_thresh}};
+    n_lists += sim->sim_grid[g];
+    const int kd = g / kModes, md = g % kModes, grid = sim->sim_grid[g];
+    const int tpb = sim_tpb(kd, md), sm = sim_smem(kd, md);
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (g) {
+      case 0: e = sim_launch_0_0(grid, tpb, sm, st, sa); break;
+      case 1: e = sim_launch_0_1(grid, tpb, sm, st, sa); break;
+      case 2: e = sim_launch_0_2(grid, tpb, sm, st, sa); break;
+      case 3: e = sim_launch_0_3(grid, tpb, sm, st, sa); break;
+      case 4: e = sim_launch_0_4(grid, tpb, sm, st, sa); break;
+      case 5: e = sim_launch_0_5(grid, tpb, sm, st, sa); break;
+      case 6: e = sim_launch_0_6(grid, tpb, sm, st, sa); break;
+      case 7: e = sim_launch_0_7(grid, tpb, sm, st, sa); break;
+      case 8: e = sim_launch_1_0(grid, tpb, sm, st, sa); break;
+      case 9: e = sim_launch_1_1(grid, tpb, sm, st, sa); break;
+      case 10: e = sim_launch_1_2(grid, tpb, sm, st, sa); break;
+      case 11: e = sim_launch_1_3(grid, tpb, sm, st, sa); break;
+      case 12: e = sim_launch_1_4(grid, tpb, sm, st, sa); break;
+      default: break;
+    }
+    CUDA_TRY(e);
+    kernels++;
+  }
+  CUDA_TRY(mark(2));
+  if (k > 0) {                        // a7: the top k of the blocks' lists
+    k_topk_select<<<1, kSelectThreads, 0, st>>>(part, part_n, n_lists, k, hdr, loc, loc_n);
+    kernels++;
   }
   CUDA_TRY(mark(3));
   if (k > 0 && comm) {
@@ -559,7 +570,8 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
 distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* ms, int64_t* pk,
                          uint32_t* rs, TopkRec* topk, int* ntopk) {
   distir_status s;
-  GraphCache& G = sim->graph;
+  // without profiling, a graph with no event-record nodes at all
+  GraphCache& G = sim->graph[sim->prof ? 1 : 0];
   const bool key_ok = G.exec && G.ws == ws && G.ms == ms && G.pk == pk && G.rs == rs &&
                       G.topk == topk && G.ntopk == ntopk && G.k == k && G.comm == comm &&
                       (comm == nullptr || G.comm_gen == g_comm_gen.load()) &&
@@ -573,7 +585,8 @@ distir_status launch_all(distir_sim* sim, int k, void* comm, void* ws, double* m
       for (int j = 0; j < 5; j++) CUDA_TRY(cudaEventCreate(&G.ph[j]));
     CUDA_TRY(cudaStreamBeginCapture(G.cap, cudaStreamCaptureModeThreadLocal));
     int64_t kern = 0;
-    s = enqueue_all(sim, G.cap, G.ph, true, k, comm, ws, ms, pk, rs, topk, ntopk, &kern);
+    s = enqueue_all(sim, G.cap, sim->prof ? G.ph : nullptr, true, k, comm, ws, ms, pk, rs, topk,
+                    ntopk, &kern);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(G.cap, &g);
     if (s != DISTIR_OK) { if (g) cudaGraphDestroy(g); return s; }
@@ -791,7 +804,10 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   for (int g = 0; g < kGroups; g++) {
     int b = per_sm[g] > 0 ? per_sm[g] : 1;
     if (cap > 0 && b > cap) b = cap;
-    sim->sim_grid[g] = sim->num_sms * b;
+    // (one partial top-k list per block; kPartLists per launch)
+    const int gr = sim->num_sms * b;
+    const int lim = kPartLists / kGroups;
+    sim->sim_grid[g] = gr < lim ? gr : lim;
   }
   // work-item budget of k_plan's splitting, in resident warps of each
   // simulate kernel (DISTIR_PLAN_BUDGET_X scales it for experiments)

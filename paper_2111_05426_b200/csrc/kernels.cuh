@@ -537,150 +537,6 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
 
 #endif  // DISTIR_SIM_TU
 
-// Persistent simulate kernel for one group (model kind x stages per lane):
-// each warp pulls work items of its group, heaviest weight class first.
-__host__ __device__ constexpr int sim_v(int mode) {
-  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : (mode == 4 || mode == 7) ? 2 : 1;
-}
-__host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per lane row
-  return kind == 1 ? 19 + 6 * sim_v(mode) : mode == 6 ? 43 : 15 + 20 * sim_v(mode);
-}
-__host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per block
-  return sim_row(kind, mode) * 8 * 128 <= 48 * 1024 ? 128 : 64;
-}
-// Binade tables (exact_add.cuh BinTab) of the wavefront kernels: the first
-// kTabCfgs configurations of a warp (S >= 2 lanes each) get one, filled by
-// their lanes before the walk: binades x 2 parities x segments doubles.
-__host__ __device__ constexpr int sim_tab(int kind, int mode) {   // doubles per config
-  return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3
-                     : kTabBinadesMlp * 2 * (mode == 6 ? 9 : 7);
-}
-__host__ __device__ constexpr int sim_tab_cfgs(int kind) {     // configurations with a table
-  return kind == 1 ? kTabCfgsGpt2 : kTabCfgs;
-}
-__host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic smem bytes
-  return 8 * (sim_tpb(kind, mode) * sim_row(kind, mode) +
-              (sim_tpb(kind, mode) / 32) * sim_tab_cfgs(kind) * sim_tab(kind, mode));
-}
-
-#ifndef DISTIR_HOST_TU
-template <int KIND, int MODE>
-#ifndef DISTIR_SIM_MINB
-#define DISTIR_SIM_MINB 1      // min resident blocks per SM asked of ptxas (register cap)
-#endif
-__global__ void __launch_bounds__(sim_tpb(KIND, MODE), DISTIR_SIM_MINB) k_simulate(const SpecBlock* __restrict__ spp,
-                                                  const DExplicit* __restrict__ ex,
-                                                  const Bucket* __restrict__ bk,
-                                                  const Item* __restrict__ items,
-                                                  const PCfg* __restrict__ perm,
-                                                  WsHeader* __restrict__ hdr,
-                                                  double* __restrict__ ms_out,
-                                                  int64_t* __restrict__ pk_out,
-                                                  uint32_t* __restrict__ rs_out,
-                                                  double* __restrict__ tp_out) {
-  constexpr int G = KIND * kModes + MODE;
-  constexpr bool SEQ = MODE < 3;
-  constexpr int V = sim_v(MODE);
-  const SpecBlock& sp = *spp;
-  const int lane = threadIdx.x & 31;
-  const unsigned int first = hdr->group_begin[G], end = hdr->group_begin[G + 1];
-  // Warp w starts on item first + w (no atomic; heaviest items go to the
-  // first warps), then pulls items past the grid's warp count from a queue.
-  const unsigned int n_warps = gridDim.x * (blockDim.x >> 5);
-  const unsigned int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  bool first_item = true;
-  // per-lane rows (op costs, then per-slot task-cache increments), then
-  // the warps' binade tables
-  constexpr int ROW = sim_row(KIND, MODE);
-  constexpr int TAB = sim_tab(KIND, MODE);
-  extern __shared__ double s_dyn[];
-  double* row = s_dyn + threadIdx.x * ROW;
-  double* wtab = s_dyn + sim_tpb(KIND, MODE) * ROW + (threadIdx.x >> 5) * sim_tab_cfgs(KIND) * TAB;
-  unsigned long long feas = 0;
-  WorkCount wc{0u, 0u};
-  while (true) {
-    unsigned int id;
-    if (first_item) {
-      id = first + gw;
-      first_item = false;
-    } else {
-      id = 0;
-      if (lane == 0) id = first + n_warps + atomicAdd(&hdr->item_counter[G], 1u);
-      id = __shfl_sync(0xffffffffu, id, 0);
-    }
-    if (id >= end) break;
-    const Item it = items[id];
-    const int S = 1 << it.lg_lanes;
-    const int seg = lane / S, sl = lane - seg * S;
-    const bool has = seg < it.n;
-    const PCfg pc = has ? perm[it.first + seg] : PCfg{1, 0u, 1, 1, 0, 0, 0, 0, 0};
-    const uint32_t q = pc.q;
-    Cfg c;
-    if (has && pc.model == kSynthModel) {
-      decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);     // arithmetic only
-    } else if (has) {
-      c.M = sp.models[pc.model];
-      c.mi = pc.model;
-      c.topo = pc.topo;
-      c.D = 1ll << pc.lgD; c.T = 1ll << pc.lgT; c.P = pc.P; c.K = pc.K; c.B = pc.B;
-    } else {
-      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0};
-      c.topo = 0; c.mi = 0; c.D = c.T = c.P = c.K = c.B = 1;
-    }
-    const DTopo& tp = sp.topos[c.topo];
-    double* tab = (TAB > 0 && S >= 2 && seg < sim_tab_cfgs(KIND)) ? wtab + seg * TAB : nullptr;
-    double ms;
-    int64_t pk;
-#ifdef DISTIR_INSTR
-    const long long t0 = clock64();
-#endif
-    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
-    else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
-    else if (warp_max_int(has ? c.M.rc : 0))          // bucket key: warp-uniform
-      run_mlp<V, SEQ, MODE == 5 || MODE == 7, true>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
-    else
-      run_mlp<V, SEQ, MODE == 5 || MODE == 7, false>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
-#ifdef DISTIR_INSTR
-    if (lane == 0) {
-      const unsigned long long dt = (unsigned long long)(clock64() - t0);
-      atomicAdd(&g_distir_instr[5], dt);
-      atomicAdd(&g_distir_instr[7], 1ull);
-      atomicMax(&g_distir_instr[8], dt);
-      // slowest item: cycles and its bucket key / configs (for probe_instr)
-      atomicMax(&g_distir_instr[11], (dt << 24) | ((unsigned long long)(bk[it.bucket].key & 0x7FFFF) << 5) |
-                                         (unsigned long long)(it.n & 31));
-    }
-#endif
-    // makespan and peak: max over the stages of the segment
-    for (int o = S >> 1; o > 0; o >>= 1) {
-      ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-      const int64_t po = __shfl_xor_sync(0xffffffffu, pk, o);
-      pk = pk > po ? pk : po;
-    }
-    if (has && sl == 0) {
-      const uint32_t r = pk > tp.capacity ? kCapacityBit : 0u;
-      ms_out[q] = ms;
-      pk_out[q] = pk;
-      rs_out[q] = r;
-      tp_out[q] = r ? 0.0 : __ddiv_rn(__ll2double_rn(c.B), ms);
-      feas += r == 0;
-    }
-  }
-  unsigned long long slow = wc.slow;
-  for (int o = 16; o > 0; o >>= 1) {
-    feas += __shfl_xor_sync(0xffffffffu, feas, o);
-    slow += __shfl_xor_sync(0xffffffffu, slow, o);
-  }
-  if (lane == 0) {
-    if (feas) atomicAdd(&hdr->n_feasible, feas);
-    if (slow) atomicAdd(&hdr->slow_tasks, slow);
-    if (wc.steps) atomicAdd(&hdr->wave_steps, (unsigned long long)wc.steps);
-  }
-}
-
-#endif  // DISTIR_HOST_TU
-
-#ifndef DISTIR_SIM_TU
 // ------------------------------------------------------------ top-k ---------
 // The C.8 total order -- throughput desc, peak asc, index asc -- as an
 // unsigned lexicographic key (larger = better): a = bits of the throughput
@@ -735,10 +591,10 @@ __device__ __forceinline__ int warp_best_lane(const Key& k) {
 // and offers the best of their heads; k rounds of a block-wide best (warp
 // winners in shared memory, then warp 0); the owner of the winner advances.
 // Pads `out` to k.
-static __device__ void merge_lists(const TopkRec* __restrict__ lists, const int* __restrict__ list_n,
+template <int kLPT = 4>                                        // lists per thread
+__device__ void merge_lists(const TopkRec* __restrict__ lists, const int* __restrict__ list_n,
                             int n_lists, int k_in, int k, TopkRec* __restrict__ out,
                             int* __restrict__ out_n) {
-  constexpr int kLPT = 4;                                      // lists per thread
   __shared__ Key s_w[32];
   __shared__ int s_win;                                        // winning thread, -1 none
   const int t = threadIdx.x, w = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
@@ -801,88 +657,314 @@ static __device__ void merge_lists(const TopkRec* __restrict__ lists, const int*
   if (t == 0) *out_n = got;
 }
 
-// Partial top-k of the shard, then the merge.  Block b takes chunks b, b +
-// gridDim, ... of kTopkThreads * kTopkIPT candidates; per chunk each thread
-// holds kTopkIPT candidates sorted in registers, each warp extracts its top
-// k by rounds of warp-best over the lanes' heads (the winning lane pops its
-// head; rounds stop when the warp runs out), and warp 0 merges the per-warp
-// lists with the best-so-far list carried from the previous chunk.  Each
-// block writes one sorted list; the last block to finish (ticket) merges
-// all of them.
-__global__ void __launch_bounds__(kTopkThreads) k_topk(
-    const SpecBlock* __restrict__ spp, const double* __restrict__ ms,
-    const int64_t* __restrict__ pk, const uint32_t* __restrict__ rs,
-    const double* __restrict__ tpv, int k, TopkRec* __restrict__ part, int* __restrict__ part_n,
-    WsHeader* __restrict__ hdr, TopkRec* __restrict__ out, int* __restrict__ out_n) {
-  constexpr int NW = kTopkThreads / 32;
-  static_assert(NW + 1 <= 32, "warp 0 merges the warps' lists and the carried list");
-  __shared__ Key s_cand[NW][kMaxK];
-  __shared__ int s_cnt[NW];
-  __shared__ Key s_acc[2][kMaxK];
-  __shared__ int s_acc_n;
-  __shared__ bool s_last;
+
+// Running top-k of one warp of a simulate kernel (row a7 fused into the
+// simulate kernels): a list L of up to k keys in shared memory, best first
+// by the C.8 order, its count in a warp-uniform register.  A candidate that
+// beats the k-th is inserted by one parallel shift (lane i moves entries i
+// and i + 32).  Warp-uniform call.
+__device__ __forceinline__ void topk_insert(Key* __restrict__ L, int& cnt, int k, const Key& kc) {
+  const int lane = threadIdx.x & 31;
+  if (cnt == k && !better(kc, L[k - 1])) return;
+  const bool b0 = lane < cnt && better(L[lane], kc);
+  const bool b1 = lane + 32 < cnt && better(L[lane + 32], kc);
+  const int pos = __popc(__ballot_sync(0xffffffffu, b0)) + __popc(__ballot_sync(0xffffffffu, b1));
+  const Key e0 = lane < cnt ? L[lane] : no_key();
+  const Key e1 = lane + 32 < cnt ? L[lane + 32] : no_key();
+  __syncwarp();
+  if (lane >= pos && lane < cnt && lane + 1 < k) L[lane + 1] = e0;
+  if (lane + 32 >= pos && lane + 32 < cnt && lane + 33 < k) L[lane + 33] = e1;
+  __syncwarp();
+  if (lane == 0) L[pos] = kc;
+  __syncwarp();
+  cnt = cnt < k ? cnt + 1 : k;
+}
+__device__ __forceinline__ Key shfl_key(const Key& x, int src) {
+  Key r;
+  r.a = __shfl_sync(0xffffffffu, x.a, src);
+  r.b = __shfl_sync(0xffffffffu, x.b, src);
+  r.c = __shfl_sync(0xffffffffu, x.c, src);
+  r.ms = __shfl_sync(0xffffffffu, x.ms, src);
+  return r;
+}
+
+// Persistent simulate kernel for one group (model kind x stages per lane):
+// each warp pulls work items of its group, heaviest weight class first.
+__host__ __device__ constexpr int sim_v(int mode) {
+  return mode == 0 ? 1 : mode == 1 ? 2 : mode == 2 ? 4 : (mode == 4 || mode == 7) ? 2 : 1;
+}
+__host__ __device__ constexpr int sim_row(int kind, int mode) {   // doubles per lane row
+  return kind == 1 ? 19 + 6 * sim_v(mode) : mode == 6 ? 43 : 15 + 20 * sim_v(mode);
+}
+__host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per block
+  return sim_row(kind, mode) * 8 * 128 <= 48 * 1024 ? 128 : 64;
+}
+// Binade tables (exact_add.cuh BinTab) of the wavefront kernels: the first
+// kTabCfgs configurations of a warp (S >= 2 lanes each) get one, filled by
+// their lanes before the walk: binades x 2 parities x segments doubles.
+__host__ __device__ constexpr int sim_tab(int kind, int mode) {   // doubles per config
+  return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3
+                     : kTabBinadesMlp * 2 * (mode == 6 ? 9 : 7);
+}
+__host__ __device__ constexpr int sim_tab_cfgs(int kind) {     // configurations with a table
+  return kind == 1 ? kTabCfgsGpt2 : kTabCfgs;
+}
+__host__ __device__ constexpr int sim_smem(int kind, int mode) {  // dynamic smem bytes
+  return 8 * (sim_tpb(kind, mode) * sim_row(kind, mode) +
+              (sim_tpb(kind, mode) / 32) * sim_tab_cfgs(kind) * sim_tab(kind, mode)) +
+         (sim_tpb(kind, mode) / 32) * kMaxK * 32;       // the warps' running top-k lists
+}
+
+#ifndef DISTIR_HOST_TU
+template <int KIND, int MODE>
+#ifndef DISTIR_SIM_MINB
+#define DISTIR_SIM_MINB 1      // min resident blocks per SM asked of ptxas (register cap)
+#endif
+__global__ void __launch_bounds__(sim_tpb(KIND, MODE), DISTIR_SIM_MINB) k_simulate(const SpecBlock* __restrict__ spp,
+                                                  const DExplicit* __restrict__ ex,
+                                                  const Bucket* __restrict__ bk,
+                                                  const Item* __restrict__ items,
+                                                  const PCfg* __restrict__ perm,
+                                                  WsHeader* __restrict__ hdr,
+                                                  double* __restrict__ ms_out,
+                                                  int64_t* __restrict__ pk_out,
+                                                  uint32_t* __restrict__ rs_out,
+                                                  double* __restrict__ tp_out,
+                                                  const SimTopk tk) {
+  constexpr int G = KIND * kModes + MODE;
+  constexpr bool SEQ = MODE < 3;
+  constexpr int V = sim_v(MODE);
   const SpecBlock& sp = *spp;
-  const int64_t n = sp.n_local;
-  const int64_t rank = sp.rank, nr = sp.n_ranks;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int64_t per = (int64_t)kTopkThreads * kTopkIPT;
-  int cur = 0;
-  if (threadIdx.x == 0) s_acc_n = 0;
-  __syncthreads();
-  for (int64_t c = blockIdx.x; c * per < n; c += gridDim.x) {
-    Key it[kTopkIPT];
-#pragma unroll
-    for (int i = 0; i < kTopkIPT; i++) {
-      const int64_t q = c * per + threadIdx.x + (int64_t)i * kTopkThreads;
-      // the four loads are independent (one memory round trip), selected after
-      const bool in = q < n;
-      const uint32_t rq = in ? rs[q] : 1u;
-      const double tq = in ? tpv[q] : 0.0, mq = in ? ms[q] : 0.0;
-      const int64_t pq = in ? pk[q] : 0;
-      it[i] = rq == 0 ? make_key(tq, pq, rank + q * nr, mq) : no_key();
+  const int lane = threadIdx.x & 31;
+  const unsigned int first = hdr->group_begin[G], end = hdr->group_begin[G + 1];
+  // Warp w starts on item first + w (no atomic; heaviest items go to the
+  // first warps), then pulls items past the grid's warp count from a queue.
+  const unsigned int n_warps = gridDim.x * (blockDim.x >> 5);
+  const unsigned int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  bool first_item = true;
+  // per-lane rows (op costs, then per-slot task-cache increments), then
+  // the warps' binade tables
+  constexpr int ROW = sim_row(KIND, MODE);
+  constexpr int TAB = sim_tab(KIND, MODE);
+  extern __shared__ double s_dyn[];
+  double* row = s_dyn + threadIdx.x * ROW;
+  double* wtab = s_dyn + sim_tpb(KIND, MODE) * ROW + (threadIdx.x >> 5) * sim_tab_cfgs(KIND) * TAB;
+  // this warp's running top-k (after every warp's tables)
+  Key* wlist = reinterpret_cast<Key*>(s_dyn + sim_tpb(KIND, MODE) * ROW +
+                                      (sim_tpb(KIND, MODE) / 32) * sim_tab_cfgs(KIND) * TAB) +
+               (threadIdx.x >> 5) * kMaxK;
+  int wcnt = 0;
+  const int k = tk.k;
+  unsigned long long feas = 0;
+  WorkCount wc{0u, 0u};
+  while (true) {
+    unsigned int id;
+    if (first_item) {
+      id = first + gw;
+      first_item = false;
+    } else {
+      id = 0;
+      if (lane == 0) id = first + n_warps + atomicAdd(&hdr->item_counter[G], 1u);
+      id = __shfl_sync(0xffffffffu, id, 0);
     }
-    static_assert(kTopkIPT == 2, "one compare-exchange sorts a thread's candidates");
-    cswap(it[0], it[1]);
-    int head = 0, got = 0;
+    if (id >= end) break;
+    const Item it = items[id];
+    const int S = 1 << it.lg_lanes;
+    const int seg = lane / S, sl = lane - seg * S;
+    const bool has = seg < it.n;
+    const PCfg pc = has ? perm[it.first + seg] : PCfg{1, 0u, 1, 1, 0, 0, 0, 0, 0};
+    const uint32_t q = pc.q;
+    Cfg c;
+    if (has && pc.model == kSynthModel) {
+      decode(sp, ex, sp.rank + (int64_t)q * sp.n_ranks, c);     // arithmetic only
+    } else if (has) {
+      c.M = sp.models[pc.model];
+      c.mi = pc.model;
+      c.topo = pc.topo;
+      c.D = 1ll << pc.lgD; c.T = 1ll << pc.lgT; c.P = pc.P; c.K = pc.K; c.B = pc.B;
+    } else {
+      c.M = DModel{KIND, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0};
+      c.topo = 0; c.mi = 0; c.D = c.T = c.P = c.K = c.B = 1;
+    }
+    const DTopo& tp = sp.topos[c.topo];
+    double* tab = (TAB > 0 && S >= 2 && seg < sim_tab_cfgs(KIND)) ? wtab + seg * TAB : nullptr;
+    double ms;
+    int64_t pk;
+#ifdef DISTIR_INSTR
+    const long long t0 = clock64();
+#endif
+    if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+    else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+    else if (warp_max_int(has ? c.M.rc : 0))          // bucket key: warp-uniform
+      run_mlp<V, SEQ, MODE == 5 || MODE == 7, true>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+    else
+      run_mlp<V, SEQ, MODE == 5 || MODE == 7, false>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+#ifdef DISTIR_INSTR
+    if (lane == 0) {
+      const unsigned long long dt = (unsigned long long)(clock64() - t0);
+      atomicAdd(&g_distir_instr[5], dt);
+      atomicAdd(&g_distir_instr[7], 1ull);
+      atomicMax(&g_distir_instr[8], dt);
+      // slowest item: cycles and its bucket key / configs (for probe_instr)
+      atomicMax(&g_distir_instr[11], (dt << 24) | ((unsigned long long)(bk[it.bucket].key & 0x7FFFF) << 5) |
+                                         (unsigned long long)(it.n & 31));
+    }
+#endif
+    // makespan and peak: max over the stages of the segment
+    for (int o = S >> 1; o > 0; o >>= 1) {
+      ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+      const int64_t po = __shfl_xor_sync(0xffffffffu, pk, o);
+      pk = pk > po ? pk : po;
+    }
+    bool cand = false;
+    Key mine = no_key();
+    if (has && sl == 0) {
+      const uint32_t r = pk > tp.capacity ? kCapacityBit : 0u;
+      const double thr = r ? 0.0 : __ddiv_rn(__ll2double_rn(c.B), ms);
+      ms_out[q] = ms;
+      pk_out[q] = pk;
+      rs_out[q] = r;
+      tp_out[q] = thr;
+      feas += r == 0;
+      cand = r == 0;
+      if (cand) mine = make_key(thr, pk, sp.rank + (int64_t)q * sp.n_ranks, ms);
+    }
+    // a7: the feasible configurations of this item join the warp's top-k
+    if (k > 0) {
+      for (unsigned m = __ballot_sync(0xffffffffu, cand); m; m &= m - 1)
+        topk_insert(wlist, wcnt, k, shfl_key(mine, __ffs(m) - 1));
+    }
+  }
+  unsigned long long slow = wc.slow;
+  for (int o = 16; o > 0; o >>= 1) {
+    feas += __shfl_xor_sync(0xffffffffu, feas, o);
+    slow += __shfl_xor_sync(0xffffffffu, slow, o);
+  }
+  if (lane == 0) {
+    if (feas) atomicAdd(&hdr->n_feasible, feas);
+    if (slow) atomicAdd(&hdr->slow_tasks, slow);
+    if (wc.steps) atomicAdd(&hdr->wave_steps, (unsigned long long)wc.steps);
+  }
+  if (k <= 0) return;
+  // ---- a7: warp 0 merges the block's warp lists into part[blockIdx.x] and,
+  // when the merged list is full, raises the threshold to its k-th key
+  constexpr int NW = sim_tpb(KIND, MODE) / 32;
+  __shared__ int s_wcnt[NW];
+  if (lane == 0) s_wcnt[threadIdx.x >> 5] = wcnt;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const Key* base = reinterpret_cast<const Key*>(s_dyn + sim_tpb(KIND, MODE) * ROW +
+                                                   NW * sim_tab_cfgs(KIND) * TAB);
+    const int cnt = lane < NW ? s_wcnt[lane] : 0;
+    int ptr = 0, o = 0;
+    uint64_t kth_a = 0;
+    TopkRec* dst = tk.part + (int64_t)blockIdx.x * k;
     for (int r = 0; r < k; r++) {
-      const Key mine = head == 0 ? it[0] : (head == 1 ? it[1] : no_key());
-      const int wl = warp_best_lane(mine);
+      const Key h = ptr < cnt ? base[lane * kMaxK + ptr] : no_key();
+      const int wl = warp_best_lane(h);
       if (wl < 0) break;
-      if (lane == wl) { s_cand[w][r] = mine; head++; }
+      if (lane == wl) { dst[r] = key_rec(h); ptr++; }
+      kth_a = __shfl_sync(0xffffffffu, h.a, wl < 0 ? 0 : wl);
+      o++;
+    }
+    if (lane == 0) {
+      tk.part_n[blockIdx.x] = o;
+      if (o == k) atomicMax(tk.thresh, (unsigned long long)kth_a);
+    }
+  }
+}
+
+#endif  // DISTIR_HOST_TU
+
+#ifndef DISTIR_SIM_TU
+// Block-wide best of one key per thread (C.8 order): the index of the
+// winning thread, or -1 when no thread holds a candidate.  Whole block.
+__device__ __forceinline__ int block_best_thread(const Key& mine) {
+  __shared__ Key s_bw[32];
+  __shared__ int s_bt[32];
+  __shared__ int s_win;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int wl = warp_best_lane(mine);
+  const Key wk = shfl_key(mine, wl < 0 ? 0 : wl);
+  if (lane == 0) {
+    s_bw[w] = wl < 0 ? no_key() : wk;
+    s_bt[w] = wl < 0 ? -1 : w * 32 + wl;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int b = warp_best_lane(lane < nw ? s_bw[lane] : no_key());
+    if (lane == 0) s_win = b < 0 ? -1 : s_bt[b];
+  }
+  __syncthreads();
+  const int r = s_win;
+  __syncthreads();                                   // s_bw / s_bt / s_win reused next call
+  return r;
+}
+
+// a7, final step: the top k of the simulate blocks' partial lists (SimTopk).
+// Records below the threshold cannot be in the top k; the survivors (at most
+// kSelectCap) are selected in shared memory by k rounds of a block-wide best.
+// With more survivors (mass ties at the threshold) every list head is
+// rescanned each round instead.  One block of kSelectThreads.
+__global__ void __launch_bounds__(kSelectThreads) k_topk_select(
+    const TopkRec* __restrict__ part, const int* __restrict__ part_n, int n_lists, int k,
+    const WsHeader* __restrict__ hdr, TopkRec* __restrict__ out, int* __restrict__ out_n) {
+  __shared__ Key s_c[kSelectCap];
+  __shared__ int s_n;
+  const int t = threadIdx.x;
+  const uint64_t T = *(volatile const unsigned long long*)&hdr->topk_thresh;
+  if (t == 0) s_n = 0;
+  __syncthreads();
+  for (int l = t; l < n_lists; l += blockDim.x) {      // lists are sorted: stop below T
+    const int cnt = part_n[l];
+    for (int r = 0; r < cnt; r++) {
+      const TopkRec x = part[(int64_t)l * k + r];
+      const Key kk = make_key(x.throughput, x.peak, x.index, x.makespan);
+      if (kk.a < T) break;
+      const int pos = atomicAdd(&s_n, 1);
+      if (pos < kSelectCap) s_c[pos] = kk;
+    }
+  }
+  __syncthreads();
+  const int n = s_n;
+  int got = 0;
+  if (n <= kSelectCap) {
+    constexpr int C = kSelectCap / kSelectThreads;
+    static_assert(C == 4, "a four-key sorting network per thread");
+    Key c[C];
+#pragma unroll
+    for (int j = 0; j < C; j++) c[j] = t + j * kSelectThreads < n ? s_c[t + j * kSelectThreads] : no_key();
+    cswap(c[0], c[1]); cswap(c[2], c[3]); cswap(c[0], c[2]); cswap(c[1], c[3]); cswap(c[1], c[2]);
+    int head = 0;
+    for (int r = 0; r < k; r++) {
+      const Key mine = head == 0 ? c[0] : head == 1 ? c[1] : head == 2 ? c[2] : head == 3 ? c[3] : no_key();
+      const int win = block_best_thread(mine);
+      if (win < 0) break;
+      if (t == win) { out[r] = key_rec(mine); head++; }
       got++;
     }
-    if (lane == 0) s_cnt[w] = got;
+  } else {
+    __shared__ unsigned char s_ptr[kPartLists];
+    for (int l = t; l < n_lists; l += blockDim.x) s_ptr[l] = 0;
     __syncthreads();
-    if (w == 0) {
-      const int acc_n = s_acc_n;
-      const int cnt = lane < NW ? s_cnt[lane] : (lane == NW ? acc_n : 0);
-      int ptr = 0, o = 0;
-      for (int r = 0; r < k; r++) {
-        Key mine = no_key();
-        if (ptr < cnt) mine = lane < NW ? s_cand[lane][ptr] : s_acc[cur][ptr];
-        const int wl = warp_best_lane(mine);
-        if (wl < 0) break;
-        if (lane == wl) { s_acc[cur ^ 1][r] = mine; ptr++; }
-        o++;
+    for (int r = 0; r < k; r++) {
+      Key best = no_key();
+      int bl = -1;
+      for (int l = t; l < n_lists; l += blockDim.x) {
+        if (s_ptr[l] >= part_n[l]) continue;
+        const TopkRec x = part[(int64_t)l * k + s_ptr[l]];
+        const Key kk = make_key(x.throughput, x.peak, x.index, x.makespan);
+        if (better(kk, best)) { best = kk; bl = l; }
       }
-      __syncwarp();                    // every lane has read s_acc_n
-      if (lane == 0) s_acc_n = o;
+      const int win = block_best_thread(best);
+      if (win < 0) break;
+      if (t == win) { out[r] = key_rec(best); s_ptr[bl]++; }
+      got++;
+      __syncthreads();
     }
-    cur ^= 1;
-    __syncthreads();
   }
-  const int got = s_acc_n;
-  TopkRec* o = part + (int64_t)blockIdx.x * k;
-  for (int r = threadIdx.x; r < got; r += blockDim.x) o[r] = key_rec(s_acc[cur][r]);
-  if (threadIdx.x == 0) part_n[blockIdx.x] = got;
-  // last block merges (threadfence reduction)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&hdr->topk_ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  merge_lists(part, part_n, gridDim.x, k, k, out, out_n);
+  for (int r = got + t; r < k; r += blockDim.x) out[r] = TopkRec{-1, 0.0, -1.0, -1};
+  if (t == 0) *out_n = got;
 }
 
 // Merge of gathered per-rank lists (and the empty-shard case).

@@ -16,7 +16,7 @@ namespace distir {
 cudaError_t DISTIR_CAT(sim_launch_, SIM_KIND, SIM_MODE)(int grid, int tpb, int smem,
                                                           cudaStream_t st, const SimArgs& a) {
   k_simulate<SIM_KIND, SIM_MODE><<<grid, tpb, smem, st>>>(a.sp, a.ex, a.bk, a.items, a.perm, a.hdr,
-                                                          a.ms, a.pk, a.rs, a.tp);
+                                                          a.ms, a.pk, a.rs, a.tp, a.topk);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,7 @@ struct SimArgs {
   int64_t* pk;
   uint32_t* rs;
   double* tp;
+  SimTopk topk;
 };
 
 #define DISTIR_SIM_DECL(KD, MD)                                                    \

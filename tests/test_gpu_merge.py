@@ -122,7 +122,7 @@ def test_device_merge_tie_breaks(G):
         assert any(ref["peak"][i] == ref["peak"][i + 1] for i in eq), "index tie-break exercised"
         lists, counts = shard_lists(s, G, min(k, 64), configs=cfgs)
         assert_same(merged(s, lists, counts, min(k, 64)), ref)
-        # the single-launch top-k (k_topk) agrees as well
+        # the single-launch top-k (simulate kernels + k_topk_select) agrees as well
         res = s.eval(configs=cfgs, k=min(k, 64))
         assert res["topk"]["index"].tolist() == ref["index"].tolist()
     finally:
@@ -189,3 +189,24 @@ def test_nccl_one_rank_in_timed_loop(sim):
                 assert_same(rec, ref)
         finally:
             pkg.distir_nccl_comm_destroy(comm)
+
+
+def test_topk_mass_ties_select_fallback():
+    """Thousands of identical configurations (equal throughput and peak:
+    only the index orders them) spread over many simulate blocks: more
+    candidates tie at the selection threshold than k_topk_select holds in
+    shared memory, so it takes its list-rescanning path; the result must still
+    be the oracle's (C.8: index ascending among equals)."""
+    from paper_2111_05426_b200 import Simulator
+    models = {"a": W.mlp(2, 64), "b": W.mlp(2, 128)}
+    topos = {"TB200": W.TOPOLOGIES["TB200"]}
+    cfgs = [(0, 0, 1, 1, 1, 1, 64)] * 6000 + [(1, 0, 1, 1, 1, 1, 64)] * 7
+    cfgs[4321] = (0, 0, 2, 1, 1, 1, 64)            # one different config inside
+    s = Simulator(models, topos, device=0)
+    try:
+        res = s.eval(configs=cfgs, k=64)
+        ref = oracle_topk_configs(models, topos, cfgs, 64)
+        assert res["topk"]["index"].tolist() == ref["index"].tolist()
+        assert (res["topk"]["throughput"] == ref["throughput"]).all()
+    finally:
+        s.close()
