@@ -452,19 +452,27 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, 
     atomicAdd(&s_nb, 1u);
   }
   __syncthreads();
-  if (threadIdx.x < kGroups) {         // split heavy classes while warps are idle
-    const int g = threadIdx.x;
-    unsigned int total = 0;
-    for (int c = 0; c < kNumClasses; c++) total += s_alt[g][c][0];
-    for (int c = kNumClasses - 1; c >= 0 && total > 0; c--) {
-      int j = 0;
-      if (s_alt[g][c][0] == 0) { s_shift[g][c] = 0; continue; }       // empty class
-      while (j < kMaxSplit && total - s_alt[g][c][j] + s_alt[g][c][j + 1] <= budget.warps[g]) {
-        total = total - s_alt[g][c][j] + s_alt[g][c][j + 1];
-        j++;
+  static_assert(kNumClasses <= 64 && kGroups <= kPlanThreads / 32, "one warp per group, 2 classes per lane");
+  const int pw = threadIdx.x >> 5, pl = threadIdx.x & 31;
+  if (pw < kGroups) {                  // split heavy classes while warps are idle
+    const int g = pw;                  // (warp g; lane 0 walks the non-empty classes)
+    const unsigned a0 = pl < kNumClasses ? s_alt[g][pl][0] : 0u;
+    const unsigned a1 = pl + 32 < kNumClasses ? s_alt[g][pl + 32][0] : 0u;
+    unsigned int total = __reduce_add_sync(0xffffffffu, a0 + a1);
+    unsigned long long ne = (unsigned long long)__ballot_sync(0xffffffffu, a0 != 0u) |
+                            ((unsigned long long)__ballot_sync(0xffffffffu, a1 != 0u) << 32);
+    if (pl == 0) {
+      while (ne && total > 0) {        // heaviest non-empty class first
+        const int c = 63 - __clzll(ne);
+        ne &= ~(1ull << c);
+        int j = 0;
+        while (j < kMaxSplit && total - s_alt[g][c][j] + s_alt[g][c][j + 1] <= budget.warps[g]) {
+          total = total - s_alt[g][c][j] + s_alt[g][c][j + 1];
+          j++;
+        }
+        s_shift[g][c] = (unsigned char)j;
+        if (j < kMaxSplit && s_alt[g][c][j] != s_alt[g][c][j + 1]) break;   // budget reached
       }
-      s_shift[g][c] = (unsigned char)j;
-      if (j < kMaxSplit && s_alt[g][c][j] != s_alt[g][c][j + 1]) break;   // budget reached
     }
   }
   __syncthreads();
@@ -481,11 +489,20 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, 
   // item numbering: group-major, heaviest class first (per-group prefix by
   // one thread per group, then the group offsets)
   __shared__ unsigned int s_gsum[kGroups];
-  if (threadIdx.x < kGroups) {
-    const int g = threadIdx.x;
-    unsigned int base = 0;
-    for (int c = kNumClasses - 1; c >= 0; c--) { s_base[g][c] = base; base += s_items[g][c]; }
-    s_gsum[g] = base;
+  if (pw < kGroups) {                  // exclusive prefix over classes, heaviest first
+    const int g = pw;
+    const int ch = 63 - pl, cl = 31 - pl;        // lanes hold classes 63..32, then 31..0
+    const unsigned vh = ch < kNumClasses ? s_items[g][ch] : 0u;
+    const unsigned vl = cl < kNumClasses ? s_items[g][cl] : 0u;
+    unsigned sh = vh, sl2 = vl;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned xh = __shfl_up_sync(0xffffffffu, sh, o), xl = __shfl_up_sync(0xffffffffu, sl2, o);
+      if (pl >= o) { sh += xh; sl2 += xl; }
+    }
+    const unsigned tot_h = __shfl_sync(0xffffffffu, sh, 31), tot_l = __shfl_sync(0xffffffffu, sl2, 31);
+    if (ch < kNumClasses) s_base[g][ch] = sh - vh;
+    if (cl < kNumClasses) s_base[g][cl] = tot_h + sl2 - vl;
+    if (pl == 0) s_gsum[g] = tot_h + tot_l;
   }
   __syncthreads();
   if (threadIdx.x < kGroups) {
@@ -915,20 +932,42 @@ __global__ void __launch_bounds__(kSelectThreads) k_topk_select(
   const uint64_t T = *(volatile const unsigned long long*)&hdr->topk_thresh;
   if (t == 0) s_n = 0;
   __syncthreads();
-  for (int l = t; l < n_lists; l += blockDim.x) {      // lists are sorted: stop below T
-    const int cnt = part_n[l];
-    for (int r = 0; r < cnt; r++) {
-      const TopkRec x = part[(int64_t)l * k + r];
-      const Key kk = make_key(x.throughput, x.peak, x.index, x.makespan);
-      if (kk.a < T) break;
-      const int pos = atomicAdd(&s_n, 1);
-      if (pos < kSelectCap) s_c[pos] = kk;
-    }
+  // every (list, record) pair at once: independent loads, no chains
+  const int64_t pairs = (int64_t)n_lists * k;
+  for (int64_t pq = t; pq < pairs; pq += blockDim.x) {
+    const int l = (int)(pq / k), r = (int)(pq - (int64_t)l * k);
+    if (r >= part_n[l]) continue;
+    const TopkRec x = part[pq];
+    const Key kk = make_key(x.throughput, x.peak, x.index, x.makespan);
+    if (kk.a < T) continue;
+    const int pos = atomicAdd(&s_n, 1);
+    if (pos < kSelectCap) s_c[pos] = kk;
   }
   __syncthreads();
   const int n = s_n;
   int got = 0;
-  if (n <= kSelectCap) {
+  if (n <= 4 * 32) {
+    // few survivors (the usual case): warp 0 alone, no block barriers
+    if (t < 32) {
+      Key c[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) c[j] = t + 32 * j < n ? s_c[t + 32 * j] : no_key();
+      cswap(c[0], c[1]); cswap(c[2], c[3]); cswap(c[0], c[2]); cswap(c[1], c[3]); cswap(c[1], c[2]);
+      int head = 0;
+      for (int r = 0; r < k; r++) {
+        const Key mine = head == 0 ? c[0] : head == 1 ? c[1] : head == 2 ? c[2] : head == 3 ? c[3] : no_key();
+        const int wl = warp_best_lane(mine);
+        if (wl < 0) break;
+        if (t == wl) { out[r] = key_rec(mine); head++; }
+        got++;
+      }
+    }
+    got = __shfl_sync(0xffffffffu, got, 0);      // (warp 0; other warps only pad)
+    __shared__ int s_got;
+    if (t == 0) s_got = got;
+    __syncthreads();
+    got = s_got;
+  } else if (n <= kSelectCap) {
     constexpr int C = kSelectCap / kSelectThreads;
     static_assert(C == 4, "a four-key sorting network per thread");
     Key c[C];
