@@ -314,7 +314,6 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     if (!is_pow2(g->world[i]) || (i && g->world[i] <= g->world[i - 1]))
       return fail(DISTIR_E_INVALID_ARG, "spec.world: ascending powers of two");
     if (g->world[i] > kMaxWorld) return fail(DISTIR_E_UNSUPPORTED, "world size > 64");
-    if (any_zero && g->world[i] > 32) return fail(DISTIR_E_UNSUPPORTED, "ZeRO with world size > 32");
   }
   for (int i = 0; i < g->n_batch; i++) {
     if (g->batch[i] < 1 || (i && g->batch[i] <= g->batch[i - 1]))
@@ -361,6 +360,10 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
         const int nK = (g->k_mode == 0 && c == 0) ? 1 : g->n_k;
         if (nK == 0) continue;
         if (ne >= kMaxEntries) return fail(DISTIR_E_UNSUPPORTED, "too many (D,T,P) triples");
+        // ZeRO's kernel holds one (stage, replica) per lane: D > 1 needs
+        // next_pow2(P) * D = 2^(a + c) <= 32 (D = 1 runs the plain kernels)
+        if (any_zero && a > 0 && a + c > 5)
+          return fail(DISTIR_E_UNSUPPORTED, "ZeRO needs next_pow2(pp) * dp <= 32");
         sp.entries[ne] = DEntry{1 << a, 1 << b, 1 << c, nK, cum};
         cum += (int64_t)nK * g->n_batch;
         ne++;

@@ -661,6 +661,119 @@ DISTIR_HD int task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bin
   return 1;
 }
 
+// The same straight-line slow path for a task of NS segments read through a
+// segment map (the MLP kernels' forward / backward tasks): (i) a stale cache
+// -- the whole task fits x's binade E; (ii) one crossing -- the segments and
+// passes that fit E in closed form, the pass that leaves E op by op, the rest
+// of the task in closed form in E + 1.  No ties in the lists it uses (else
+// 2, add_task handles them), the table covering E (and E + 1); 0 in every
+// other case; x untouched unless 1.
+template <int NS>
+DISTIR_HD int taskN_quick(double& x, const Seg (&sg)[NS], TaskCache& c, const BinTab& t,
+                          const int (&map)[NS]) {
+  const int64_t xb = d2bits(x);
+  const int32_t ef = (int32_t)((xb >> 52) & 0x7FF);
+  const int32_t b = ef - t.e0;
+  if (!(x > 0.0) || b < 0 || b >= t.nb || ef > 1992) return 0;
+  const int64_t* r0 = t.tab + (int64_t)b * t.nu * 2;
+  auto sat = [](int64_t v) { return v > kTwo53 ? kTwo53 : v; };
+  int64_t R[NS];
+  int64_t tot = 0;
+  bool tie = false;
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    const int64_t a0 = r0[2 * map[i]], a1 = r0[2 * map[i] + 1];
+    R[i] = a0;
+    if (sg[i].reps > 0) {
+      tie |= a0 != a1 || a0 >= kNeverI;
+      tot = sat(tot + sat(sg[i].reps * (a0 < kNeverI ? a0 : kTwo53)));
+    }
+  }
+  if (tie) return 2;
+  const int64_t M = (xb & kMant) | kHidden, avail = kTwo53 - 1 - M;
+  if (tot <= avail) {                                   // (i) the task fits E
+    x = bits2d(((int64_t)ef << 52) | ((M + tot) & kMant));
+#pragma unroll
+    for (int i = 0; i < NS; i++) { c.R[2 * i] = R[i]; c.R[2 * i + 1] = R[i]; }
+    c.ef = ef;
+    c.lo = ef << 20;
+    c.hi = (ef + 1) << 20;
+    c.Su0 = c.Su1 = xmul((double)tot, bits2d((int64_t)(ef - 52) << 52));
+    return 1;
+  }
+  if (b + 1 >= t.nb) return 0;
+  const int64_t* r1 = r0 + t.nu * 2;
+  int64_t R1[NS];
+  int64_t tot1 = 0;
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    const int64_t a0 = r1[2 * map[i]], a1 = r1[2 * map[i] + 1];
+    R1[i] = a0;
+    if (sg[i].reps > 0) {
+      tie |= a0 != a1 || a0 >= kNeverI;
+      tot1 = sat(tot1 + sat(sg[i].reps * (a0 < kNeverI ? a0 : kTwo53)));
+    }
+  }
+  if (tie) return 2;
+  // the segment j that leaves E, the passes of it that still fit
+  int64_t pre = 0, rest = 0, fitj = 0;
+  int j = -1;
+  const double* aj = nullptr;
+  int naj = 0;
+#pragma unroll
+  for (int i = 0; i < NS; i++) {
+    if (sg[i].reps <= 0) continue;
+    if (j < 0) {
+      const int64_t need = sat(sg[i].reps * R[i]);
+      if (pre + need <= avail) { pre += need; continue; }
+      const int64_t room = avail - pre;
+      int64_t fit = R[i] > 0 ? (int64_t)fdiv_approx((float)room, (float)R[i]) : sg[i].reps - 1;
+      fit = fit < 0 ? 0 : (fit > sg[i].reps - 1 ? sg[i].reps - 1 : fit);
+      if (fit * R[i] > room) fit--;
+      if (fit + 1 < sg[i].reps && (fit + 1) * R[i] <= room) fit++;
+      j = i;
+      fitj = fit;
+      pre += fit * R[i];
+      aj = sg[i].a;
+      naj = sg[i].n;
+      rest = sat((sg[i].reps - fit - 1) * R1[i]);
+    } else {
+      rest = sat(rest + sat(sg[i].reps * R1[i]));
+    }
+  }
+  (void)fitj;
+  if (j < 0) return 0;
+  double y = bits2d(((int64_t)ef << 52) | ((M + pre) & kMant));   // exact, in E
+  {
+    double v[kSegMax];
+#pragma unroll
+    for (int q = 0; q < kSegMax; q++) v[q] = q < naj ? aj[q] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kSegMax; q++)
+      if (q < naj) y = xadd(y, v[q]);
+  }
+  const int64_t yb = d2bits(y);
+  if ((int32_t)((yb >> 52) & 0x7FF) != ef + 1) return 0;
+  const int64_t M1 = (yb & kMant) | kHidden;
+  if (M1 + rest > kTwo53 - 1) return 0;
+  x = bits2d(((int64_t)(ef + 1) << 52) | ((M1 + rest) & kMant));
+#pragma unroll
+  for (int i = 0; i < NS; i++) { c.R[2 * i] = R1[i]; c.R[2 * i + 1] = R1[i]; }
+  c.ef = ef + 1;
+  c.lo = (ef + 1) << 20;
+  c.hi = (ef + 2) << 20;
+  c.Su0 = c.Su1 = tot1 < kTwo53 ? xmul((double)tot1, bits2d((int64_t)(ef + 1 - 52) << 52)) : kInf();
+  return 1;
+}
+
+// Any task walked op by op (short tasks: cheaper than any table lookup).
+template <int NS>
+DISTIR_HD void taskN_plain(double& x, const Seg (&sg)[NS]) {
+#pragma unroll
+  for (int i = 0; i < NS; i++)
+    for (int64_t r = 0; r < sg[i].reps; r++) seq_plain(x, sg[i].a, sg[i].n);
+}
+
 // A three-segment task (as task3_quick) walked op by op -- for a clock at
 // zero (stage 0's first task), where the sum climbs through many binades:
 // the repeated segment's costs are held in registers.

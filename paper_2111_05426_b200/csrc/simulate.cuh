@@ -61,6 +61,20 @@ __device__ __forceinline__ int64_t* i64(double* p) { return reinterpret_cast<int
 #endif
 constexpr int kPlainBlocks = DISTIR_PLAIN_BLOCKS;   // GPT-2: walk tasks of <= 12 blocks op by op
                                                     // when the quick path cannot take them
+#ifndef DISTIR_QUICKN
+#define DISTIR_QUICKN 1     // MLP: straight-line stale-cache / single-crossing slow path
+#endif
+#ifndef DISTIR_PLAIN_MLP
+#define DISTIR_PLAIN_MLP 32
+#endif
+// MLP configurations walked op by op throughout (no table, no cached
+// increments): layers per stage x K <= DISTIR_PLAIN_MLP x configurations per
+// warp.  A plain walk costs every lane ~4 adds per layer per task, in
+// lock step; the cached fast path costs ~1 add per task plus ~20 binade
+// crossings per configuration, which the configurations of a warp take one
+// after another (divergent) -- so warps of many short configurations walk
+// plainly (W5 2.4x faster), warps of few long ones keep the fast path.
+constexpr int kPlainMlp = DISTIR_PLAIN_MLP;
 #ifndef DISTIR_TIES
 #define DISTIR_TIES 0       // GPT-2 tasks of > kPlainBlocks blocks with ties: closed forms
 #endif                      // (task3_quick_ties) instead of add_task; measured equal on W3 (r02j), off
@@ -218,6 +232,14 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     if constexpr (RC) alt_segs(row, 0, 3, lo[q] & 1, nl > 1 ? nl - 1 : 0, sg[1], sg[2], sg[3]);
     alt_segs(row, 6, 4, (hi[q] - 1) & 1, nl, sg[NB - 3], sg[NB - 2], sg[NB - 1]);
   };
+  bool plain_cfg;
+  {
+    int nlm = 0;
+#pragma unroll
+    for (int q = 0; q < V; q++) nlm = ok[q] && hi[q] - lo[q] > nlm ? hi[q] - lo[q] : nlm;
+    for (int o = S >> 1; o > 0; o >>= 1) nlm = max(nlm, __shfl_xor_sync(0xffffffffu, nlm, o));
+    plain_cfg = (int64_t)nlm * warp_max_int(has ? (int)K : 0) <= (int64_t)kPlainMlp * (32 / S);
+  }
   BinTab btf{nullptr, 0, 0, 0};
   if constexpr (!SEQ) {
     // binade table of the 7 distinct op lists (forward b / ab / a,
@@ -233,7 +255,20 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       const double w = (double)(hi[q] - lo[q]) * (rc ? 2.0 : 1.0) * lay + row[14] + sendf[q] + sendb[q];
       work = fmax(work, w * (double)K);
     }
-    btf = bintab_range(has ? tab : nullptr, kTabBinadesMlp, 7, cmin, work, P, S);
+    // every task but stage 0's first starts at or after stage 0's first
+    // forward task, which is at least its layers x the lighter layer's
+    // forward ops: the table starts one binade below that (GPT-2 likewise)
+    {
+      double t0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < V; q++)
+        if (ok[q] && s[q] == 0)
+          t0 = __dmul_rn(__dmul_rn((double)(hi[q] - lo[q]),
+                                   fmin(row[0] + row[1] + row[2], row[3] + row[4] + row[5])), 0.5);
+      for (int o = S >> 1; o > 0; o >>= 1) t0 = fmax(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+      if (t0 > cmin && t0 < kInf()) cmin = t0;
+    }
+    btf = bintab_range(has && !plain_cfg ? tab : nullptr, kTabBinadesMlp, 7, cmin, work, P, S);
     Seg f[3], g[NB], u[7];
     fsegs(0, f);
     bsegs(0, g);
@@ -242,47 +277,48 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     bintab_fill(btf, u, sl, S);
     __syncwarp();
   }
+  // slow paths: the straight-line quick path (taskN_quick), else add_task
+  // (configurations with short tasks and few microbatches are walked op by
+  // op throughout -- plain_cfg, no binade table)
+  auto fwd_slow = [&](int q) {
+    Seg sg[3];
+    fsegs(q, sg);
+    if (plain_cfg) { taskN_plain(clk[q], sg); return; }
+    if (DISTIR_QUICKN && clk[q] > 0.0 && taskN_quick(clk[q], sg, cf[q], btf, kMapId3) == 1) return;
+    add_task(clk[q], sg, cf[q], btf, kMapId3, DISTIR_PLAIN_AFTER_MLP);
+  };
+  auto bwd_slow = [&](int q) {
+    Seg sg[NB];
+    bsegs(q, sg);
+    if (plain_cfg) { taskN_plain(clk[q], sg); return; }
+    if constexpr (RC) {
+      if (DISTIR_QUICKN && taskN_quick(clk[q], sg, cb[q], btf, kMapMlpBwd) == 1) return;
+      add_task(clk[q], sg, cb[q], btf, kMapMlpBwd, DISTIR_PLAIN_AFTER_MLP);
+    } else {
+      if (DISTIR_QUICKN && taskN_quick(clk[q], sg, cb[q], btf, kMapMlpBwd4) == 1) return;
+      add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4, DISTIR_PLAIN_AFTER_MLP);
+    }
+  };
   auto fwd_task = [&](int q, bool act) {
-    if constexpr (SEQ || F1B) {
+    if constexpr (SEQ) {
       if (act) mem_apply(live[q], peak[q], pf[q]);
     }
     const bool slow = task_fast_or_slow(clk[q], cf[q], act);
     wc.slow += slow;
     DISTIR_SLOW_T0
     const bool any = DISTIR_ANY(slow);
-    if (any) {
-      Seg sg[3];
-      fsegs(q, sg);
-      // the single-crossing path only when every slow lane qualifies (else
-      // add_task runs anyway and would pay for both)
-      bool s2 = slow;
-      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], cf[q], btf)))
-        s2 = slow && !task_cross1(clk[q], sg, cf[q], btf, kMapId3);
-      if (DISTIR_ANY(s2) && s2) add_task(clk[q], sg, cf[q], btf, kMapId3, DISTIR_PLAIN_AFTER_MLP);
-    }
+    if (any && slow) fwd_slow(q);
     DISTIR_SLOW_T1(any)
   };
   auto bwd_task = [&](int q, bool act) {
-    if constexpr (SEQ || F1B) {
+    if constexpr (SEQ) {
       if (act) mem_apply(live[q], peak[q], pb[q]);
     }
     const bool slow = task_fast_or_slow(clk[q], cb[q], act);
     wc.slow += slow;
     DISTIR_SLOW_T0
     const bool any = DISTIR_ANY(slow);
-    if (any) {
-      Seg sg[NB];
-      bsegs(q, sg);
-      bool s2 = slow;
-      if (DISTIR_CROSS1 && __all_sync(0xffffffffu, !slow || cross1_eligible(clk[q], cb[q], btf))) {
-        if constexpr (RC) s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd);
-        else s2 = slow && !task_cross1(clk[q], sg, cb[q], btf, kMapMlpBwd4);
-      }
-      if (DISTIR_ANY(s2) && s2) {
-        if constexpr (RC) add_task(clk[q], sg, cb[q], btf, kMapMlpBwd, DISTIR_PLAIN_AFTER_MLP);
-        else add_task(clk[q], sg, cb[q], btf, kMapMlpBwd4, DISTIR_PLAIN_AFTER_MLP);
-      }
-    }
+    if (any && slow) bwd_slow(q);
     DISTIR_SLOW_T1(any)
   };
   if constexpr (F1B) {
@@ -290,139 +326,93 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     // ---- synchronous 1F1B (NEXT row f1).  Stage s's ops are the
     // PipeDream-flush sequence (w = min(P-1-s, K) warm-up forwards, then
     // F(w+i), B(i) pairs, then the remaining backwards) interleaved with its
-    // Sends in the order of the unit-time schedule (DESIGN reading R6): in
-    // that schedule F(k, s) starts at s + k (k <= w) or 2k + s, B(k, s) at
-    // 2P - 1 - s + 2k, and a Send happens when its producer finishes; Sends
-    // precede tasks at equal times, then by lower stage, forward first.  The
-    // warp co-simulates the stages (lane = stage; with V = 2, 32 < P <= 64,
-    // a lane holds stages sl and sl + 32): a stage whose next event is a task
-    // runs it; a Send runs when both ends have it next (rendezvous).
-    // This is exactly the per-device order of the oracle's program.
+    // Sends in the order of the unit-time schedule (DESIGN reading R6): F(k,
+    // s) in slot s + k (k <= w) or 2k + s, B(k, s) in slot 2P - 1 - s + 2k; a
+    // Send in the slot after its producer; in a slot, Sends before the task,
+    // by lower stage of the pair, forward before backward.
+    //
+    // Slot wavefront: stage s runs its slot-t events at steps 3t + s + j:
+    // [j = 0] the Sends on the link to s-1 (forward receive, then gradient
+    // send), [1] the Sends on the link to s+1 (forward send, then gradient
+    // receive), [2] the task.  The two ends of a link run its Sends at the
+    // same step (stage s's j = 1 is stage s+1's j = 0); after the first Send
+    // of a link both ends hold the same clock, so the second is one add.
+    // Each stage runs its events in its program order and its slot blocks do
+    // not overlap (3 steps per slot), so every op's end time is the
+    // program-order walk's (Theorem 1); chains of Sends across stages within
+    // a slot (warm-up, cool-down) pipeline along the skew.  Memory follows
+    // the events in program order (C.7).
     const int Pi = (int)P, Ki = (int)K;
-    auto fstart = [&](int k, int ss) {
-      const int ww = Pi - 1 - ss < Ki ? Pi - 1 - ss : Ki;
-      return k <= ww ? ss + k : 2 * k + ss;
-    };
-    // event key: ((t * 2 + cls) * 64 + lower) * 2 + kind; cls 0 = Send
-    auto key = [](int t, int cls, int lower, int kind) -> int64_t {
-      return (((int64_t)t * 2 + cls) * 64 + lower) * 2 + kind;
-    };
-    constexpr int64_t kDone = INT64_MAX;
-#ifndef DISTIR_F1B_TASKS
-#define DISTIR_F1B_TASKS 2
-#endif
-    constexpr int kF1bTasks = DISTIR_F1B_TASKS;
-#ifndef DISTIR_F1B_SENDS
-#define DISTIR_F1B_SENDS 1   // send rounds per 1F1B iteration (A/B: 2 is -6% on W2, +4% on W4)
-#endif
-    constexpr int kF1bSends = DISTIR_F1B_SENDS;
-    int wu[V], jt[V], ka_in[V], ka_out[V], kg_out[V], kg_in[V], n_tasks[V];
+    int wu[V], wd[V];                              // w of this stage and of s-1
 #pragma unroll
     for (int q = 0; q < V; q++) {
       wu[q] = Pi - 1 - s[q] < Ki ? Pi - 1 - s[q] : Ki;
-      jt[q] = ka_in[q] = ka_out[q] = kg_out[q] = kg_in[q] = 0;
-      n_tasks[q] = ok[q] ? 2 * Ki : 0;
+      wd[q] = Pi - s[q] < Ki ? Pi - s[q] : Ki;
     }
-    // every iteration runs >= 1 event of each configuration (its globally
-    // first one); the guard only bounds a broken schedule
-    const int max_iter = warp_max_int(has ? 4 * Pi * Ki + 64 : 0);
-    // next event of stage slot q's five streams (task, recv act, send act,
-    // send grad, recv grad), by the unit-time keys
-    auto next_event = [&](int q, int& which, int& tkind) {
-      const int st = s[q];
-      int64_t best = kDone;
-      int tk = 0;
-      which = -1;
-      tkind = 0;
-      if (jt[q] < n_tasks[q]) {
-        const int w = wu[q];
-        if (jt[q] < w) { tkind = 0; tk = jt[q]; }
-        else if (jt[q] < 2 * Ki - w) { const int jj = jt[q] - w; tkind = jj & 1; tk = (jj >> 1) + (tkind ? 0 : w); }
-        else { tkind = 1; tk = jt[q] - Ki; }
-        const int t = tkind ? 2 * Pi - 1 - st + 2 * tk : fstart(tk, st);
-        best = key(t, 1, st, tkind);
-        which = 0;
-      }
-      if (ok[q] && st > 0 && ka_in[q] < Ki) {
-        const int64_t k2 = key(fstart(ka_in[q], st - 1) + 1, 0, st - 1, 0);
-        if (k2 < best) { best = k2; which = 1; }
-      }
-      if (ok[q] && st < Pi - 1 && ka_out[q] < Ki) {
-        const int64_t k2 = key(fstart(ka_out[q], st) + 1, 0, st, 0);
-        if (k2 < best) { best = k2; which = 2; }
-      }
-      if (ok[q] && st > 0 && kg_out[q] < Ki) {
-        const int64_t k2 = key(2 * Pi - st + 2 * kg_out[q], 0, st - 1, 1);
-        if (k2 < best) { best = k2; which = 3; }
-      }
-      if (ok[q] && st < Pi - 1 && kg_in[q] < Ki) {
-        const int64_t k2 = key(2 * Pi - (st + 1) + 2 * kg_in[q], 0, st, 1);
-        if (k2 < best) { best = k2; which = 4; }
-      }
+    // is there a forward / backward task of stage ss in slot t
+    auto has_f = [&](int t, int ss, int w) -> bool {
+      const int dd = t - ss;
+      if (dd < 0) return false;
+      if (dd <= w) return dd < Ki;
+      return (dd & 1) == 0 && (dd >> 1) > w && (dd >> 1) < Ki;
     };
-    for (int iter = 0; iter < max_iter; iter++) {
+    auto has_b = [&](int t, int ss) -> bool {
+      const int dd = t - (2 * Pi - 1 - ss);
+      return dd >= 0 && (dd & 1) == 0 && (dd >> 1) < Ki;
+    };
+    // the last task is B(K-1, 0) in slot 2P + 2K - 3, at step 3 (2P + 2K - 3) + 2
+    const int nsteps = warp_max_int(has ? 3 * (2 * Pi + 2 * Ki - 3) + 3 : 0);
+    int u[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) u[q] = -s[q];     // step - s
+    for (int step = 0; step < nsteps; step++) {
       wc.steps++;
-      int which[V], tkind[V];
-#pragma unroll
-      for (int q = 0; q < V; q++) next_event(q, which[q], tkind[q]);
-      // tasks need no partner: a stage runs up to kF1bTasks consecutive
-      // tasks before the send round (its per-device order is unchanged)
-      for (int r = 0; r < kF1bTasks; r++) {
-        bool anyt = false;
-#pragma unroll
-        for (int q = 0; q < V; q++) anyt |= which[q] == 0;
-        if (!__any_sync(0xffffffffu, anyt)) break;
-#pragma unroll
-        for (int q = 0; q < V; q++) {
-          fwd_task(q, which[q] == 0 && tkind[q] == 0);
-          bwd_task(q, which[q] == 0 && tkind[q] == 1);
-          if (which[q] == 0) { jt[q]++; next_event(q, which[q], tkind[q]); }
-        }
-      }
-      bool anye = false;
-#pragma unroll
-      for (int q = 0; q < V; q++) anye |= which[q] >= 0;
-      if (!__any_sync(0xffffffffu, anye)) break;
-      // up to kF1bSends send rounds: a stage whose send completed moves on to
-      // its next event, which may be another send of the same time slot
-      for (int sr = 0; sr < kF1bSends; sr++) {
-      if (sr > 0) {
-        bool anys = false;
-#pragma unroll
-        for (int q = 0; q < V; q++) anys |= which[q] > 0;
-        if (!__any_sync(0xffffffffu, anys)) break;
-      }
-      // rendezvous identity (lower stage, direction, microbatch); -1 = none
-      double my_id[V], up_id[V], dn_id[V], up_c[V], dn_c[V];
+      bool e1[V], e2[V], dn[V], tf[V], tb[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
+        const int uq = u[q]++;
+        const int t = uq >= 0 ? uq / 3 : -1, j = uq - 3 * t;
         const int st = s[q];
-        my_id[q] = which[q] == 1 ? (double)((st - 1) << 14 | ka_in[q])
-                 : which[q] == 2 ? (double)(st << 14 | ka_out[q])
-                 : which[q] == 3 ? (double)((st - 1) << 14 | 1 << 13 | kg_out[q])
-                 : which[q] == 4 ? (double)(st << 14 | 1 << 13 | kg_in[q]) : -1.0;
-      }
-      Nbr<V>::up_stage(my_id, up_id, lane);
-      Nbr<V>::down_stage(my_id, dn_id, lane);
-      Nbr<V>::up_stage(clk, up_c, lane);
-      Nbr<V>::down_stage(clk, dn_c, lane);
-#pragma unroll
-      for (int q = 0; q < V; q++) {
-        const int st = s[q];
-        const bool down_link = which[q] == 1 || which[q] == 3;      // partner s - 1
-        const bool ready = which[q] > 0 && (down_link ? (st > 0 && dn_id[q] == my_id[q])
-                                                      : (st < Pi - 1 && up_id[q] == my_id[q]));
-        if (ready) {
-          const double other = down_link ? dn_c[q] : up_c[q];
-          clk[q] = dadd(fmax(clk[q], other), down_link ? sendb[q] : sendf[q]);
-          if (which[q] == 1) { MEM(q, m * kin[lo[q] & 1] * e, 0); ka_in[q]++; }        // recv act
-          else if (which[q] == 2) { ka_out[q]++; }                                    // send act
-          else if (which[q] == 3) { live[q] -= m * kin[lo[q] & 1] * e; kg_out[q]++; } // send grad
-          else { MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0); kg_in[q]++; }              // recv grad
-          next_event(q, which[q], tkind[q]);
+        const bool lo_ok = ok[q] && st > 0 && t >= 0, hi_ok = ok[q] && st < Pi - 1 && t >= 0;
+        dn[q] = j == 0;
+        // the link's forward Send, then its gradient Send (slot t - 1 producers)
+        e1[q] = j == 0 ? (lo_ok && has_f(t - 1, st - 1, wd[q])) : (j == 1 && hi_ok && has_f(t - 1, st, wu[q]));
+        e2[q] = j == 0 ? (lo_ok && has_b(t - 1, st)) : (j == 1 && hi_ok && has_b(t - 1, st + 1));
+        tf[q] = j == 2 && ok[q] && t >= 0 && has_f(t, st, wu[q]);
+        tb[q] = j == 2 && ok[q] && t >= 0 && has_b(t, st);
+        // the task: one fast path on the forward or backward cache
+        if (tf[q]) mem_apply(live[q], peak[q], pf[q]);
+        if (tb[q]) mem_apply(live[q], peak[q], pb[q]);
+        const bool act = tf[q] || tb[q];
+        const double x = clk[q];
+        const double Su = (loword(x) & 1) ? (tb[q] ? cb[q].Su1 : cf[q].Su1) : (tb[q] ? cb[q].Su0 : cf[q].Su0);
+        const double y = xadd(x, Su);
+        const bool fast = act && hiword(y) < (tb[q] ? cb[q].hi : cf[q].hi);
+        clk[q] = fast ? y : x;
+        const bool slow = act && !fast;
+        wc.slow += slow;
+        if (slow) {
+          if (tb[q]) bwd_slow(q);
+          else fwd_slow(q);
         }
       }
-      }   // send rounds
+      double nbu[V], nbd[V];
+      Nbr<V>::up_stage(clk, nbu, lane);
+      Nbr<V>::down_stage(clk, nbd, lane);
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        if (!(e1[q] || e2[q])) continue;
+        const double o = dn[q] ? nbd[q] : nbu[q];
+        const double c1 = dn[q] ? sendb[q] : sendf[q];
+        clk[q] = dadd(fmax(clk[q], o), c1);        // the link's first Send
+        if (e1[q] && e2[q]) clk[q] = dadd(clk[q], c1);   // both ends now equal: max is the clock
+        if (dn[q]) {
+          if (e1[q]) MEM(q, m * kin[lo[q] & 1] * e, 0);            // received activation
+          if (e2[q]) live[q] -= m * kin[lo[q] & 1] * e;            // sent gradient dies
+        } else if (e2[q]) {
+          MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);                // received gradient
+        }
+      }
     }
   } else if constexpr (SEQ) {
     // ---- program order (one lane owns all P <= V stages)

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <random>
 static long g_cnt[32];
+static long g_quickN_ok = 0;
 #define DISTIR_COUNT(i) (g_cnt[i]++)
 #include "../../paper_2111_05426_b200/csrc/exact_add.cuh"
 
@@ -58,9 +59,16 @@ static long check(std::mt19937_64& g, int trials, int mode) {
       for (int i = 0; i < NS; i++)
         for (int64_t r = 0; r < sg[i].reps; r++)
           for (int j = 0; j < sg[i].n; j++) x = x + sg[i].a[j];
-      // as the kernels do: fast path, else the single-crossing path, else add_task
-      if ((g() & 1) || !task_fast(y, c))
-        if (!(g() & 3) || !task_cross1(y, sg, c, tb, map)) add_task(y, sg, c, tb, map, (int)(g() % 3));
+      // as the kernels do: fast path, else the straight-line quick path
+      // (or the single-crossing path), else add_task
+      if ((g() & 1) || !task_fast(y, c)) {
+        if (g() & 1) {
+          if (taskN_quick(y, sg, c, tb, map) == 1) g_quickN_ok++;
+          else add_task(y, sg, c, tb, map, (int)(g() % 3));
+        } else if (!(g() & 3) || !task_cross1(y, sg, c, tb, map)) {
+          add_task(y, sg, c, tb, map, (int)(g() % 3));
+        }
+      }
       if (std::memcmp(&x, &y, 8) != 0) {
         if (bad < 5) std::printf("mismatch NS=%d mode=%d task=%d plain=%a agg=%a\n", NS, mode, k, x, y);
         bad++;
@@ -155,7 +163,7 @@ int main(int argc, char** argv) {
     bad += check_gpt2(g, 2 * trials, mode);
   }
   bad += check_mem(g, trials * 5);
-  std::printf("task3_quick_ties: %ld taken\n", g_ties_ok);
+  std::printf("task3_quick_ties: %ld taken, taskN_quick: %ld taken\n", g_ties_ok, g_quickN_ok);
   std::printf("task3_quick: %ld taken; misses: outside table %ld, never-fitting lists %ld / %ld, "
               "crossing beyond E+1 %ld, rest beyond E+1 %ld\n", g_quick_ok, g_cnt[21], g_cnt[22],
               g_cnt[24], g_cnt[25], g_cnt[26]);

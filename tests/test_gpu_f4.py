@@ -99,7 +99,8 @@ def test_checkpointing_lowers_gpu_peaks(sim):
 
 def test_zero_unsupported_shapes():
     """ZeRO under 1F1B and ZeRO configurations needing more than 32 lanes
-    are rejected with DISTIR_E_UNSUPPORTED (include/distir.h)."""
+    (next_pow2(P) * D > 32 with D > 1) are rejected with DISTIR_E_UNSUPPORTED
+    (include/distir.h)."""
     from paper_2111_05426_b200 import DistirError, Simulator
     with pytest.raises(DistirError) as e:
         Simulator({"z": W.mlp(4, 64, zero=1, schedule=1)}, {"t": W.TOPOLOGIES["TB200"]}, device=0)
@@ -108,7 +109,15 @@ def test_zero_unsupported_shapes():
     with pytest.raises(DistirError) as e:
         s.eval(configs=[(0, 0, 4, 1, 16, 2, 64)], k=1)
     assert e.value.status == 2
+    # a grid is rejected only when one of its (D, T, P) needs > 32 lanes
     with pytest.raises(DistirError) as e:
-        s.eval(W.grid_with("W4", models=["z"], topos=["t"]), k=1)
+        s.eval(W.grid_with("W4", models=["z"], topos=["t"], dp_mask=W.ALL), k=1)
     assert e.value.status == 2
     s.close()
+
+
+def test_w4_zero_model_runs(sim):
+    """The W4 grid (P up to 64, D = 1) of a ZeRO model: D = 1 configurations
+    run on the plain kernels (ZeRO partitions over replicas only), against
+    the oracle on the whole grid."""
+    assert full_grid_check(sim, W.grid_with("W4", models=["mlp_w4_zero"])) == 1.0

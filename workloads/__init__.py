@@ -84,6 +84,8 @@ MODELS = {
     "gpt2_1_6b": gpt2(24, 2048, 16),
     "gpt2_13b": gpt2(40, 5120, 40),
     "gpt2_175b": gpt2(96, 12288, 96),
+    # W4 under ZeRO (D = 1 on W4: the plain kernels; P up to 64)
+    "mlp_w4_zero": mlp(64, 8192, zero=1),
 }
 
 HF_GPT2 = ["gpt2_small", "gpt2_medium", "gpt2_large", "gpt2_xl"]
