@@ -349,16 +349,15 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       wu[q] = Pi - 1 - s[q] < Ki ? Pi - 1 - s[q] : Ki;
       wd[q] = Pi - s[q] < Ki ? Pi - s[q] : Ki;
     }
-    // is there a forward / backward task of stage ss in slot t
+    // is there a forward / backward task of stage ss in slot t (branch-free:
+    // the lanes of a warp are at different sub-steps of their slots)
     auto has_f = [&](int t, int ss, int w) -> bool {
-      const int dd = t - ss;
-      if (dd < 0) return false;
-      if (dd <= w) return dd < Ki;
-      return (dd & 1) == 0 && (dd >> 1) > w && (dd >> 1) < Ki;
+      const int dd = t - ss, h = dd >> 1;
+      return (dd >= 0) & (((dd <= w) & (dd < Ki)) | (((dd & 1) == 0) & (h > w) & (h < Ki)));
     };
     auto has_b = [&](int t, int ss) -> bool {
       const int dd = t - (2 * Pi - 1 - ss);
-      return dd >= 0 && (dd & 1) == 0 && (dd >> 1) < Ki;
+      return (dd >= 0) & ((dd & 1) == 0) & ((dd >> 1) < Ki);
     };
     // the last task is B(K-1, 0) in slot 2P + 2K - 3, at step 3 (2P + 2K - 3) + 2
     const int nsteps = warp_max_int(has ? 3 * (2 * Pi + 2 * Ki - 3) + 3 : 0);
@@ -380,10 +379,15 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         e2[q] = j == 0 ? (lo_ok && has_b(t - 1, st)) : (j == 1 && hi_ok && has_b(t - 1, st + 1));
         tf[q] = j == 2 && ok[q] && t >= 0 && has_f(t, st, wu[q]);
         tb[q] = j == 2 && ok[q] && t >= 0 && has_b(t, st);
-        // the task: one fast path on the forward or backward cache
-        if (tf[q]) mem_apply(live[q], peak[q], pf[q]);
-        if (tb[q]) mem_apply(live[q], peak[q], pb[q]);
+        // the task: its memory profile, then one fast path on the forward or
+        // backward cache (predicated)
         const bool act = tf[q] || tb[q];
+        {
+          const int64_t mp = tb[q] ? pb[q].mp : pf[q].mp, net = tb[q] ? pb[q].net : pf[q].net;
+          const int64_t hi_m = live[q] + mp;
+          peak[q] = (act && hi_m > peak[q]) ? hi_m : peak[q];
+          live[q] += act ? net : 0;
+        }
         const double x = clk[q];
         const double Su = (loword(x) & 1) ? (tb[q] ? cb[q].Su1 : cf[q].Su1) : (tb[q] ? cb[q].Su0 : cf[q].Su0);
         const double y = xadd(x, Su);
@@ -400,18 +404,19 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       Nbr<V>::up_stage(clk, nbu, lane);
       Nbr<V>::down_stage(clk, nbd, lane);
 #pragma unroll
-      for (int q = 0; q < V; q++) {
-        if (!(e1[q] || e2[q])) continue;
+      for (int q = 0; q < V; q++) {                // predicated, no branches
         const double o = dn[q] ? nbd[q] : nbu[q];
         const double c1 = dn[q] ? sendb[q] : sendf[q];
-        clk[q] = dadd(fmax(clk[q], o), c1);        // the link's first Send
-        if (e1[q] && e2[q]) clk[q] = dadd(clk[q], c1);   // both ends now equal: max is the clock
-        if (dn[q]) {
-          if (e1[q]) MEM(q, m * kin[lo[q] & 1] * e, 0);            // received activation
-          if (e2[q]) live[q] -= m * kin[lo[q] & 1] * e;            // sent gradient dies
-        } else if (e2[q]) {
-          MEM(q, m * dout[(hi[q] - 1) & 1] * e, 0);                // received gradient
-        }
+        const double y1 = dadd(fmax(clk[q], o), c1);   // the link's first Send
+        const double y2 = dadd(y1, c1);                // both ends now equal: max is the clock
+        clk[q] = (e1[q] && e2[q]) ? y2 : ((e1[q] || e2[q]) ? y1 : clk[q]);
+        // memory: received activation (lower link, forward), sent gradient
+        // dies (lower link, backward), received gradient (upper link, backward)
+        const int64_t act_b = m * kin[lo[q] & 1] * e, grd_b = m * dout[(hi[q] - 1) & 1] * e;
+        const int64_t add = (dn[q] && e1[q]) ? act_b : ((!dn[q] && e2[q]) ? grd_b : 0);
+        live[q] += add;
+        peak[q] = peak[q] > live[q] ? peak[q] : live[q];
+        live[q] -= (dn[q] && e2[q]) ? act_b : 0;
       }
     }
   } else if constexpr (SEQ) {
