@@ -43,7 +43,7 @@
  *   * Limits (DISTIR_E_UNSUPPORTED beyond them): world size <= 64, n_layer
  *     <= 1024, microbatches <= 4096, node_size a power of two, k <= 64,
  *     dp and tp powers of two in explicit configs (stage symmetry); ZeRO
- *     models: GPipe only and next_pow2(pp) * dp <= 32 (distir_model).
+ *     configurations with dp > 1: next_pow2(pp) * dp <= 32 (distir_model).
  */
 #ifndef DISTIR_H_
 #define DISTIR_H_
@@ -93,8 +93,8 @@ enum {
  *              live on replica l mod D of its (tp, stage) group, which
  *              broadcasts W_l before each forward / backward use and
  *              receives the gradients by a reduce after the stage's backward;
- *              GPipe only (DISTIR_E_UNSUPPORTED with 1F1B), and configs with
- *              D > 1 need next_pow2(pp) * dp <= 32 (DISTIR_E_UNSUPPORTED).
+ *              either schedule; configs with D > 1 need next_pow2(pp) * dp
+ *              <= 32 (DISTIR_E_UNSUPPORTED).
  *              Broadcast / Reduce cost (g-1) alpha + bytes / bw.
  * Unused fields are ignored. */
 enum { DISTIR_SCHED_GPIPE = 0, DISTIR_SCHED_1F1B = 1 };

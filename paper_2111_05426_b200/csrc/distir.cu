@@ -226,8 +226,6 @@ distir_status validate_model(const distir_model& m, int i) {
   if (m.kind == DISTIR_MODEL_MLP_TRAIN && ((m.recompute != 0 && m.recompute != 1) ||
                                            (m.zero != 0 && m.zero != 1)))
     return bad("recompute / zero must be 0 or 1");
-  if (m.kind == DISTIR_MODEL_MLP_TRAIN && m.zero && m.schedule != DISTIR_SCHED_GPIPE)
-    return fail(DISTIR_E_UNSUPPORTED, "model " + std::to_string(i) + ": ZeRO needs the GPipe schedule");
   if (m.d_model > (1 << 20)) return fail(DISTIR_E_UNSUPPORTED, "d_model > 2^20");
   if (m.kind == DISTIR_MODEL_GPT2_INFER) {
     if (m.n_head < 1 || m.seq_len < 1 || m.vocab_pad < 1 || m.n_ctx < 0 || m.id_bytes < 1)
@@ -338,6 +336,7 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     uint32_t m = 0;
     for (int mi = 0; mi < g->n_models; mi++) {
       const DModel& M = sim->models[g->models[mi]];
+      if (M.kind == 0 && M.zero) m |= gbit(0, 6);   // ZeRO with D > 1, either schedule
       if (M.kind == 0 && M.sched == 1) { m |= gbit(0, 5) | (wmax > 32 ? gbit(0, 7) : 0); continue; }
       m |= gbit(M.kind, 3);
       if (wmax > 32) m |= gbit(M.kind, 4);
@@ -677,9 +676,10 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
     uint32_t m = 0, kinds = 0;
     for (int64_t i = 0; i < n_configs; i++) {
       const DModel& M = sim->models[configs[i].model];
-      kinds |= 1u << (M.kind == 0 && M.sched == 1 ? 2 : M.kind == 0 && M.zero && configs[i].dp > 1 ? 3 : M.kind);
-      if (M.kind == 0 && M.sched == 1) m |= configs[i].pp > 32 ? gbit(0, 7) : gbit(0, 5);
-      else if (M.kind == 0 && M.zero && configs[i].dp > 1) m |= gbit(0, 6);
+      const bool zero = M.kind == 0 && M.zero && configs[i].dp > 1;    // ZeRO lanes, either schedule
+      kinds |= 1u << (zero ? 3 : M.kind == 0 && M.sched == 1 ? 2 : M.kind);
+      if (zero) m |= gbit(0, 6);
+      else if (M.kind == 0 && M.sched == 1) m |= configs[i].pp > 32 ? gbit(0, 7) : gbit(0, 5);
       else m |= gbit(M.kind, configs[i].pp > 32 ? 4 : 3);
     }
     if (n_configs > kNumBuckets / 2)

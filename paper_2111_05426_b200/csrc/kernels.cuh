@@ -29,7 +29,7 @@
 #include <climits>
 #ifdef DISTIR_INSTR
 // Debug instrumentation (tools/probe_instr.py): warp-aggregated event counts.
-static __device__ unsigned long long g_distir_instr[32];   // per translation unit
+static __device__ unsigned long long g_distir_instr[40];   // per translation unit
 __device__ __forceinline__ void distir_count(int i) {
   const unsigned m_ = __activemask();
   if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));

@@ -27,10 +27,10 @@ const void* DISTIR_CAT(sim_fn_, SIM_KIND, SIM_MODE)() {
 #ifdef DISTIR_INSTR
 // this TU's instrumentation counters: read, add into out[0..n), reset
 int DISTIR_CAT(sim_counters_, SIM_KIND, SIM_MODE)(unsigned long long* out, int n) {
-  unsigned long long h[32];
+  unsigned long long h[40];
   if (cudaMemcpyFromSymbol(h, g_distir_instr, sizeof(h)) != cudaSuccess) return -1;
-  for (int i = 0; i < n && i < 32; i++) out[i] = (i == 8 || i == 11) ? (out[i] > h[i] ? out[i] : h[i]) : out[i] + h[i];
-  unsigned long long z[32] = {0};
+  for (int i = 0; i < n && i < 40; i++) out[i] = (i == 8 || i == 11) ? (out[i] > h[i] ? out[i] : h[i]) : out[i] + h[i];
+  unsigned long long z[40] = {0};
   return cudaMemcpyToSymbol(g_distir_instr, z, sizeof(z)) == cudaSuccess ? 0 : -1;
 }
 #endif

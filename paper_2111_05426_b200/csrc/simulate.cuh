@@ -820,6 +820,10 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   for (int w = 0; w < nsteps; w++) {
       wc.steps++;
     if (lane == 0) DISTIR_COUNT(4);
+#ifdef DISTIR_INSTR
+    const long long t_step = clock64();
+    const unsigned slow0 = wc.slow;
+#endif
     bool act[V], rcv[V];
 #pragma unroll
     for (int q = 0; q < V; q++) {
@@ -838,6 +842,16 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       const double nc = dadd(fmax(clk[q], o), sd ? sendf[q] : recvc[q]);
       clk[q] = (sd || rcv[q]) ? nc : clk[q];
     }
+#ifdef DISTIR_INSTR
+    {   // per-step cycles, split by whether any lane of the warp took a slow path
+      const bool sl_any = __any_sync(0xffffffffu, wc.slow != slow0);
+      const long long dt_step = clock64() - t_step;
+      if (lane == 0) {
+        atomicAdd(&g_distir_instr[sl_any ? 34 : 32], (unsigned long long)dt_step);
+        atomicAdd(&g_distir_instr[sl_any ? 35 : 33], 1ull);
+      }
+    }
+#endif
   }
 #ifdef DISTIR_INSTR
   if (lane == 0) distir_clk_add(19, t_wave);
@@ -961,7 +975,10 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
   }
   for (int l = lo; l < hi; l++)
     if (own(l)) tail = mem_then(tail, mem_op(Wb, 2 * Wb));                         // SGD
-  {
+  // the schedule (bucket key: warp-uniform); GPipe composes the stage's
+  // memory events here, 1F1B applies them in its walk's order
+  const bool f1b = warp_max_int(has ? (int)c.M.sched : 0) == 1;
+  if (!f1b) {
     const MemProf ra = st > 0 ? mem_op(m * kin[lo & 1] * e, 0) : mem_id();
     const MemProf rg = st < P - 1 ? mem_op(m * dout[(hi - 1) & 1] * e, 0) : mem_id();
     const MemProf sg = st > 0 ? mem_op(0, m * kin[lo & 1] * e) : mem_id();
@@ -1046,6 +1063,54 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
   // costs of the Sends this lane receives (replica ri of stage st -/+ 1)
   const double recvf = dn ? cost_send(m * dout[(lo - 1) & 1] * e, group_intra(r0 - T * D, r0, ns), tp) : 0.0;
   const double recvb = up ? cost_send(m * kin[hi & 1] * e, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
+  if (f1b) {
+    // ---- ZeRO under synchronous 1F1B: run_mlp's slot wavefront (DESIGN
+    // reading R6; stage st's slot-t events at steps 3t + st + j: the Sends on
+    // the link to st-1, those on the link to st+1, the task), with the
+    // replica of this lane pairing with replica ri of the neighbouring stages
+    // (lanes Di apart) and every task starting with its Broadcast (the
+    // segment max over the stage's Di replicas, all at the same sub-step)
+    const int Pi = (int)P, Ki = (int)K;
+    const int w_s = Pi - 1 - st < Ki ? Pi - 1 - st : Ki, w_d = Pi - st < Ki ? Pi - st : Ki;
+    auto has_f = [&](int t, int ss, int w) -> bool {
+      const int dd = t - ss, hh = dd >> 1;
+      return (dd >= 0) & (((dd <= w) & (dd < Ki)) | (((dd & 1) == 0) & (hh > w) & (hh < Ki)));
+    };
+    auto has_b = [&](int t, int ss) -> bool {
+      const int dd = t - (2 * Pi - 1 - ss);
+      return (dd >= 0) & ((dd & 1) == 0) & ((dd >> 1) < Ki);
+    };
+    const int n1 = warp_max_int(has ? 3 * (2 * Pi + 2 * Ki - 3) + 3 : 0);
+    int uq = -st;
+    const int64_t act_b = m * kin[lo & 1] * e, grd_b = m * dout[(hi - 1) & 1] * e;
+    for (int step = 0; step < n1; step++) {
+      wc.steps++;
+      const int u = uq++;
+      const int t = u >= 0 ? u / 3 : -1, j = u - 3 * t;
+      const bool lo_ok = ok && st > 0 && t >= 0, hi_ok = ok && st < Pi - 1 && t >= 0;
+      const bool dnl = j == 0;
+      const bool e1 = dnl ? (lo_ok && has_f(t - 1, st - 1, w_d)) : (j == 1 && hi_ok && has_f(t - 1, st, w_s));
+      const bool e2 = dnl ? (lo_ok && has_b(t - 1, st)) : (j == 1 && hi_ok && has_b(t - 1, st + 1));
+      const bool tf = j == 2 && ok && t >= 0 && has_f(t, st, w_s);
+      const bool tb = j == 2 && ok && t >= 0 && has_b(t, st);
+      if (tf) mem_apply(live, peak, pf);
+      if (tb) mem_apply(live, peak, pb);
+      fwd_task(tf);                                // (collective: every lane, every step)
+      bwd_task(tb);
+      const double nbu = __shfl_down_sync(0xffffffffu, clk, Di);
+      const double nbd = __shfl_up_sync(0xffffffffu, clk, Di);
+      const double o = dnl ? nbd : nbu;
+      const double c1 = dnl ? recvf : recvb;       // the link's cost (both directions)
+      const double y1 = dadd(fmax(clk, o), c1);
+      const double y2 = dadd(y1, c1);
+      clk = (e1 && e2) ? y2 : ((e1 || e2) ? y1 : clk);
+      const int64_t add = (dnl && e1) ? act_b : ((!dnl && e2) ? grd_b : 0);
+      live += add;
+      peak = peak > live ? peak : live;
+      live -= (dnl && e2) ? act_b : 0;
+    }
+    if (ok) mem_apply(live, peak, tail);
+  } else {
   {   // forward wavefront: task (k, s) at step 2k + s, then Send s -> s+1
     int kk = -st;
     for (int wv = 0; wv < nsteps; wv++) {
@@ -1076,6 +1141,7 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
       clk = (sd || rcv) ? nc : clk;
     }
   }
+  }   // GPipe
   // tail: the owner updates its layers (SGD); no DP AllReduce under ZeRO
   if (ok)
     for (int l = lo; l < hi; l++)

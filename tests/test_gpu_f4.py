@@ -98,13 +98,9 @@ def test_checkpointing_lowers_gpu_peaks(sim):
 
 
 def test_zero_unsupported_shapes():
-    """ZeRO under 1F1B and ZeRO configurations needing more than 32 lanes
-    (next_pow2(P) * D > 32 with D > 1) are rejected with DISTIR_E_UNSUPPORTED
-    (include/distir.h)."""
+    """ZeRO configurations needing more than 32 lanes (next_pow2(P) * D > 32
+    with D > 1) are rejected with DISTIR_E_UNSUPPORTED (include/distir.h)."""
     from paper_2111_05426_b200 import DistirError, Simulator
-    with pytest.raises(DistirError) as e:
-        Simulator({"z": W.mlp(4, 64, zero=1, schedule=1)}, {"t": W.TOPOLOGIES["TB200"]}, device=0)
-    assert e.value.status == 2
     s = Simulator({"z": W.mlp(64, 64, zero=1)}, {"t": W.TOPOLOGIES["TB200"]}, device=0)
     with pytest.raises(DistirError) as e:
         s.eval(configs=[(0, 0, 4, 1, 16, 2, 64)], k=1)
@@ -121,3 +117,18 @@ def test_w4_zero_model_runs(sim):
     run on the plain kernels (ZeRO partitions over replicas only), against
     the oracle on the whole grid."""
     assert full_grid_check(sim, W.grid_with("W4", models=["mlp_w4_zero"])) == 1.0
+
+
+@pytest.mark.parametrize("name", ["mlp_w1_zero_1f1b"])
+def test_w1_zero_under_1f1b(sim, name):
+    """ZeRO under the paper's 1F1B schedule (oracle: the same ZeRO tasks in
+    the unit-time order of reading R6)."""
+    for topo in ["TB200", "TV100", "TM0", "TM5"]:
+        assert full_grid_check(sim, W.grid_with("W1", models=[name], topos=[topo])) == 1.0
+
+
+def test_w2_zero_under_1f1b(sim):
+    """The paper's MLP-1B grid under ZeRO + 1F1B, plain and with checkpointing
+    in one spec with the GPipe variant."""
+    g = W.grid_with("W2", models=["mlp_1b_zero_1f1b", "mlp_1b_zero"], topos=["TB200", "TM1"])
+    assert full_grid_check(sim, g) == 1.0

@@ -14,12 +14,13 @@ from paper_2111_05426_b200 import Simulator
 NAMES = ["tasks", "fast", "refresh", "plain", "steps", "item_cycles", "-", "items", "max_item_cycles",
          "slow_cycles", "slow_entries", "max_item_tag", "refresh_cyc", "cross_cyc", "-", "addtask_cyc",
          "quick_try", "quick_ok", "setup_cycles", "wave_cycles", "fill_cycles", "q_range", "q_tieE", "q_range1", "q_tieE1",
-         "q_twice", "q_rest", "cost_cycles", "mem_cycles"] + ["-"] * 3
+         "q_twice", "q_rest", "cost_cycles", "mem_cycles", "-", "-", "-", "fstep_cyc", "fstep_n",
+         "sstep_cyc", "sstep_n", "-", "-", "-", "-"]
 
 
 def counters():
-    buf = (ctypes.c_ulonglong * 32)()
-    pkg.lib.distir_debug_counters(buf, 32)
+    buf = (ctypes.c_ulonglong * 40)()
+    pkg.lib.distir_debug_counters(buf, 40)
     return list(buf)
 
 
@@ -67,6 +68,8 @@ def main():
         print("   quick-path misses: x outside table %d, ties in E %d, E+1 outside table %d, ties in E+1 %d, "
               "crossing pass beyond E+1 %d, rest overflows E+1 %d" % tuple(d[k] for k in (
                   "q_range", "q_tieE", "q_range1", "q_tieE1", "q_twice", "q_rest")))
+        print("   GPT-2 wavefront steps without a slow lane: %d, %.0f cycles each; with: %d, %.0f cycles each" % (
+            d["fstep_n"], d["fstep_cyc"] / max(d["fstep_n"], 1), d["sstep_n"], d["sstep_cyc"] / max(d["sstep_n"], 1)))
         tag = d["max_item_tag"]
         key = (tag >> 5) & 0x7FFFF
         print("   slowest item: %d cycles, kind %d P %d L %d, %d configs" % (

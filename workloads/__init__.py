@@ -86,6 +86,9 @@ MODELS = {
     "gpt2_175b": gpt2(96, 12288, 96),
     # W4 under ZeRO (D = 1 on W4: the plain kernels; P up to 64)
     "mlp_w4_zero": mlp(64, 8192, zero=1),
+    # ZeRO under the paper's 1F1B schedule
+    "mlp_w1_zero_1f1b": mlp(2, 64, zero=1, schedule=1),
+    "mlp_1b_zero_1f1b": mlp(16, 8192, zero=1, schedule=1),
 }
 
 HF_GPT2 = ["gpt2_small", "gpt2_medium", "gpt2_large", "gpt2_xl"]
