@@ -661,6 +661,29 @@ DISTIR_HD int task3_quick(double& x, const Seg (&sg)[3], TaskCache& c, const Bin
   return 1;
 }
 
+// Point a three-segment task cache at x's binade from the table (no add):
+// after a task walked op by op, so the next task takes the fast path.  The
+// cache is left as it was (stale: the next task re-enters the slow path) when
+// the table does not cover the binade or a list has ties there.
+DISTIR_HD void task3_cache_to(double x, const Seg (&sg)[3], TaskCache& c, const BinTab& t) {
+  const int32_t ef = exp_field(x);
+  const int32_t b = ef - t.e0;
+  if (!(x > 0.0) || b < 0 || b >= t.nb || ef > 1992) return;
+  const int64_t* r0 = t.tab + (int64_t)b * 6;
+  const int64_t A0 = r0[0], A0b = r0[1], B0 = r0[2], B0b = r0[3], C0 = r0[4], C0b = r0[5];
+  const int64_t p = sg[0].reps, n = sg[1].reps, e = sg[2].reps;
+  if (!(B0 == B0b && B0 < kNeverI && (!p || (A0 == A0b && A0 < kNeverI)) &&
+        (!e || (C0 == C0b && C0 < kNeverI))))
+    return;
+  auto sat = [](int64_t v) { return v > kTwo53 ? kTwo53 : v; };
+  const int64_t tot = p * A0 + sat(n * B0) + e * C0;
+  c.R[0] = A0; c.R[1] = A0b; c.R[2] = B0; c.R[3] = B0b; c.R[4] = C0; c.R[5] = C0b;
+  c.ef = ef;
+  c.lo = ef << 20;
+  c.hi = (ef + 1) << 20;
+  c.Su0 = c.Su1 = tot < kTwo53 ? xmul((double)tot, bits2d((int64_t)(ef - 52) << 52)) : kInf();
+}
+
 // The same straight-line slow path for a task of NS segments read through a
 // segment map (the MLP kernels' forward / backward tasks): (i) a stale cache
 // -- the whole task fits x's binade E; (ii) one crossing -- the segments and

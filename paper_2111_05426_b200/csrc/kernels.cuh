@@ -206,8 +206,13 @@ __device__ __forceinline__ double cost_op(int64_t flops, int64_t bytes, bool mm,
   if (t.cost_model == 1) return cost_regression(flops, bytes, mm, t);
   return cost_compute(flops, t);
 }
+// Non-negative integer quotient, in 32 bits when both operands fit (64-bit
+// division is a long software routine on the GPU; the setup does ~15).
+__device__ __forceinline__ int64_t qdiv(int64_t a, int64_t b) {
+  return ((uint64_t)(a | b) >> 32) == 0 ? (int64_t)((uint32_t)a / (uint32_t)b) : a / b;
+}
 __device__ __forceinline__ bool group_intra(int64_t first, int64_t last, int32_t ns) {
-  return first / ns == last / ns;
+  return qdiv(first, ns) == qdiv(last, ns);
 }
 __device__ __forceinline__ double cost_send(int64_t bytes, bool intra, const DTopo& t) {
   const double a = intra ? t.a_intra : t.a_inter, bw = intra ? t.bw_intra : t.bw_inter;
@@ -294,11 +299,13 @@ struct WorkCount {
 // ------------------------------------------------------------- kernels ------
 #ifndef DISTIR_SIM_TU   // sim_inst.cu compiles only k_simulate
 
-__global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* __restrict__ ex,
+// Bodies of the prepare phases (bid / nblk: this block's index and the grid
+// size).
+__device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp, const DExplicit* __restrict__ ex,
                             Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
                             double* __restrict__ ms_out, int64_t* __restrict__ pk_out,
                             uint32_t* __restrict__ rs_out, double* __restrict__ tp_out,
-                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr) {
+                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr, int bid, int nblk) {
   const SpecBlock& sp = *spp;
   const int64_t nloc = sp.n_local;
   unsigned long long ev = 0, st = 0, nv = 0, tk = 0;
@@ -306,8 +313,8 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
   __shared__ DEntry s_ent[kMaxEntries];
   for (int j = threadIdx.x; j < sp.n_entries; j += blockDim.x) s_ent[j] = sp.entries[j];
   __syncthreads();
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nloc;
-       q += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = bid * (int64_t)blockDim.x + threadIdx.x; q < nloc;
+       q += (int64_t)nblk * blockDim.x) {
     const int64_t i = sp.rank + q * sp.n_ranks;
     Cfg c;
     decode(sp, ex, i, c, s_ent);
@@ -355,6 +362,14 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
   }
 }
 
+__global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* __restrict__ ex,
+                            Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
+                            double* __restrict__ ms_out, int64_t* __restrict__ pk_out,
+                            uint32_t* __restrict__ rs_out, double* __restrict__ tp_out,
+                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr) {
+  enumerate_body(spp, ex, bk, cfg_bucket, ms_out, pk_out, rs_out, tp_out, pc_out, hdr, blockIdx.x, gridDim.x);
+}
+
 __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
   uint32_t p = 1;
   while (p < x) p <<= 1;
@@ -378,8 +393,8 @@ __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
 // more resident warps than items, the heaviest classes are split into items
 // of fewer configurations (cpw halved per step, heaviest class first).
 constexpr int kPlanThreads = 1024;   // k_plan's block size (distir.cu launch)
-__global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
-                                                       PlanBudget budget) {
+__device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
+                                          const PlanBudget& budget) {
   __shared__ unsigned int s_items[kGroups][kNumClasses];
   __shared__ unsigned int s_alt[kGroups][kNumClasses][kMaxSplit + 1];   // items at split j
   __shared__ unsigned char s_shift[kGroups][kNumClasses];
@@ -529,12 +544,17 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, 
   }
 }
 
-__global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
+__global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
+                                                       PlanBudget budget) {
+  plan_body(bk, hdr, budget);
+}
+
+__device__ __forceinline__ void scatter_body(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
                           const uint32_t* __restrict__ cfg_bucket, const PCfg* __restrict__ pc,
-                          PCfg* __restrict__ perm, Item* __restrict__ items) {
+                          PCfg* __restrict__ perm, Item* __restrict__ items, int bid, int nblk) {
   const int64_t nloc = spp->n_local;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nloc;
-       q += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = bid * (int64_t)blockDim.x + threadIdx.x; q < nloc;
+       q += (int64_t)nblk * blockDim.x) {
     const uint32_t b = cfg_bucket[q];
     if (b == kEmptyKey) continue;
     const uint32_t pos = atomicAdd(&bk[b].cursor, 1u);
@@ -551,6 +571,28 @@ __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict_
     }
   }
 }
+
+__global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
+                          const uint32_t* __restrict__ cfg_bucket, const PCfg* __restrict__ pc,
+                          PCfg* __restrict__ perm, Item* __restrict__ items) {
+  scatter_body(spp, bk, cfg_bucket, pc, perm, items, blockIdx.x, gridDim.x);
+}
+
+// Empty bucket table and zero header (every launch starts from them).
+__device__ __forceinline__ void reset_body(Bucket* bk, WsHeader* hdr, int bid, int nblk) {
+  for (int i = bid * blockDim.x + threadIdx.x; i < kBucketSlots; i += nblk * blockDim.x) {
+    Bucket b{};
+    b.key = kEmptyKey;
+    bk[i] = b;
+  }
+  if (bid == 0 && threadIdx.x == 0) {
+    WsHeader h{};
+    *hdr = h;
+  }
+}
+
+__global__ void k_reset(Bucket* bk, WsHeader* hdr) { reset_body(bk, hdr, blockIdx.x, gridDim.x); }
+
 
 #endif  // DISTIR_SIM_TU
 
@@ -932,16 +974,26 @@ __global__ void __launch_bounds__(kSelectThreads) k_topk_select(
   const uint64_t T = *(volatile const unsigned long long*)&hdr->topk_thresh;
   if (t == 0) s_n = 0;
   __syncthreads();
-  // every (list, record) pair at once: independent loads, no chains
-  const int64_t pairs = (int64_t)n_lists * k;
-  for (int64_t pq = t; pq < pairs; pq += blockDim.x) {
-    const int l = (int)(pq / k), r = (int)(pq - (int64_t)l * k);
-    if (r >= part_n[l]) continue;
-    const TopkRec x = part[pq];
-    const Key kk = make_key(x.throughput, x.peak, x.index, x.makespan);
-    if (kk.a < T) continue;
-    const int pos = atomicAdd(&s_n, 1);
-    if (pos < kSelectCap) s_c[pos] = kk;
+  // one list per thread: its count, then its records in batches of 8
+  // independent loads (a list's records are contiguous; one L2 round trip
+  // per batch instead of one dependent count + record pair per record)
+  for (int l = t; l < n_lists; l += blockDim.x) {
+    const int nl = part_n[l];
+    const TopkRec* src = part + (int64_t)l * k;
+    for (int r0 = 0; r0 < nl; r0 += 8) {
+      TopkRec x[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        if (r0 + j < nl) x[j] = src[r0 + j];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        if (r0 + j >= nl) continue;
+        const Key kk = make_key(x[j].throughput, x[j].peak, x[j].index, x[j].makespan);
+        if (kk.a < T) continue;
+        const int pos = atomicAdd(&s_n, 1);
+        if (pos < kSelectCap) s_c[pos] = kk;
+      }
+    }
   }
   __syncthreads();
   const int n = s_n;

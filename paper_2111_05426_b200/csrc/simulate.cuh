@@ -88,6 +88,86 @@ constexpr int kPlainMlp = DISTIR_PLAIN_MLP;
 #if DISTIR_CROSS1 && !DISTIR_VOTE
 #error "DISTIR_CROSS1 uses warp votes inside the slow path: build with DISTIR_VOTE=1"
 #endif
+#ifndef DISTIR_PLAIN_ALL
+#define DISTIR_PLAIN_ALL 8  // GPT-2: tasks of <= N blocks walked op by op at every slow entry
+                            // (A/B on one B200, r02y: W3 -2.5%, W5 -6.5%, XL P16 K128 -8%; 16: W3 +3%)
+#endif
+#ifndef DISTIR_JUMP
+#define DISTIR_JUMP 1       // GPipe wavefronts: exact steady-state jumps (steady_jump)
+#endif
+#ifndef DISTIR_JUMP_MIN_K
+#define DISTIR_JUMP_MIN_K 64  // ... in warps of K >= this many microbatches (the checks cost
+#endif                        // more than short pipelines gain: W5, K <= 32, +8% with them)
+
+// Steady-state jump of a GPipe wavefront (exact).  In the pipeline's
+// interior every period of two wavefront steps runs the same events on every
+// stage (each stage one task, one receive, one send), so the map F over a
+// window of R steps is the same function window after window.  If one window
+// moved every stage clock of a configuration by the same real Delta --
+// F(X) = X + Delta -- then F(X + j Delta) = F(X) + j Delta for as long as
+// each clock stays in its binade and Delta is an even number of that
+// binade's ulps: every IEEE add of the window is the add of some stage's
+// clock whose exact result moves by j Delta inside one binade, where RN
+// commutes with a shift by an even number of ulps (ties to even included),
+// and max commutes with any common shift.  (Each lane's add results are its
+// own clock values, which lie between its window-start and window-end
+// clocks.)  So n more windows add n Delta exactly -- the same bits as walking
+// them (Theorem 1 keeps the per-device program order; only clocks move).
+//
+// Called by every lane of the warp at the end of a window; x / snap = this
+// lane's clock now / at the window's start, lane_ok = the lane holds a stage
+// of the configuration, J = the configuration's stage-0 wavefront counter,
+// n_max = how many more whole windows stay in the interior (<= 0: none).
+// Returns the number of windows to skip (0: none), uniform over the
+// configuration's S lanes; the caller adds n Delta and advances its counters.
+__device__ __forceinline__ int64_t steady_jump(double x, double snap, bool lane_ok, bool cfg_live,
+                                               int64_t n_max, int S, int lane) {
+  const int base = lane & ~(S - 1);
+  const unsigned smask = S == 32 ? 0xffffffffu : (((1u << S) - 1u) << base);
+  const double dl = x - snap;                        // exact when both share a binade
+  const double d0 = __shfl_sync(0xffffffffu, dl, base);
+  const int64_t du = d2bits(x) - d2bits(snap);       // ulps of that binade
+  const bool ok = !lane_ok || (snap > 0.0 && exp_field(x) == exp_field(snap) && dl == d0 && !(du & 1));
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  const bool go = cfg_live && n_max > 0 && d0 > 0.0 && (bal & smask) == smask;
+  if (!__any_sync(0xffffffffu, go)) return 0;
+  int64_t n = go ? n_max : 0;
+  if (go && lane_ok) {
+    const int64_t room = ((int64_t)(exp_field(x) + 1) << 52) - 1 - d2bits(x);   // ulps left in the binade
+    n = min(n, room / du);
+  }
+  for (int o = S >> 1; o > 0; o >>= 1) n = min(n, __shfl_xor_sync(0xffffffffu, n, o));
+  return n;
+}
+
+// The jump check of a GPipe wavefront (one stage per lane), every 8 steps:
+// windows of 4 periods (even ulp counts arise with stages one binade apart).
+// kk = this lane's wavefront counter (stage s' runs task kk/2 when kk is even
+// and receives when it is odd, kk = w - s' without jumps), first = the lane
+// offset of the wavefront's first stage s' = 0 in the configuration's
+// segment (stage 0 forward, stage P-1 backward).  J = that stage's counter
+// at the next step; the window [J - 8, J) was interior iff J - 8 >= P - 1,
+// and n skipped windows are iff J + 8n - 2 <= 2K - 2 (every stage s' >= 1
+// receives and runs one task per period, stage 0 runs one task).  After a
+// jump the warp's step bound shrinks to its configurations' remaining steps
+// (a configuration ends after stage s' = P-1's task K-1, counter 2K+P-3).
+__device__ __forceinline__ void wave_jump(int w, int& nsteps, double& clk, double& snap, int& kk,
+                                          bool lane_ok, bool has, int64_t P, int64_t K, int S,
+                                          int lane, int first) {
+  if ((w & 7) != 7) return;
+  const int J = __shfl_sync(0xffffffffu, kk, (lane & ~(S - 1)) + first);
+  const int64_t nmax = J >= P + 7 ? (2 * K - J) / 8 : 0;
+  const int64_t nj = steady_jump(clk, snap, lane_ok, has, nmax, S, lane);
+  if (__any_sync(0xffffffffu, nj > 0)) {
+    if (nj > 0) {
+      if (lane_ok) clk = bits2d(d2bits(clk) + nj * (d2bits(clk) - d2bits(snap)));
+      kk += (int)(8 * nj);
+    }
+    nsteps = w + 1 + warp_max_int(has ? (int)(2 * K + P - 2) - (J + (int)(8 * nj)) : 0);
+  }
+  snap = clk;
+}
+
 // Segment -> distinct-op-list maps of the task caches (BinTab).
 static __device__ constexpr int kMapId3[3] = {0, 1, 2};
 // MLP backward: LossGrad, recompute (the forward lists), layers (desc)
@@ -119,11 +199,11 @@ template <int V, bool SEQ, bool F1B, bool RC>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                         double* row, double* tab, double& ms_out, int64_t& peak_out, WorkCount& wc) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
-  const int64_t m = has ? c.B / (D * K) : 0;
+  const int64_t m = has ? qdiv(c.B, D * K) : 0;
   const int32_t ns = tp.node_size;
   // Layer shapes by parity of the global layer index: even = column
   // parallel, odd = row parallel (Megatron pairing); T = 1: both full.
-  const Par<int64_t> kin{d, d / T}, nout{d / T, d}, dout{d / T, d};
+  const Par<int64_t> kin{d, qdiv(d, T)}, nout{qdiv(d, T), d}, dout{qdiv(d, T), d};
   const bool tp_intra = group_intra(0, T - 1, ns);
   const bool dp_intra = group_intra(0, T * (D - 1), ns);
   const int64_t w0 = kin.a * nout.a, w1 = kin.b * nout.b;
@@ -192,8 +272,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
   for (int q = 0; q < V; q++) {
     s[q] = sl + S * q;
     ok[q] = has && s[q] < P;
-    lo[q] = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
-    hi[q] = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
+    lo[q] = ok[q] ? (int)qdiv((int64_t)s[q] * L, P) : 0;
+    hi[q] = ok[q] ? (int)qdiv((int64_t)(s[q] + 1) * L, P) : 0;
     const int64_t r0 = T * D * (int64_t)s[q];    // rank (0, 0, s)
     sendf[q] = (ok[q] && s[q] < P - 1)
                    ? cost_send(m * dout[(hi[q] - 1) & 1] * e, group_intra(r0, r0 + T * D, ns), tp)
@@ -240,6 +320,10 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int o = S >> 1; o > 0; o >>= 1) nlm = max(nlm, __shfl_xor_sync(0xffffffffu, nlm, o));
     plain_cfg = (int64_t)nlm * warp_max_int(has ? (int)K : 0) <= (int64_t)kPlainMlp * (32 / S);
   }
+  // steady-state jumps only in warps of long configurations (a warp of many
+  // short, plainly walked ones gains less than the checks cost)
+  const bool jump_ok = warp_max_int(has ? (int)K : 0) >= DISTIR_JUMP_MIN_K &&
+                       __all_sync(0xffffffffu, !has || !plain_cfg);
   BinTab btf{nullptr, 0, 0, 0};
   if constexpr (!SEQ) {
     // binade table of the 7 distinct op lists (forward b / ab / a,
@@ -464,7 +548,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     mem_apply(live[q], peak[q], mem_then(mem_rep(mem_then(ra, pf[q]), K),
                                          mem_rep(mem_then(mem_then(rg, pb[q]), sg), K)));
   }
-  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  const int nsteps0 = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
   const unsigned int K2 = (unsigned int)(2 * K);
   bool up[V], dn[V];
   double recvf[V], recvb[V];
@@ -485,6 +569,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     int kk[V];
 #pragma unroll
     for (int q = 0; q < V; q++) kk[q] = -s[q];
+    int nsteps = nsteps0;
+    double snap = 0.0;   // clock at the start of the jump window
     for (int w = 0; w < nsteps; w++) {
       wc.steps++;
       bool act[V], rcv[V];
@@ -504,6 +590,11 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         const double nc = dadd(fmax(clk[q], sd ? nbu[q] : nbd[q]), sd ? sendf[q] : recvf[q]);
         clk[q] = (sd || rcv[q]) ? nc : clk[q];
       }
+#if DISTIR_JUMP
+      if constexpr (V == 1) {
+        if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, 0);
+      }
+#endif
     }
   }
   // ---- backward wavefront: task (k, s) at step 2k + (P-1-s), then Send s -> s-1
@@ -511,6 +602,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     int kk[V];
 #pragma unroll
     for (int q = 0; q < V; q++) kk[q] = -(int)(P - 1 - s[q]);
+    int nsteps = nsteps0;
+    double snap = 0.0;
     for (int w = 0; w < nsteps; w++) {
       wc.steps++;
       bool act[V], rcv[V];
@@ -530,6 +623,12 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         const double nc = dadd(fmax(clk[q], sd ? nbd[q] : nbu[q]), sd ? sendb[q] : recvb[q]);
         clk[q] = (sd || rcv[q]) ? nc : clk[q];
       }
+#if DISTIR_JUMP
+      // the backward wavefront's first stage is P-1
+      if constexpr (V == 1) {
+        if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, (int)P - 1);
+      }
+#endif
     }
   }
   }  // wavefront
@@ -575,8 +674,8 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
                 ide = c.M.ide, nctx = c.M.nctx;
   const bool lm = c.M.lm != 0;
   const int64_t D = c.D, T = c.T, P = c.P, K = c.K;
-  const int64_t m = has ? c.B / (D * K) : 0;
-  const int64_t n = m * Sq, dT = d / T, hT = h / T, VT = Vp / T;
+  const int64_t m = has ? qdiv(c.B, D * K) : 0;
+  const int64_t n = m * Sq, dT = qdiv(d, T), hT = qdiv(h, T), VT = qdiv(Vp, T);
   const int32_t ns = tp.node_size;
   const bool tp_intra = group_intra(0, T - 1, ns);
   const int64_t nde = n * d * e;
@@ -659,8 +758,8 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   for (int q = 0; q < V; q++) {
     s[q] = sl + S * q;
     ok[q] = has && s[q] < P;
-    const int lo = ok[q] ? (int)((int64_t)s[q] * L / P) : 0;
-    const int hi = ok[q] ? (int)((int64_t)(s[q] + 1) * L / P) : 0;
+    const int lo = ok[q] ? (int)qdiv((int64_t)s[q] * L, P) : 0;
+    const int hi = ok[q] ? (int)qdiv((int64_t)(s[q] + 1) * L, P) : 0;
     nb[q] = hi - lo;
     const int64_t r0 = T * D * (int64_t)s[q];
     sendf[q] = (ok[q] && s[q] < P - 1) ? cost_send(nde, group_intra(r0, r0 + T * D, ns), tp) : 0.0;
@@ -744,6 +843,14 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
         task3_plain(clk[q], sg);
         s2 = false;
       }
+#if DISTIR_PLAIN_ALL > 0
+      // short tasks: op by op, then the cache moves to the new binade
+      if (s2 && nb[q] <= DISTIR_PLAIN_ALL) {
+        task3_plain(clk[q], sg);
+        task3_cache_to(clk[q], sg, tc[q], bt);
+        s2 = false;
+      }
+#endif
       if (s2) {
         DISTIR_COUNT(16);
         const int r = task3_quick(clk[q], sg, tc[q], bt);
@@ -801,10 +908,12 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
   // and receiver both wait for each other and end at
   // max(their clocks) + cost; each computes it from the other's clock
   // (both neighbours' clocks are shuffled independently), bit-identically.
-  const int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
+  int nsteps = warp_max_int(has ? (int)(2 * (K - 1) + P) : 0);
 #ifdef DISTIR_INSTR
   const long long t_wave = clock64();
 #endif
+  double snap = 0.0;   // this lane's clock at the start of the jump window
+  const bool jump_ok = warp_max_int(has ? (int)K : 0) >= DISTIR_JUMP_MIN_K;
   bool up[V], dn[V];
   int kk[V];
   double recvc[V];
@@ -842,6 +951,11 @@ __device__ void run_gpt2(const Cfg& c, const DTopo& tp, bool has, int sl, int S,
       const double nc = dadd(fmax(clk[q], o), sd ? sendf[q] : recvc[q]);
       clk[q] = (sd || rcv[q]) ? nc : clk[q];
     }
+#if DISTIR_JUMP
+    if constexpr (V == 1) {
+      if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, 0);
+    }
+#endif
 #ifdef DISTIR_INSTR
     {   // per-step cycles, split by whether any lane of the warp took a slow path
       const bool sl_any = __any_sync(0xffffffffu, wc.slow != slow0);
@@ -891,10 +1005,10 @@ __device__ __forceinline__ double cost_chain(int64_t g, int64_t bytes, bool intr
 static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                              double* row, double* tab, double& ms_out, int64_t& peak_out, WorkCount& wc) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
-  const int64_t m = has ? c.B / (D * K) : 0;
+  const int64_t m = has ? qdiv(c.B, D * K) : 0;
   const int32_t ns = tp.node_size;
   const bool rc = c.M.rc != 0;
-  const Par<int64_t> kin{d, d / T}, nout{d / T, d}, dout{d / T, d};
+  const Par<int64_t> kin{d, qdiv(d, T)}, nout{qdiv(d, T), d}, dout{qdiv(d, T), d};
   const bool tp_intra = group_intra(0, T - 1, ns);
   const bool dp_intra = group_intra(0, T * (D - 1), ns);
   const int64_t w = kin.a * nout.a;              // == kin.b * nout.b (d^2 / T)
@@ -928,8 +1042,8 @@ static __device__ void run_mlp_zero(const Cfg& c, const DTopo& tp, bool has, int
   const int Di = warp_max_int(has ? (int)D : 1);
   const int ri = sl % Di, st = sl / Di;            // replica, stage
   const bool ok = has && st < P;
-  const int lo = ok ? (int)((int64_t)st * L / P) : 0;
-  const int hi = ok ? (int)((int64_t)(st + 1) * L / P) : 0;
+  const int lo = ok ? (int)qdiv((int64_t)st * L, P) : 0;
+  const int hi = ok ? (int)qdiv((int64_t)(st + 1) * L, P) : 0;
   const int nl = hi - lo;
   const int64_t r0 = T * D * (int64_t)st;
   const double sendf = (ok && st < P - 1)

@@ -1,0 +1,10 @@
+#!/bin/bash
+# round-2 session 3: GPU parity with the MLP/GPT-2 GPipe jumps, A/B without
+# them, and the instrumented long-pole probe.
+cd "$(dirname "$0")/.."
+OUT=gpurun_out/r02w; mkdir -p $OUT
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "exit $?" >> $OUT/pytest_gpu.log
+tail -2 $OUT/pytest_gpu.log
+PROBE_TAIL=20 bash tools/ab_so.sh variants/nojump.so paper_2111_05426_b200/libdistir.so > $OUT/ab.txt 2>&1
+cat $OUT/ab.txt
+PROBE_GRIDS=1 bash tools/instr_probe.sh $OUT > /dev/null 2>&1; cat $OUT/instr.txt
