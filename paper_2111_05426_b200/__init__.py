@@ -100,6 +100,9 @@ class distir_stats(ctypes.Structure):
         "wave_steps")]
 
 
+_STATS_FIELDS = tuple(f for f, _ in distir_stats._fields_)
+
+
 class distir_raw_op(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "n_dev", "dev_off", "n_in", "in_off", "n_out", "out_off")] + [
@@ -340,26 +343,31 @@ class Simulator:
                         torch.empty(m, dtype=torch.int64, pin_memory=pinned),
                         torch.empty(m, dtype=torch.int32, pin_memory=pinned), pinned)
                 self._host_bufs = bufs
+                # numpy views and raw pointers, made once per buffer set
+                self._host_np = tuple(t.numpy() for t in bufs[:3])
+                self._host_ptr = tuple(ctypes.c_void_p(t.data_ptr()) for t in bufs[:3])
             outs = {"makespan": bufs[0], "peak": bufs[1], "reason": bufs[2]}
             if n_ranks > 1:       # entries of other ranks stay untouched: mark them
                 bufs[0][:n].fill_(float("nan"))
                 bufs[1][:n].fill_(-2)
                 bufs[2][:n].fill_(-1)
+            ptrs = self._host_ptr
+        else:
+            ptrs = (None, None, None)
         topk = np.zeros(max(k, 1), dtype=TOPK_DTYPE) if copy else self._topk_buf(k)
         ntopk = ctypes.c_int32()
         st = distir_stats()
-        p = lambda name: ctypes.c_void_p(outs[name].data_ptr()) if name in outs else None
         _check(lib.distir_grid_eval_sharded(
             self.handle, ctypes.byref(sp) if sp is not None else None,
             cf, ncf, rank, n_ranks, comm, k, ctypes.c_void_p(ws.data_ptr()),
-            ws.numel(), p("makespan"), p("peak"), p("reason"),
+            ws.numel(), ptrs[0], ptrs[1], ptrs[2],
             topk.ctypes.data_as(ctypes.c_void_p), ctypes.byref(ntopk),
             ctypes.byref(st)))
         res = dict(topk=topk[:ntopk.value], n=n,
-                   stats={f: getattr(st, f) for f, _ in distir_stats._fields_})
-        for name, t in outs.items():
-            res[name] = t.numpy()[:n].copy() if copy else t.numpy()[:n]
+                   stats={f: getattr(st, f) for f in _STATS_FIELDS})
         if per_config:
+            for name, a in zip(("makespan", "peak", "reason"), self._host_np):
+                res[name] = a[:n].copy() if copy else a[:n]
             res["reason"] = res["reason"].view(np.uint32)
         return res
 

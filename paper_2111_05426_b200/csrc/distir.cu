@@ -77,7 +77,6 @@ Layout layout(int64_t n_local, int64_t n_explicit) {
     return o;
   };
   const size_t n = (size_t)(n_local > 0 ? n_local : 1);
-  L.hdr = take(sizeof(WsHeader));
   L.spec = take(sizeof(SpecBlock));
   L.ex = take((size_t)(n_explicit > 0 ? n_explicit : 1) * sizeof(DExplicit));
   L.bk = take(kBucketSlots * sizeof(Bucket));
@@ -94,8 +93,11 @@ Layout layout(int64_t n_local, int64_t n_explicit) {
   L.gath = take((size_t)kMaxRanks * kMaxK * sizeof(TopkRec));
   L.fin = take((size_t)kMaxK * sizeof(TopkRec));
   L.fin_n = take(16);
+  // final top-k, its count and the header contiguous: the host-buffer path
+  // fetches all three with one copy
   L.out = take((size_t)kMaxK * sizeof(TopkRec));
   L.out_n = take(16);
+  L.hdr = take(sizeof(WsHeader));
   L.total = off;
   return L;
 }
@@ -182,9 +184,8 @@ struct distir_sim {
   // its count and the statistics header D2H), so they are true async DMA
   struct Pinned {
     SpecBlock spec;
-    WsHeader hdr;
-    TopkRec topk[kMaxK];
-    int32_t ntopk;
+    // image of the workspace's [out | out_n | hdr] sections (Layout)
+    alignas(256) unsigned char tail[kMaxK * sizeof(TopkRec) + 256 + sizeof(WsHeader)];
   };
   Pinned* pin = nullptr;
   cudaEvent_t pin_ev = nullptr;     // the last H2D from pin->spec
@@ -945,23 +946,26 @@ distir_status distir_grid_eval_sharded(distir_sim* sim, const distir_grid_spec* 
     if (reason_out) CUDA_TRY(get(reason_out + rank, at<uint32_t>(d_workspace, L.rs), 4));
   }
   distir_sim::Pinned* P = sim->pin;
-  if (k > 0) {
-    CUDA_TRY(cudaMemcpyAsync(P ? (void*)P->topk : (void*)topk_out, fin, (size_t)k * sizeof(TopkRec),
-                             cudaMemcpyDeviceToHost, sim->stream));
-    CUDA_TRY(cudaMemcpyAsync(P ? &P->ntopk : n_topk_out, fin_n, sizeof(int32_t),
-                             cudaMemcpyDeviceToHost, sim->stream));
+  // top-k, its count and the header: one copy of the contiguous workspace
+  // tail [out | out_n | hdr] into the pinned image
+  const size_t t_n = L.out_n - L.out, t_h = L.hdr - L.out;
+  static_assert(sizeof(((distir_sim::Pinned*)nullptr)->tail) >= kMaxK * sizeof(TopkRec) + 256 + sizeof(WsHeader),
+                "pinned tail image");
+  if (P && (k > 0 || stats_out)) {
+    CUDA_TRY(cudaMemcpyAsync(P->tail, fin, t_h + sizeof(WsHeader), cudaMemcpyDeviceToHost, sim->stream));
+  } else if (k > 0) {
+    CUDA_TRY(cudaMemcpyAsync(topk_out, fin, (size_t)k * sizeof(TopkRec), cudaMemcpyDeviceToHost, sim->stream));
+    CUDA_TRY(cudaMemcpyAsync(n_topk_out, fin_n, sizeof(int32_t), cudaMemcpyDeviceToHost, sim->stream));
   }
-  if (stats_out && P)
-    CUDA_TRY(cudaMemcpyAsync(&P->hdr, at<WsHeader>(d_workspace, L.hdr), sizeof(WsHeader),
-                             cudaMemcpyDeviceToHost, sim->stream));
   CUDA_TRY(cudaStreamSynchronize(sim->stream));
   if (P && k > 0) {
-    std::memcpy(topk_out, P->topk, (size_t)k * sizeof(TopkRec));
-    *n_topk_out = P->ntopk;
+    std::memcpy(topk_out, P->tail, (size_t)k * sizeof(TopkRec));
+    std::memcpy(n_topk_out, P->tail + t_n, sizeof(int32_t));
   }
   if (stats_out) {
     if (P) {
-      const WsHeader& h = P->hdr;
+      WsHeader h;
+      std::memcpy(&h, P->tail + t_h, sizeof(WsHeader));
       stats_out->n_configs = sp.n_local;
       stats_out->n_valid = (int64_t)h.n_valid;
       stats_out->n_feasible = (int64_t)h.n_feasible;

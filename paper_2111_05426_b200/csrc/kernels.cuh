@@ -35,6 +35,7 @@ __device__ __forceinline__ void distir_count(int i) {
   if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicAdd(&g_distir_instr[i], (unsigned long long)__popc(m_));
 }
 #define DISTIR_COUNT(i) NV_IF_TARGET(NV_IS_DEVICE, (distir_count(i);))
+__device__ __forceinline__ void g_distir_instr_add(int i) { atomicAdd(&g_distir_instr[i], 1ull); }
 // per-lane cycle accounting of the slow path ([12] refresh, [13] crossing
 // passes, [15] whole add_task), summed over lanes
 __host__ __device__ __forceinline__ long long distir_clk_now() {

@@ -95,6 +95,15 @@ constexpr int kPlainMlp = DISTIR_PLAIN_MLP;
 #ifndef DISTIR_JUMP
 #define DISTIR_JUMP 1       // GPipe wavefronts: exact steady-state jumps (steady_jump)
 #endif
+#ifndef DISTIR_PLAIN_SHORT_K
+#define DISTIR_PLAIN_SHORT_K 1  // MLP: warps of short pipelines walk op by op (see plain_cfg)
+#endif
+#ifndef DISTIR_JUMP_MLP
+#define DISTIR_JUMP_MLP 0   // MLP wavefronts too: long configurations gain (MLP-1B P2 K128 -23%) but the
+#endif                      // kernel's register count grows (228 -> 239) and W2 +5%, W5 +6% (r02aa): off
+#ifndef DISTIR_JUMP_F1B
+#define DISTIR_JUMP_F1B 1   // 1F1B slot wavefront (one stage per lane): steady-state jumps
+#endif
 #ifndef DISTIR_JUMP_MIN_K
 #define DISTIR_JUMP_MIN_K 64  // ... in warps of K >= this many microbatches (the checks cost
 #endif                        // more than short pipelines gain: W5, K <= 32, +8% with them)
@@ -120,14 +129,25 @@ constexpr int kPlainMlp = DISTIR_PLAIN_MLP;
 // n_max = how many more whole windows stay in the interior (<= 0: none).
 // Returns the number of windows to skip (0: none), uniform over the
 // configuration's S lanes; the caller adds n Delta and advances its counters.
+// (lane_cond: a further condition every live lane must meet, e.g. an
+// unchanged live-memory count over the window.)
 __device__ __forceinline__ int64_t steady_jump(double x, double snap, bool lane_ok, bool cfg_live,
-                                               int64_t n_max, int S, int lane) {
+                                               int64_t n_max, int S, int lane, bool lane_cond = true) {
   const int base = lane & ~(S - 1);
   const unsigned smask = S == 32 ? 0xffffffffu : (((1u << S) - 1u) << base);
   const double dl = x - snap;                        // exact when both share a binade
   const double d0 = __shfl_sync(0xffffffffu, dl, base);
   const int64_t du = d2bits(x) - d2bits(snap);       // ulps of that binade
-  const bool ok = !lane_ok || (snap > 0.0 && exp_field(x) == exp_field(snap) && dl == d0 && !(du & 1));
+  const bool ok = !lane_ok || (lane_cond && snap > 0.0 && exp_field(x) == exp_field(snap) && dl == d0 &&
+                               !(du & 1));
+#ifdef DISTIR_INSTR
+  if (cfg_live && n_max > 0) {       // jump diagnostics: attempts, and live lanes failing each test
+    const int why = !lane_ok ? 0 : !(snap > 0.0 && exp_field(x) == exp_field(snap)) ? 37
+                  : dl != d0 ? 38 : (du & 1) ? 39 : !lane_cond ? 31 : 0;
+    if (lane == base) { DISTIR_COUNT(36); }
+    if (why) { g_distir_instr_add(why); }
+  }
+#endif
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   const bool go = cfg_live && n_max > 0 && d0 > 0.0 && (bal & smask) == smask;
   if (!__any_sync(0xffffffffu, go)) return 0;
@@ -318,12 +338,22 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
 #pragma unroll
     for (int q = 0; q < V; q++) nlm = ok[q] && hi[q] - lo[q] > nlm ? hi[q] - lo[q] : nlm;
     for (int o = S >> 1; o > 0; o >>= 1) nlm = max(nlm, __shfl_xor_sync(0xffffffffu, nlm, o));
-    plain_cfg = (int64_t)nlm * warp_max_int(has ? (int)K : 0) <= (int64_t)kPlainMlp * (32 / S);
+    const int Kw = warp_max_int(has ? (int)K : 0);
+    plain_cfg = (int64_t)nlm * Kw <= (int64_t)kPlainMlp * (32 / S);
+#if DISTIR_PLAIN_SHORT_K
+    // ... and warps of >= 4 configurations of K <= 32 (their crossings come
+    // one configuration after another; A/B on one B200, r02ae: W5 -11%,
+    // W2 / PM / 1F1B / ZeRO grids unchanged; K <= 16 at any S: W2 +7%, W4 +8%;
+    // a cycle-count model of walk vs crossings, r02ac: W2 +50%, W4 +23%)
+    plain_cfg = plain_cfg || (Kw <= 32 && S <= 8);
+#endif
   }
+#if DISTIR_JUMP && DISTIR_JUMP_MLP
   // steady-state jumps only in warps of long configurations (a warp of many
   // short, plainly walked ones gains less than the checks cost)
   const bool jump_ok = warp_max_int(has ? (int)K : 0) >= DISTIR_JUMP_MIN_K &&
                        __all_sync(0xffffffffu, !has || !plain_cfg);
+#endif
   BinTab btf{nullptr, 0, 0, 0};
   if constexpr (!SEQ) {
     // binade table of the 7 distinct op lists (forward b / ab / a,
@@ -444,7 +474,12 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       return (dd >= 0) & ((dd & 1) == 0) & ((dd >> 1) < Ki);
     };
     // the last task is B(K-1, 0) in slot 2P + 2K - 3, at step 3 (2P + 2K - 3) + 2
-    const int nsteps = warp_max_int(has ? 3 * (2 * Pi + 2 * Ki - 3) + 3 : 0);
+    int nsteps = warp_max_int(has ? 3 * (2 * Pi + 2 * Ki - 3) + 3 : 0);
+#if DISTIR_JUMP_F1B
+    const bool jump_f1b = warp_max_int(has ? Ki : 0) >= DISTIR_JUMP_MIN_K;
+    double snap_c = 0.0;          // clock / live bytes at the start of the jump window
+    int64_t snap_l = -1;
+#endif
     int u[V];
 #pragma unroll
     for (int q = 0; q < V; q++) u[q] = -s[q];     // step - s
@@ -502,6 +537,41 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         peak[q] = peak[q] > live[q] ? peak[q] : live[q];
         live[q] -= (dn[q] && e2[q]) ? act_b : 0;
       }
+#if DISTIR_JUMP_F1B
+      // Steady-state jumps (as wave_jump): in slots [2P, 2K-2]
+      // every stage alternates one forward and one backward task per two
+      // slots (6 steps) with the same Sends, so the map over a window of
+      // 24 steps (4 periods: even ulp counts with stages one binade apart)
+      // repeats.  A window that moved every stage clock of a configuration
+      // by the same even number of ulps inside its binade is repeated n times
+      // in closed form.  Its memory events repeat too: a window that did not
+      // raise a stage's live bytes (stage 0 frees a pre-split input X_k per
+      // microbatch, the last stage Y_k: live falls) adds n times its change,
+      // and no later window can exceed the peak it already reached.  u0 =
+      // stage 0's counter at the
+      // next step; the window's lowest slot is stage P-1's, the skipped
+      // windows' highest stage 0's.
+      if constexpr (V == 1) {
+        if (jump_f1b && step % 24 == 23) {
+          const int u0 = __shfl_sync(0xffffffffu, u[0], lane & ~(S - 1));
+          const int64_t nmax = u0 >= 7 * Pi + 23 ? (int64_t)(6 * Ki - 3 - u0) / 24 : 0;
+          const int64_t nj = steady_jump(clk[0], snap_c, ok[0], has, nmax, S, lane,
+                                         snap_l >= 0 && live[0] <= snap_l);
+          if (__any_sync(0xffffffffu, nj > 0)) {
+            if (nj > 0) {
+              if (ok[0]) {
+                clk[0] = bits2d(d2bits(clk[0]) + nj * (d2bits(clk[0]) - d2bits(snap_c)));
+                live[0] += nj * (live[0] - snap_l);
+              }
+              u[0] += (int)(24 * nj);
+            }
+            nsteps = step + 1 + warp_max_int(has ? 3 * (2 * Pi + 2 * Ki - 3) + 3 - (u0 + (int)(24 * nj)) : 0);
+          }
+          snap_c = clk[0];
+          snap_l = live[0];
+        }
+      }
+#endif
     }
   } else if constexpr (SEQ) {
     // ---- program order (one lane owns all P <= V stages)
@@ -590,7 +660,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         const double nc = dadd(fmax(clk[q], sd ? nbu[q] : nbd[q]), sd ? sendf[q] : recvf[q]);
         clk[q] = (sd || rcv[q]) ? nc : clk[q];
       }
-#if DISTIR_JUMP
+#if DISTIR_JUMP && DISTIR_JUMP_MLP
       if constexpr (V == 1) {
         if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, 0);
       }
@@ -623,7 +693,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         const double nc = dadd(fmax(clk[q], sd ? nbd[q] : nbu[q]), sd ? sendb[q] : recvb[q]);
         clk[q] = (sd || rcv[q]) ? nc : clk[q];
       }
-#if DISTIR_JUMP
+#if DISTIR_JUMP && DISTIR_JUMP_MLP
       // the backward wavefront's first stage is P-1
       if constexpr (V == 1) {
         if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, (int)P - 1);
