@@ -486,6 +486,8 @@ def main():
         value = ops_all / (ms_step / 1e3)
         cfg = bench_config(args.workload, grid, n_total, k, n_gpus)
         cfg["nccl_merge"] = comm is not None
+        if comm is not None:   # the a8 communicator: one rank per GPU, made by distir_nccl_comm_init
+            cfg["nccl_comm"] = {"n_ranks": world, "init": "ncclCommInitRank via distir_nccl_comm_init"}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
             "steps": K, "warmup": args.warmup, "ms_per_step": ms_step,

@@ -217,6 +217,16 @@ distir_status distir_grid_size(const distir_sim* sim, const distir_grid_spec* sp
 distir_status distir_workspace_size(const distir_sim* sim, int64_t n_configs,
                                     size_t* bytes);
 
+/* Packed host layout of the per-configuration results for n_configs
+ * configurations: byte offsets of makespan / peak / reason (offsets[0..2],
+ * offsets[0] == 0) in one host buffer of *bytes bytes.  When the three
+ * output pointers of distir_grid_eval / _sharded (single rank) sit at these
+ * offsets of one buffer, the results arrive in ONE device->host copy, which
+ * also writes the (unspecified) padding between the arrays; any other
+ * placement is copied array by array.  Pure host arithmetic. */
+distir_status distir_result_layout(const distir_sim* sim, int64_t n_configs, int64_t offsets[3],
+                                   size_t* bytes);
+
 /* Evaluate a grid (spec != NULL, configs == NULL) or an explicit list
  * (spec == NULL, configs/n_configs) on this handle's GPU, synchronously.
  * All outputs are HOST buffers owned by the caller:

@@ -134,7 +134,7 @@ EXPORTS = ("distir_sim_create", "distir_sim_destroy", "distir_grid_size",
            "distir_nccl_comm_init", "distir_nccl_comm_destroy",
            "distir_shard_indices", "distir_raw_workspace_size",
            "distir_raw_eval", "distir_topk_merge", "distir_last_error",
-           "distir_version")
+           "distir_version", "distir_result_layout")
 
 
 class DistirError(RuntimeError):
@@ -159,6 +159,7 @@ def _load():
     L.distir_sim_destroy.restype = None
     L.distir_grid_size.argtypes = [vp, P(distir_grid_spec), P(i64)]
     L.distir_workspace_size.argtypes = [vp, i64, P(ctypes.c_size_t)]
+    L.distir_result_layout.argtypes = [vp, i64, P(i64), P(ctypes.c_size_t)]
     L.distir_grid_eval.argtypes = [vp, P(distir_grid_spec), P(distir_config), i64,
                                    i32, vp, ctypes.c_size_t, vp, vp, vp, vp,
                                    P(i32), P(distir_stats)]
@@ -337,13 +338,24 @@ class Simulator:
         outs = {}
         if per_config:
             bufs = getattr(self, "_host_bufs", None)
-            if bufs is None or bufs[0].numel() < max(n, 1) or bufs[3] != pinned:
+            if bufs is None or bufs[4] != n or bufs[3] != pinned:
+                # the library's packed result layout for n configurations
+                # (distir_result_layout): the three arrays arrive in one
+                # copy.  One pinned buffer, grown when too small, carved per n
+                # (so copy=False views are overwritten by the next call)
                 m = max(n, 1)
-                bufs = (torch.empty(m, dtype=torch.float64, pin_memory=pinned),
-                        torch.empty(m, dtype=torch.int64, pin_memory=pinned),
-                        torch.empty(m, dtype=torch.int32, pin_memory=pinned), pinned)
+                off = (ctypes.c_int64 * 3)()
+                nb = ctypes.c_size_t()
+                _check(lib.distir_result_layout(self.handle, m, off, ctypes.byref(nb)))
+                raw = getattr(self, "_host_raw", None)
+                if raw is None or raw.numel() < nb.value or self._host_raw_pinned != pinned:
+                    raw = self._host_raw = torch.empty(nb.value, dtype=torch.uint8, pin_memory=pinned)
+                    self._host_raw_pinned = pinned
+                bufs = (raw[off[0]:off[0] + 8 * m].view(torch.float64),
+                        raw[off[1]:off[1] + 8 * m].view(torch.int64),
+                        raw[off[2]:off[2] + 4 * m].view(torch.int32), pinned, n)
                 self._host_bufs = bufs
-                # numpy views and raw pointers, made once per buffer set
+                # numpy views and raw pointers, made once per carving
                 self._host_np = tuple(t.numpy() for t in bufs[:3])
                 self._host_ptr = tuple(ctypes.c_void_p(t.data_ptr()) for t in bufs[:3])
             outs = {"makespan": bufs[0], "peak": bufs[1], "reason": bufs[2]}

@@ -849,6 +849,21 @@ distir_status distir_workspace_size(const distir_sim* sim, int64_t n_configs, si
   return DISTIR_OK;
 }
 
+distir_status distir_result_layout(const distir_sim* sim, int64_t n_configs, int64_t offsets[3],
+                                   size_t* bytes) {
+  g_err.clear();
+  distir_status s;
+  if ((s = check_handle(sim)) != DISTIR_OK) return s;
+  if (!offsets || !bytes || n_configs < 0) return fail(DISTIR_E_INVALID_ARG, "offsets / bytes / n_configs");
+  // the device sections ms | pk | rs of the workspace (Layout), back to back
+  const Layout L = layout(n_configs, 0);
+  offsets[0] = 0;
+  offsets[1] = (int64_t)(L.pk - L.ms);
+  offsets[2] = (int64_t)(L.rs - L.ms);
+  *bytes = (L.rs - L.ms) + (size_t)(n_configs > 0 ? n_configs : 1) * 4;
+  return DISTIR_OK;
+}
+
 distir_status distir_grid_upload(distir_sim* sim, const distir_grid_spec* spec,
                                  const distir_config* configs, int64_t n_configs, int32_t rank,
                                  int32_t n_ranks, void* d_workspace, size_t ws_bytes,
@@ -941,9 +956,18 @@ distir_status distir_grid_eval_sharded(distir_sim* sim, const distir_grid_spec* 
       if (n_ranks == 1) return cudaMemcpyAsync(dst, src, w * n, cudaMemcpyDeviceToHost, sim->stream);
       return cudaMemcpy2DAsync(dst, pitch * w, src, w, w, n, cudaMemcpyDeviceToHost, sim->stream);
     };
-    if (makespan_out) CUDA_TRY(get(makespan_out + rank, at<double>(d_workspace, L.ms), 8));
-    if (peak_out) CUDA_TRY(get(peak_out + rank, at<int64_t>(d_workspace, L.pk), 8));
-    if (reason_out) CUDA_TRY(get(reason_out + rank, at<uint32_t>(d_workspace, L.rs), 4));
+    const char* m0 = reinterpret_cast<const char*>(makespan_out);
+    const bool packed = n_ranks == 1 && makespan_out && peak_out && reason_out &&
+                        reinterpret_cast<const char*>(peak_out) - m0 == (ptrdiff_t)(L.pk - L.ms) &&
+                        reinterpret_cast<const char*>(reason_out) - m0 == (ptrdiff_t)(L.rs - L.ms);
+    if (packed) {          // distir_result_layout: one copy of ms | pk | rs
+      CUDA_TRY(cudaMemcpyAsync(makespan_out, at<double>(d_workspace, L.ms), (L.rs - L.ms) + (size_t)n * 4,
+                               cudaMemcpyDeviceToHost, sim->stream));
+    } else {
+      if (makespan_out) CUDA_TRY(get(makespan_out + rank, at<double>(d_workspace, L.ms), 8));
+      if (peak_out) CUDA_TRY(get(peak_out + rank, at<int64_t>(d_workspace, L.pk), 8));
+      if (reason_out) CUDA_TRY(get(reason_out + rank, at<uint32_t>(d_workspace, L.rs), 4));
+    }
   }
   distir_sim::Pinned* P = sim->pin;
   // top-k, its count and the header: one copy of the contiguous workspace
