@@ -101,6 +101,9 @@ constexpr int kPlainMlp = DISTIR_PLAIN_MLP;
 #ifndef DISTIR_JUMP_MLP
 #define DISTIR_JUMP_MLP 0   // MLP wavefronts too: long configurations gain (MLP-1B P2 K128 -23%) but the
 #endif                      // kernel's register count grows (228 -> 239) and W2 +5%, W5 +6% (r02aa): off
+#ifndef DISTIR_JUMP_MLP2
+#define DISTIR_JUMP_MLP2 1  // MLP GPipe wavefronts with two stages per lane (32 < P <= 64)
+#endif
 #ifndef DISTIR_JUMP_F1B
 #define DISTIR_JUMP_F1B 1   // 1F1B slot wavefront (one stage per lane): steady-state jumps
 #endif
@@ -186,6 +189,46 @@ __device__ __forceinline__ void wave_jump(int w, int& nsteps, double& clk, doubl
     nsteps = w + 1 + warp_max_int(has ? (int)(2 * K + P - 2) - (J + (int)(8 * nj)) : 0);
   }
   snap = clk;
+}
+
+// The same check for two stages per lane (32 < P <= 64: S = 32, one
+// configuration per warp; lane l holds stages l and l + 32).  Every live
+// stage must show the shift of stage 0 (lane 0, first slot).
+__device__ __forceinline__ void wave_jump2(int w, int& nsteps, double (&clk)[2], double (&snap)[2],
+                                           int (&kk)[2], const bool (&ok)[2], bool has, int64_t P,
+                                           int64_t K, int lane, int first) {
+  if ((w & 7) != 7) return;
+  const int k0 = __shfl_sync(0xffffffffu, kk[0], first & 31);
+  const int k1 = __shfl_sync(0xffffffffu, kk[1], first & 31);
+  const int J = (first >> 5) ? k1 : k0;
+  const int64_t nmax = J >= P + 7 ? (2 * K - J) / 8 : 0;
+  const double d0 = __shfl_sync(0xffffffffu, clk[0] - snap[0], 0);
+  bool good = true;
+  int64_t n = nmax;
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const int64_t du = d2bits(clk[q]) - d2bits(snap[q]);
+    const bool lok = snap[q] > 0.0 && exp_field(clk[q]) == exp_field(snap[q]) && clk[q] - snap[q] == d0 &&
+                     !(du & 1);
+    good = good && (!ok[q] || lok);
+    if (ok[q] && lok && du > 0) {
+      const int64_t room = ((int64_t)(exp_field(clk[q]) + 1) << 52) - 1 - d2bits(clk[q]);
+      n = min(n, room / du);
+    }
+  }
+  if (__all_sync(0xffffffffu, good) && has && nmax > 0 && d0 > 0.0) {
+    for (int o = 16; o > 0; o >>= 1) n = min(n, __shfl_xor_sync(0xffffffffu, n, o));
+    if (n > 0) {
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        if (ok[q]) clk[q] = bits2d(d2bits(clk[q]) + n * (d2bits(clk[q]) - d2bits(snap[q])));
+        kk[q] += (int)(8 * n);
+      }
+      nsteps = w + 1 + (int)(2 * K + P - 2) - (J + (int)(8 * n));
+    }
+  }
+  snap[0] = clk[0];
+  snap[1] = clk[1];
 }
 
 // Segment -> distinct-op-list maps of the task caches (BinTab).
@@ -348,6 +391,11 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     plain_cfg = plain_cfg || (Kw <= 32 && S <= 8);
 #endif
   }
+#if DISTIR_JUMP && DISTIR_JUMP_MLP2
+  // two stages per lane: one configuration per warp, jumps when it is long
+  const bool jump_ok2 = warp_max_int(has ? (int)K : 0) >= DISTIR_JUMP_MIN_K &&
+                        __all_sync(0xffffffffu, !has || !plain_cfg);
+#endif
 #if DISTIR_JUMP && DISTIR_JUMP_MLP
   // steady-state jumps only in warps of long configurations (a warp of many
   // short, plainly walked ones gains less than the checks cost)
@@ -641,6 +689,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) kk[q] = -s[q];
     int nsteps = nsteps0;
     double snap = 0.0;   // clock at the start of the jump window
+    double snap2[2] = {0.0, 0.0};
     for (int w = 0; w < nsteps; w++) {
       wc.steps++;
       bool act[V], rcv[V];
@@ -665,6 +714,11 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
         if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, 0);
       }
 #endif
+#if DISTIR_JUMP && DISTIR_JUMP_MLP2
+      if constexpr (V == 2) {
+        if (jump_ok2) wave_jump2(w, nsteps, clk, snap2, kk, ok, has, P, K, lane, 0);
+      }
+#endif
     }
   }
   // ---- backward wavefront: task (k, s) at step 2k + (P-1-s), then Send s -> s-1
@@ -674,6 +728,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) kk[q] = -(int)(P - 1 - s[q]);
     int nsteps = nsteps0;
     double snap = 0.0;
+    double snap2[2] = {0.0, 0.0};
     for (int w = 0; w < nsteps; w++) {
       wc.steps++;
       bool act[V], rcv[V];
@@ -697,6 +752,11 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
       // the backward wavefront's first stage is P-1
       if constexpr (V == 1) {
         if (jump_ok) wave_jump(w, nsteps, clk[0], snap, kk[0], ok[0], has, P, K, S, lane, (int)P - 1);
+      }
+#endif
+#if DISTIR_JUMP && DISTIR_JUMP_MLP2
+      if constexpr (V == 2) {
+        if (jump_ok2) wave_jump2(w, nsteps, clk, snap2, kk, ok, has, P, K, lane, (int)P - 1);
       }
 #endif
     }

@@ -76,3 +76,15 @@ def test_mlp_1f1b_jumps(sim, topo):
     fired = [_steps_alone(sim, (mi, ti, 1, 1, P, 128, 256)) < 3 * (2 * P + 2 * 128 - 3) + 3
              for P in (2, 4, 8)]
     assert any(fired), fired
+
+
+@pytest.mark.parametrize("topo", ["TB200", "TRD"])
+def test_mlp_gpipe_two_stages_per_lane_jumps(sim, topo):
+    """32 < P <= 64: lanes hold two stages (k_simulate mode 4) and the jump
+    tests both (wave_jump2)."""
+    ti = TOPOS.index(topo)
+    mi = MODELS.index("mlp_w4")
+    cfgs = [(mi, ti, 1, 1, P, K, 1024) for P in (33, 48, 64) for K in (64, 128)]
+    _check_list(sim, cfgs)
+    fired = [_steps_alone(sim, (mi, ti, 1, 1, P, 128, 1024)) < 2 * (2 * 127 + P) for P in (48, 64)]
+    assert any(fired), fired
