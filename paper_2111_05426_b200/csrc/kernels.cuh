@@ -341,7 +341,11 @@ __device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp
       if (cur == kEmptyKey) cur = atomicCAS(&bk[sl].key, kEmptyKey, key);
       if (cur == kEmptyKey || cur == key) { found = sl; break; }
     }
-    atomicAdd(&bk[found].count, 1u);
+    {   // warp-aggregated count: one atomic per bucket per warp (grids put
+        // thousands of configurations in one bucket)
+      const unsigned peers = __match_any_sync(__activemask(), found);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&bk[found].count, (unsigned)__popc(peers));
+    }
     cfg_bucket[q] = found;
     pc_out[q] = PCfg{c.B, (uint32_t)q, (uint16_t)c.K, (uint8_t)c.P,
                      c.mi < 0 ? kSynthModel : (uint8_t)c.mi, (uint8_t)c.topo,
@@ -558,7 +562,15 @@ __device__ __forceinline__ void scatter_body(const SpecBlock* __restrict__ spp, 
        q += (int64_t)nblk * blockDim.x) {
     const uint32_t b = cfg_bucket[q];
     if (b == kEmptyKey) continue;
-    const uint32_t pos = atomicAdd(&bk[b].cursor, 1u);
+    // warp-aggregated cursor: the lanes of one bucket take consecutive
+    // positions from one atomic (any order within a bucket is valid: a
+    // configuration's result does not depend on its warp neighbours)
+    const unsigned peers = __match_any_sync(__activemask(), b);
+    const int lead = __ffs(peers) - 1, me = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (me == lead) base = atomicAdd(&bk[b].cursor, (unsigned)__popc(peers));
+    base = __shfl_sync(peers, base, lead);
+    const uint32_t pos = base + (uint32_t)__popc(peers & ((1u << me) - 1u));
     const uint32_t cpw = bk[b].cpw;
     perm[bk[b].cfg_base + pos] = pc[q];
     if (pos % cpw == 0) {
