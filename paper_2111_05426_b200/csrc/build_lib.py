@@ -23,7 +23,7 @@ BUILD = os.path.join(ROOT, "build", "distir")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-lineinfo", "-O3", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
-SIM_INSTANCES = [(0, m) for m in range(8)] + [(1, m) for m in range(5)]
+SIM_INSTANCES = [(0, m) for m in range(9)] + [(1, m) for m in range(5)]
 
 
 def sources():

@@ -24,14 +24,18 @@ constexpr int kBucketSlots = kNumBuckets + 4;   // + MLP, GPT-2, MLP-1F1B, MLP-Z
 // 32 < P <= 64, and the catch-all buckets); mode 5 (MLP only): the 1F1B
 // co-simulation, one lane per stage, P <= 32; mode 6 (MLP only): ZeRO (f4),
 // one lane per (stage, replica), next_pow2(P) * D <= 32; mode 7 (MLP only):
-// 1F1B with two stages per lane, 32 < P <= 64, and the 1F1B catch-all.
-constexpr int kModes = 8;
+// 1F1B with two stages per lane, 32 < P <= 64, and the 1F1B catch-all;
+// mode 8 (MLP only): mode 3 for warps that walk every task op by op
+// (mlp_plain_shape), without the cached paths -- fewer registers, more
+// warps per SM.
+constexpr int kModes = 9;
 constexpr int kGroups = 2 * kModes;
 constexpr int kNumClasses = 40;     // weight classes (LPT order of items)
 constexpr int kMaxSplit = 5;        // configs per item divided by up to 2^5
 constexpr double kPlanBudgetX = 1.0; // k_plan splits while items <= X x resident warps
 struct PlanBudget {                 // resident warps of each simulate kernel
   uint32_t warps[kGroups];
+  uint32_t launched;                  // the simulate kernels enqueued (SpecBlock.f1b)
 };
 // Binade tables (exact_add.cuh BinTab) of the wavefront simulate kernels:
 // the first kTabCfgs configurations of a warp get one.

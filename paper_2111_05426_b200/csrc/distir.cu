@@ -290,7 +290,7 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
     sp.synth_seed = g->synth_seed;
     n_total = g->synth_count;
     // synthetic sweep: GPipe MLP and GPT-2, P up to 64
-    sp.f1b = gbit(0, 3) | gbit(0, 4) | gbit(1, 3) | gbit(1, 4);
+    sp.f1b = gbit(0, 3) | gbit(0, 8) | gbit(0, 4) | gbit(1, 3) | gbit(1, 4);
     return DISTIR_OK;
   }
   sp.mode = MODE_GRID;
@@ -339,7 +339,21 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
       const DModel& M = sim->models[g->models[mi]];
       if (M.kind == 0 && M.zero) m |= gbit(0, 6);   // ZeRO with D > 1, either schedule
       if (M.kind == 0 && M.sched == 1) { m |= gbit(0, 5) | (wmax > 32 ? gbit(0, 7) : 0); continue; }
-      m |= gbit(M.kind, 3);
+      if (M.kind == 0) {
+        // the plain-walk kernel or the cached one, as the grid's (P, K)
+        // shapes need (k_plan's mlp_plain_shape on every P <= 32)
+        for (int32_t P = 1; P <= (wmax < 32 ? wmax : 32); P <<= 1) {
+          const int nk = (sp.k_mode == 0 && P == 1) ? 1 : g->n_k;
+          for (int i = 0; i < nk; i++) {
+            const int32_t K = (sp.k_mode == 0 && P == 1) ? 1 : g->k_set[i];
+            m |= mlp_plain_shape((uint32_t)M.L, (uint32_t)P, (uint32_t)(K < 255 ? K : 255))
+                     ? gbit(0, 8) : gbit(0, 3);
+          }
+        }
+      } else {
+        m |= gbit(M.kind, 3);
+      }
+      if (m & gbit(0, 3)) m &= ~gbit(0, 8);      // mixed shapes: one kernel walks both
       if (wmax > 32) m |= gbit(M.kind, 4);
       if (M.kind == 0 && M.zero) m |= gbit(0, 6);
     }
@@ -470,6 +484,7 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   PlanBudget pb;
   for (int g = 0; g < kGroups; g++)
     pb.warps[g] = (uint32_t)(sim->plan_x * sim->sim_grid[g] * (sim_tpb(g / kModes, g % kModes) / 32));
+  pb.launched = sp.f1b;
   // (one cooperative kernel with grid barriers instead of these four was
   // measured 10 us slower per launch on a B200 and dropped)
   k_reset<<<(kBucketSlots + 255) / 256, 256, 0, st>>>(bk, hdr);
@@ -512,19 +527,11 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     const int tpb = sim_tpb(kd, md), sm = sim_smem(kd, md);
     cudaError_t e = cudaErrorInvalidValue;
     switch (g) {
-      case 0: e = sim_launch_0_0(grid, tpb, sm, st, sa); break;
-      case 1: e = sim_launch_0_1(grid, tpb, sm, st, sa); break;
-      case 2: e = sim_launch_0_2(grid, tpb, sm, st, sa); break;
-      case 3: e = sim_launch_0_3(grid, tpb, sm, st, sa); break;
-      case 4: e = sim_launch_0_4(grid, tpb, sm, st, sa); break;
-      case 5: e = sim_launch_0_5(grid, tpb, sm, st, sa); break;
-      case 6: e = sim_launch_0_6(grid, tpb, sm, st, sa); break;
-      case 7: e = sim_launch_0_7(grid, tpb, sm, st, sa); break;
-      case 8: e = sim_launch_1_0(grid, tpb, sm, st, sa); break;
-      case 9: e = sim_launch_1_1(grid, tpb, sm, st, sa); break;
-      case 10: e = sim_launch_1_2(grid, tpb, sm, st, sa); break;
-      case 11: e = sim_launch_1_3(grid, tpb, sm, st, sa); break;
-      case 12: e = sim_launch_1_4(grid, tpb, sm, st, sa); break;
+#define DISTIR_CASE(KD, MD) case KD * kModes + MD: e = sim_launch_##KD##_##MD(grid, tpb, sm, st, sa); break;
+      DISTIR_CASE(0, 0) DISTIR_CASE(0, 1) DISTIR_CASE(0, 2) DISTIR_CASE(0, 3) DISTIR_CASE(0, 4)
+      DISTIR_CASE(0, 5) DISTIR_CASE(0, 6) DISTIR_CASE(0, 7) DISTIR_CASE(0, 8)
+      DISTIR_CASE(1, 0) DISTIR_CASE(1, 1) DISTIR_CASE(1, 2) DISTIR_CASE(1, 3) DISTIR_CASE(1, 4)
+#undef DISTIR_CASE
       default: break;
     }
     CUDA_TRY(e);
@@ -672,8 +679,13 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
       kinds |= 1u << (zero ? 3 : M.kind == 0 && M.sched == 1 ? 2 : M.kind);
       if (zero) m |= gbit(0, 6);
       else if (M.kind == 0 && M.sched == 1) m |= configs[i].pp > 32 ? gbit(0, 7) : gbit(0, 5);
-      else m |= gbit(M.kind, configs[i].pp > 32 ? 4 : 3);
+      else if (configs[i].pp > 32) m |= gbit(M.kind, 4);
+      else if (M.kind == 0 && mlp_plain_shape((uint32_t)M.L, (uint32_t)configs[i].pp,
+                                              (uint32_t)(configs[i].microbatches < 255 ? configs[i].microbatches : 255)))
+        m |= gbit(0, 8);
+      else m |= gbit(M.kind, 3);
     }
+    if (m & gbit(0, 3)) m &= ~gbit(0, 8);        // mixed shapes: one kernel walks both
     if (n_configs > kNumBuckets / 2)
       m |= ((kinds & 1) ? gbit(0, 4) : 0) | ((kinds & 2) ? gbit(1, 4) : 0) |
            ((kinds & 4) ? gbit(0, 7) : 0);
@@ -779,10 +791,14 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sim->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   int per_sm[kGroups] = {};
-  const void* fns[kGroups] = {
-      sim_fn_0_0(), sim_fn_0_1(), sim_fn_0_2(), sim_fn_0_3(), sim_fn_0_4(), sim_fn_0_5(),
-      sim_fn_0_6(), sim_fn_0_7(), sim_fn_1_0(), sim_fn_1_1(), sim_fn_1_2(), sim_fn_1_3(),
-      sim_fn_1_4(), nullptr, nullptr, nullptr};
+  const void* fns[kGroups] = {};
+  {
+    const void* k0[] = {sim_fn_0_0(), sim_fn_0_1(), sim_fn_0_2(), sim_fn_0_3(), sim_fn_0_4(),
+                        sim_fn_0_5(), sim_fn_0_6(), sim_fn_0_7(), sim_fn_0_8()};
+    const void* k1[] = {sim_fn_1_0(), sim_fn_1_1(), sim_fn_1_2(), sim_fn_1_3(), sim_fn_1_4()};
+    for (int m = 0; m < 9; m++) fns[m] = k0[m];
+    for (int m = 0; m < 5; m++) fns[kModes + m] = k1[m];
+  }
   for (int g = 0; g < kGroups && e == cudaSuccess; g++) {
     if (!fns[g]) continue;
     const int smem = sim_smem(g / kModes, g % kModes);
@@ -1092,7 +1108,8 @@ int distir_debug_counters(unsigned long long* out, int n) {
   int r = 0;
   r |= sim_counters_0_0(out, n); r |= sim_counters_0_1(out, n); r |= sim_counters_0_2(out, n);
   r |= sim_counters_0_3(out, n); r |= sim_counters_0_4(out, n); r |= sim_counters_0_5(out, n);
-  r |= sim_counters_0_6(out, n); r |= sim_counters_0_7(out, n); r |= sim_counters_1_0(out, n);
+  r |= sim_counters_0_6(out, n); r |= sim_counters_0_7(out, n); r |= sim_counters_0_8(out, n);
+  r |= sim_counters_1_0(out, n);
   r |= sim_counters_1_1(out, n); r |= sim_counters_1_2(out, n); r |= sim_counters_1_3(out, n);
   r |= sim_counters_1_4(out, n);
   return r;

@@ -398,6 +398,25 @@ __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
 // more resident warps than items, the heaviest classes are split into items
 // of fewer configurations (cpw halved per step, heaviest class first).
 constexpr int kPlanThreads = 1024;   // k_plan's block size (distir.cu launch)
+#ifndef DISTIR_PLAIN_KERNEL
+#define DISTIR_PLAIN_KERNEL 1           // route plain MLP warps to k_simulate<0, 8>
+#endif
+constexpr int kPlainMlpRule = 32;       // = DISTIR_PLAIN_MLP (simulate.cuh), the plain_cfg rule
+// Whether an MLP GPipe warp shape (L layers, P <= 32 stages, K microbatches
+// as the bucket key holds it, min(K, 255)) walks op by op.  k_plan routes
+// such buckets to k_simulate<0, 8> when the host launched it: for a grid or
+// list whose MLP GPipe shapes are ALL plain (else the plain configurations
+// stay in k_simulate<0, 3>, which walks them too: two simulate kernels run
+// one after the other, and the second would add its time), and for the
+// synthetic sweep.
+__host__ __device__ __forceinline__ bool mlp_plain_shape(uint32_t L, uint32_t P, uint32_t K) {
+  uint32_t lanes = 1;
+  while (lanes < P) lanes <<= 1;
+  const uint32_t nlm = (L + P - 1) / P;
+  return DISTIR_PLAIN_KERNEL && P <= 32 &&
+         ((unsigned long long)nlm * K <= (unsigned long long)kPlainMlpRule * (32 / lanes) ||
+          (K <= 32 && lanes <= 8));
+}
 __device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
                                           const PlanBudget& budget) {
   __shared__ unsigned int s_items[kGroups][kNumClasses];
@@ -453,6 +472,13 @@ __device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __r
         lanes = P < 32 ? pow2ceil32(P) : 32;
         mode = (B.key >> 25) & 1 ? (P > 32 ? 7 : 5) : P > 32 ? 4 : 3;
         est = (2ull * K + P) * (kind ? 1ull : 2ull) * 2;
+        // MLP GPipe warps of short pipelines walk every task op by op
+        // (run_mlp's plain_cfg rule, decided here from the bucket's shape):
+        // their own kernel, without the cached paths' registers, fits more
+        // warps per SM
+        if (kind == 0 && mode == 3 && ((budget.launched >> 8) & 1u) &&
+            mlp_plain_shape(((B.key >> 7) & 1023) + 1, P, K))
+          mode = 8;
       }
       cls = 63 - __clzll(est + 1);
       if (cls >= kNumClasses) cls = kNumClasses - 1;
@@ -775,7 +801,7 @@ __host__ __device__ constexpr int sim_tpb(int kind, int mode) {   // threads per
 // kTabCfgs configurations of a warp (S >= 2 lanes each) get one, filled by
 // their lanes before the walk: binades x 2 parities x segments doubles.
 __host__ __device__ constexpr int sim_tab(int kind, int mode) {   // doubles per config
-  return mode < 3 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3
+  return mode < 3 || mode == 8 ? 0 : kind == 1 ? kTabBinadesGpt2 * 2 * 3
                      : kTabBinadesMlp * 2 * (mode == 6 ? 9 : 7);
 }
 __host__ __device__ constexpr int sim_tab_cfgs(int kind) {     // configurations with a table
@@ -792,7 +818,11 @@ template <int KIND, int MODE>
 #ifndef DISTIR_SIM_MINB
 #define DISTIR_SIM_MINB 1      // min resident blocks per SM asked of ptxas (register cap)
 #endif
-__global__ void __launch_bounds__(sim_tpb(KIND, MODE), DISTIR_SIM_MINB) k_simulate(const SpecBlock* __restrict__ spp,
+#ifndef DISTIR_PLAIN_MINB
+#define DISTIR_PLAIN_MINB 4    // the plain MLP kernel (mode 8): 4 blocks per SM (<= 128 registers)
+#endif
+__global__ void __launch_bounds__(sim_tpb(KIND, MODE), MODE == 8 ? DISTIR_PLAIN_MINB : DISTIR_SIM_MINB)
+k_simulate(const SpecBlock* __restrict__ spp,
                                                   const DExplicit* __restrict__ ex,
                                                   const Bucket* __restrict__ bk,
                                                   const Item* __restrict__ items,
@@ -867,6 +897,12 @@ __global__ void __launch_bounds__(sim_tpb(KIND, MODE), DISTIR_SIM_MINB) k_simula
 #endif
     if constexpr (KIND == 1) run_gpt2<V, SEQ>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
     else if constexpr (MODE == 6) run_mlp_zero(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+    else if constexpr (MODE == 8) {   // warps of short pipelines: every task walked op by op
+      if (warp_max_int(has ? c.M.rc : 0))
+        run_mlp<1, false, false, true, true>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+      else
+        run_mlp<1, false, false, false, true>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
+    }
     else if (warp_max_int(has ? c.M.rc : 0))          // bucket key: warp-uniform
       run_mlp<V, SEQ, MODE == 5 || MODE == 7, true>(c, tp, has, sl, S, lane, row, tab, ms, pk, wc);
     else

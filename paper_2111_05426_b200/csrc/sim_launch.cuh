@@ -29,6 +29,7 @@ struct SimArgs {
   const void* sim_fn_##KD##_##MD();
 DISTIR_SIM_DECL(0, 0) DISTIR_SIM_DECL(0, 1) DISTIR_SIM_DECL(0, 2) DISTIR_SIM_DECL(0, 3)
 DISTIR_SIM_DECL(0, 4) DISTIR_SIM_DECL(0, 5) DISTIR_SIM_DECL(0, 6) DISTIR_SIM_DECL(0, 7)
+DISTIR_SIM_DECL(0, 8)
 DISTIR_SIM_DECL(1, 0) DISTIR_SIM_DECL(1, 1) DISTIR_SIM_DECL(1, 2) DISTIR_SIM_DECL(1, 3)
 DISTIR_SIM_DECL(1, 4)
 #undef DISTIR_SIM_DECL
@@ -36,6 +37,7 @@ DISTIR_SIM_DECL(1, 4)
 #define DISTIR_SIM_CNT(KD, MD) int sim_counters_##KD##_##MD(unsigned long long* out, int n);
 DISTIR_SIM_CNT(0, 0) DISTIR_SIM_CNT(0, 1) DISTIR_SIM_CNT(0, 2) DISTIR_SIM_CNT(0, 3)
 DISTIR_SIM_CNT(0, 4) DISTIR_SIM_CNT(0, 5) DISTIR_SIM_CNT(0, 6) DISTIR_SIM_CNT(0, 7)
+DISTIR_SIM_CNT(0, 8)
 DISTIR_SIM_CNT(1, 0) DISTIR_SIM_CNT(1, 1) DISTIR_SIM_CNT(1, 2) DISTIR_SIM_CNT(1, 3)
 DISTIR_SIM_CNT(1, 4)
 #undef DISTIR_SIM_CNT

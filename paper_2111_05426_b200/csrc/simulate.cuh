@@ -258,7 +258,7 @@ __device__ __forceinline__ void alt_segs(double* row, int oa, int na, int p0, in
   a = Seg{row + oa, na, n1 & 1};
 }
 
-template <int V, bool SEQ, bool F1B, bool RC>
+template <int V, bool SEQ, bool F1B, bool RC, bool PLAIN = false>
 __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, int lane,
                         double* row, double* tab, double& ms_out, int64_t& peak_out, WorkCount& wc) {
   const int64_t L = c.M.L, d = c.M.d, e = c.M.e, D = c.D, T = c.T, P = c.P, K = c.K;
@@ -382,7 +382,7 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     for (int q = 0; q < V; q++) nlm = ok[q] && hi[q] - lo[q] > nlm ? hi[q] - lo[q] : nlm;
     for (int o = S >> 1; o > 0; o >>= 1) nlm = max(nlm, __shfl_xor_sync(0xffffffffu, nlm, o));
     const int Kw = warp_max_int(has ? (int)K : 0);
-    plain_cfg = (int64_t)nlm * Kw <= (int64_t)kPlainMlp * (32 / S);
+    plain_cfg = PLAIN || (int64_t)nlm * Kw <= (int64_t)kPlainMlp * (32 / S);
 #if DISTIR_PLAIN_SHORT_K
     // ... and warps of >= 4 configurations of K <= 32 (their crossings come
     // one configuration after another; A/B on one B200, r02ae: W5 -11%,
