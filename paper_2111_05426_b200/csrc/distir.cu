@@ -190,7 +190,15 @@ struct distir_sim {
   Pinned* pin = nullptr;
   cudaEvent_t pin_ev = nullptr;     // the last H2D from pin->spec
   bool pin_pending = false;
+  // side streams and events of the concurrent simulate kernels (fork / join)
+  cudaStream_t side[kGroups] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kGroups] = {};
   ~distir_sim() {
+    for (int i = 0; i < kGroups; i++) {
+      if (side[i]) cudaStreamDestroy(side[i]);
+      if (join_ev[i]) cudaEventDestroy(join_ev[i]);
+    }
+    if (fork_ev) cudaEventDestroy(fork_ev);
     if (pin) cudaFreeHost(pin);
     if (pin_ev) cudaEventDestroy(pin_ev);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -506,14 +514,24 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   // the simulate kernels the grid can need (SpecBlock.f1b mask, plus the
   // program-order variants when built in); a7 runs inside them, the last one
   // launched merging the per-kernel top-k lists
+  // Several simulate kernels run CONCURRENTLY, one per stream (fork / join
+  // on the library's stream): each is persistent and sized to the whole GPU,
+  // so the next one's blocks start as the previous one's retire -- in its
+  // tail, where its heaviest items leave most SMs idle -- instead of after
+  // it.  Longest pipelines first (they set the tail).
+  static const int kOrder[] = {0 * kModes + 4, 0 * kModes + 7, 1 * kModes + 4, 0 * kModes + 5,
+                               0 * kModes + 6, 1 * kModes + 3, 0 * kModes + 3, 0 * kModes + 8,
+                               0, 1, 2, kModes + 0, kModes + 1, kModes + 2};
   int groups[kGroups], ng = 0;
   if (n > 0) {
-    for (int g = 0; g < kGroups; g++) {
+    for (int g : kOrder) {
       const int md = g % kModes;
       const bool seq = md < 3 && md < DISTIR_SEQ_MAXP && g / kModes <= 1;
       if (seq || (md >= 3 && (sp.f1b & (1u << g)))) groups[ng++] = g;
     }
   }
+  const bool fork = ng > 1 && sim->fork_ev != nullptr;
+  if (fork) CUDA_TRY(cudaEventRecord(sim->fork_ev, st));
   int n_lists = 0;                    // partial top-k lists (one per simulate block)
   for (int i = 0; i < ng; i++) {
     const int g = groups[i];
@@ -525,9 +543,14 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     n_lists += sim->sim_grid[g];
     const int kd = g / kModes, md = g % kModes, grid = sim->sim_grid[g];
     const int tpb = sim_tpb(kd, md), sm = sim_smem(kd, md);
+    cudaStream_t ks = st;
+    if (fork && i > 0) {
+      ks = sim->side[i];
+      CUDA_TRY(cudaStreamWaitEvent(ks, sim->fork_ev, 0));
+    }
     cudaError_t e = cudaErrorInvalidValue;
     switch (g) {
-#define DISTIR_CASE(KD, MD) case KD * kModes + MD: e = sim_launch_##KD##_##MD(grid, tpb, sm, st, sa); break;
+#define DISTIR_CASE(KD, MD) case KD * kModes + MD: e = sim_launch_##KD##_##MD(grid, tpb, sm, ks, sa); break;
       DISTIR_CASE(0, 0) DISTIR_CASE(0, 1) DISTIR_CASE(0, 2) DISTIR_CASE(0, 3) DISTIR_CASE(0, 4)
       DISTIR_CASE(0, 5) DISTIR_CASE(0, 6) DISTIR_CASE(0, 7) DISTIR_CASE(0, 8)
       DISTIR_CASE(1, 0) DISTIR_CASE(1, 1) DISTIR_CASE(1, 2) DISTIR_CASE(1, 3) DISTIR_CASE(1, 4)
@@ -536,6 +559,10 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
     }
     CUDA_TRY(e);
     kernels++;
+    if (fork && i > 0) {
+      CUDA_TRY(cudaEventRecord(sim->join_ev[i], ks));
+      CUDA_TRY(cudaStreamWaitEvent(st, sim->join_ev[i], 0));
+    }
   }
   CUDA_TRY(mark(2));
   if (k > 0) {                        // a7: the top k of the blocks' lists
@@ -836,6 +863,19 @@ distir_status distir_sim_create(const distir_model* models, int32_t n_models,
   const char* ng = getenv("DISTIR_NO_GRAPH");
   sim->use_graph = !(ng && ng[0] == '1');
   sim->enum_grid = sim->num_sms * 8;
+  {   // concurrent simulate kernels (DISTIR_CONCURRENT=0: one after another)
+    const char* cc = getenv("DISTIR_CONCURRENT");
+    bool ok = !(cc && cc[0] == '0') &&
+              cudaEventCreateWithFlags(&sim->fork_ev, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < kGroups; i++)
+      ok = cudaStreamCreateWithFlags(&sim->side[i], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&sim->join_ev[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      if (sim->fork_ev) cudaEventDestroy(sim->fork_ev);
+      sim->fork_ev = nullptr;
+    }
+  }
   *out = sim;
   return DISTIR_OK;
 }
