@@ -216,6 +216,9 @@ namespace {
 
 // bit of simulate kernel (kind, mode) in SpecBlock.f1b
 constexpr uint32_t gbit(int kind, int mode) { return 1u << (kind * kModes + mode); }
+#ifndef DISTIR_PLAIN_MIXED
+#define DISTIR_PLAIN_MIXED 0   // grids mixing plain and cached MLP shapes: both kernels (concurrent)
+#endif
 
 distir_status check_handle(const distir_sim* sim) {
   if (!sim) return fail(DISTIR_E_INVALID_ARG, "sim is NULL");
@@ -361,7 +364,7 @@ distir_status build_spec(const distir_sim* sim, const distir_grid_spec* g, SpecB
       } else {
         m |= gbit(M.kind, 3);
       }
-      if (m & gbit(0, 3)) m &= ~gbit(0, 8);      // mixed shapes: one kernel walks both
+      if (!DISTIR_PLAIN_MIXED && (m & gbit(0, 3))) m &= ~gbit(0, 8);   // mixed shapes: one kernel walks both
       if (wmax > 32) m |= gbit(M.kind, 4);
       if (M.kind == 0 && M.zero) m |= gbit(0, 6);
     }
@@ -712,7 +715,7 @@ distir_status upload(distir_sim* sim, const distir_grid_spec* spec, const distir
         m |= gbit(0, 8);
       else m |= gbit(M.kind, 3);
     }
-    if (m & gbit(0, 3)) m &= ~gbit(0, 8);        // mixed shapes: one kernel walks both
+    if (!DISTIR_PLAIN_MIXED && (m & gbit(0, 3))) m &= ~gbit(0, 8);   // mixed shapes: one kernel walks both
     if (n_configs > kNumBuckets / 2)
       m |= ((kinds & 1) ? gbit(0, 4) : 0) | ((kinds & 2) ? gbit(1, 4) : 0) |
            ((kinds & 4) ? gbit(0, 7) : 0);
