@@ -35,7 +35,10 @@
  *   * Outputs are bit-identical for any sharding, launch shape or GPU count.
  *   * fp64 arithmetic is IEEE binary64 round-to-nearest without FMA
  *     contraction, in the order of §8c C.5.
- *   * A handle is bound to one CUDA device and one stream; it is not
+ *   * A handle is bound to one CUDA device and one stream (when a grid needs
+ *     several simulate kernels they run on the handle's private side
+ *     streams, forked from and joined back into that stream: the caller sees
+ *     stream order as usual); it is not
  *     thread-safe.  Distinct handles are independent.
  *   * The library owns the handle; model/topology arrays are copied at
  *     create.  The caller owns every output buffer and the device workspace
