@@ -181,12 +181,28 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
 // ZeRO with D > 1 runs its own kernel (mode 6) with D lanes per stage
 __device__ __forceinline__ bool is_zero(const Cfg& c) { return c.M.kind == 0 && c.M.zero && c.D > 1; }
 
-__device__ __forceinline__ uint32_t bucket_key(const Cfg& c) {
+#ifndef DISTIR_GPT2_GROUP
+#define DISTIR_GPT2_GROUP 1             // GPT-2 buckets also keyed by the microbatch size (warps of equal costs)
+#endif
+__device__ __forceinline__ uint32_t bucket_key(const Cfg& c, bool group_m) {
   const uint32_t K = (uint32_t)(c.K < 255 ? c.K : 255);
   const uint32_t z = is_zero(c) ? 1u : 0u;
   const uint32_t ld = z ? (uint32_t)(63 - __clzll((unsigned long long)c.D)) : 0u;
-  return (uint32_t)c.M.kind | (uint32_t)(c.P - 1) << 1 | (uint32_t)(c.M.L - 1) << 7 | K << 17 |
-         (uint32_t)(c.M.sched & 1) << 25 | ld << 26 | z << 29 | (uint32_t)(c.M.rc & 1) << 30;
+  uint32_t key = (uint32_t)c.M.kind | (uint32_t)(c.P - 1) << 1 | (uint32_t)(c.M.L - 1) << 7 | K << 17 |
+                 (uint32_t)(c.M.sched & 1) << 25 | ld << 26 | z << 29 | (uint32_t)(c.M.rc & 1) << 30;
+#if DISTIR_GPT2_GROUP
+  // GPT-2 in grids and lists: bits 25-29 (MLP-only fields) carry log2 of the
+  // microbatch size, so a warp's configurations share it -- equal op costs
+  // for equal T and topology, binade crossings in the same steps (W3 k_simulate
+  // 0.1005 -> 0.0915 ms, r02az).  Not for the synthetic sweep (W5 +5 %: its
+  // shapes already fill the hash table's buckets thinly)
+  if (c.M.kind == 1 && group_m) {
+    const int64_t m = c.B / (c.D * c.K);
+    const uint32_t lm = m > 0 ? (uint32_t)(63 - __clzll((unsigned long long)m)) : 0u;
+    key |= (lm < 31 ? lm : 31u) << 25;
+  }
+#endif
+  return key;
 }
 
 // ------------------------------------------------------------ costs (C.5) ---
@@ -332,7 +348,7 @@ __device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp
     op_counts(c, events, steps);
     ev += events; st += steps; nv += 1;
     tk += (unsigned long long)(c.K * c.P * (c.M.kind == 0 ? 2 : 1));
-    const uint32_t key = bucket_key(c);
+    const uint32_t key = bucket_key(c, sp.mode != MODE_SYNTH);
     uint32_t slot = (key * 2654435761u) >> 20;                 // 12-bit hash
     uint32_t found = kOverflowBucket + (is_zero(c) ? 3u : c.M.sched ? 2u : (uint32_t)c.M.kind);
     for (int probe = 0; probe < kNumBuckets; probe++) {
@@ -462,19 +478,20 @@ __device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __r
             : b == kOverflowBucket + 2 ? 7 : (uint32_t)(b - kOverflowBucket) * kModes + 4;
     } else {
       const uint32_t kind = B.key & 1, P = ((B.key >> 1) & 63) + 1, K = (B.key >> 17) & 255;
+      const uint32_t mkey = kind ? (B.key & 0x01FFFFFFu) : B.key;   // GPT-2: bits 25-31 are grouping only
       uint32_t mode;
       unsigned long long est;            // serial chain, in tasks
       if (P <= DISTIR_SEQ_MAXP) {
         lanes = 1;
         mode = P == 1 ? 0 : (P == 2 ? 1 : 2);
         est = (unsigned long long)K * P * (kind ? 1ull : 2ull);
-      } else if ((B.key >> 29) & 1) {    // ZeRO: D lanes per stage
-        lanes = pow2ceil32(P) << ((B.key >> 26) & 7);
+      } else if ((mkey >> 29) & 1) {     // ZeRO: D lanes per stage
+        lanes = pow2ceil32(P) << ((mkey >> 26) & 7);
         mode = 6;
         est = (2ull * K + P) * 4;
       } else {
         lanes = P < 32 ? pow2ceil32(P) : 32;
-        mode = (B.key >> 25) & 1 ? (P > 32 ? 7 : 5) : P > 32 ? 4 : 3;
+        mode = (mkey >> 25) & 1 ? (P > 32 ? 7 : 5) : P > 32 ? 4 : 3;
         est = (2ull * K + P) * (kind ? 1ull : 2ull) * 2;
         // MLP GPipe warps of short pipelines walk every task op by op
         // (run_mlp's plain_cfg rule, decided here from the bucket's shape):
