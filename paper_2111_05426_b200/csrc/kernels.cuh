@@ -182,7 +182,7 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
 __device__ __forceinline__ bool is_zero(const Cfg& c) { return c.M.kind == 0 && c.M.zero && c.D > 1; }
 
 #ifndef DISTIR_GPT2_GROUP
-#define DISTIR_GPT2_GROUP 1             // GPT-2 buckets also keyed by the microbatch size (warps of equal costs)
+#define DISTIR_GPT2_GROUP 0             // GPT-2 buckets also keyed by the microbatch size (experiment, off)
 #endif
 __device__ __forceinline__ uint32_t bucket_key(const Cfg& c, bool group_m) {
   const uint32_t K = (uint32_t)(c.K < 255 ? c.K : 255);
@@ -193,9 +193,10 @@ __device__ __forceinline__ uint32_t bucket_key(const Cfg& c, bool group_m) {
 #if DISTIR_GPT2_GROUP
   // GPT-2 in grids and lists: bits 25-29 (MLP-only fields) carry log2 of the
   // microbatch size, so a warp's configurations share it -- equal op costs
-  // for equal T and topology, binade crossings in the same steps (W3 k_simulate
-  // 0.1005 -> 0.0915 ms, r02az).  Not for the synthetic sweep (W5 +5 %: its
-  // shapes already fill the hash table's buckets thinly)
+  // for equal T and topology, binade crossings in the same steps.  Measured
+  // (r02az, r02ba): W3 k_simulate 0.1005 -> 0.0915 ms, but 15x the buckets
+  // cost k_enumerate / k_plan +7 us and the select +4 us, so the W3 step is
+  // 0.1297 -> 0.1313 ms: off.  (With T as well: k_simulate 0.113 ms.)
   if (c.M.kind == 1 && group_m) {
     const int64_t m = c.B / (c.D * c.K);
     const uint32_t lm = m > 0 ? (uint32_t)(63 - __clzll((unsigned long long)m)) : 0u;
