@@ -1,7 +1,9 @@
 """One evaluation of a named grid through the C ABI (for compute-sanitizer
 runs, tools/sanitize.sh): W1, W4 (two stages per lane, shuffles across the
 lane-31/32 wrap), W4 under 1F1B (the co-simulation), W2 under ZeRO (lane =
-(stage, replica)), W3 (GPT-2) -- plus the device merge of 3 virtual shards.
+(stage, replica)), W3 (GPT-2 and its steady-state jumps), W2 under 1F1B (its
+jumps), a 3,000-configuration synthetic sweep (concurrent simulate kernels,
+the plain MLP kernel) -- plus the device merge of 3 virtual shards.
 usage: python tools/sanitize.py NAME"""
 import os
 import sys
@@ -16,6 +18,11 @@ GRIDS = {
     "W4": W.GRIDS["W4"],
     "W4_1F1B": W.grid_with("W4", models=["mlp_w4_1f1b"]),
     "W2_ZERO": W.grid_with("W2", models=["mlp_1b_zero"]),
+    # the 1F1B steady-state jumps (K up to 128)
+    "W2_1F1B": W.grid_with("W2", models=["mlp_1b_1f1b"]),
+    # the synthetic sweep: five simulate kernels at once (side streams), the
+    # plain MLP kernel (mode 8)
+    "SYN": dict(W.GRIDS["W5"], synth_count=3000),
 }
 
 
