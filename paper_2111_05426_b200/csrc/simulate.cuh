@@ -107,6 +107,9 @@ constexpr int kPlainMlp = DISTIR_PLAIN_MLP;
 #ifndef DISTIR_JUMP_F1B
 #define DISTIR_JUMP_F1B 1   // 1F1B slot wavefront (one stage per lane): steady-state jumps
 #endif
+#ifndef DISTIR_JUMP_F1B2
+#define DISTIR_JUMP_F1B2 1  // ... and with two stages per lane (32 < P <= 64)
+#endif
 #ifndef DISTIR_JUMP_MIN_K
 #define DISTIR_JUMP_MIN_K 64  // ... in warps of K >= this many microbatches (the checks cost
 #endif                        // more than short pipelines gain: W5, K <= 32, +8% with them)
@@ -527,6 +530,8 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
     const bool jump_f1b = warp_max_int(has ? Ki : 0) >= DISTIR_JUMP_MIN_K;
     double snap_c = 0.0;          // clock / live bytes at the start of the jump window
     int64_t snap_l = -1;
+    double snap2c[2] = {0.0, 0.0};
+    int64_t snap2l[2] = {-1, -1};
 #endif
     int u[V];
 #pragma unroll
@@ -619,6 +624,44 @@ __device__ void run_mlp(const Cfg& c, const DTopo& tp, bool has, int sl, int S, 
           snap_l = live[0];
         }
       }
+#if DISTIR_JUMP_F1B2
+      if constexpr (V == 2) {           // two stages per lane (32 < P <= 64): one configuration per warp
+        if (jump_f1b && step % 24 == 23) {
+          const int u0 = __shfl_sync(0xffffffffu, u[0], 0);
+          const int64_t nmax = u0 >= 7 * Pi + 23 ? (int64_t)(6 * Ki - 3 - u0) / 24 : 0;
+          const double d0 = __shfl_sync(0xffffffffu, clk[0] - snap2c[0], 0);
+          bool good = true;
+          int64_t n = nmax;
+#pragma unroll
+          for (int q = 0; q < 2; q++) {
+            const int64_t du = d2bits(clk[q]) - d2bits(snap2c[q]);
+            const bool lok = snap2c[q] > 0.0 && exp_field(clk[q]) == exp_field(snap2c[q]) &&
+                             clk[q] - snap2c[q] == d0 && !(du & 1) && snap2l[q] >= 0 && live[q] <= snap2l[q];
+            good = good && (!ok[q] || lok);
+            if (ok[q] && lok && du > 0) {
+              const int64_t room = ((int64_t)(exp_field(clk[q]) + 1) << 52) - 1 - d2bits(clk[q]);
+              n = min(n, room / du);
+            }
+          }
+          if (__all_sync(0xffffffffu, good) && has && nmax > 0 && d0 > 0.0) {
+            for (int o = 16; o > 0; o >>= 1) n = min(n, __shfl_xor_sync(0xffffffffu, n, o));
+            if (n > 0) {
+#pragma unroll
+              for (int q = 0; q < 2; q++) {
+                if (ok[q]) {
+                  clk[q] = bits2d(d2bits(clk[q]) + n * (d2bits(clk[q]) - d2bits(snap2c[q])));
+                  live[q] += n * (live[q] - snap2l[q]);
+                }
+                u[q] += (int)(24 * n);
+              }
+              nsteps = step + 1 + 3 * (2 * Pi + 2 * Ki - 3) + 3 - (u0 + (int)(24 * n));
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 2; q++) { snap2c[q] = clk[q]; snap2l[q] = live[q]; }
+        }
+      }
+#endif
 #endif
     }
   } else if constexpr (SEQ) {

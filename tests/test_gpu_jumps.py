@@ -88,3 +88,15 @@ def test_mlp_gpipe_two_stages_per_lane_jumps(sim, topo):
     _check_list(sim, cfgs)
     fired = [_steps_alone(sim, (mi, ti, 1, 1, P, 128, 1024)) < 2 * (2 * 127 + P) for P in (48, 64)]
     assert any(fired), fired
+
+
+@pytest.mark.parametrize("topo", ["TB200", "TRD"])
+def test_mlp_1f1b_two_stages_per_lane_jumps(sim, topo):
+    """1F1B with 32 < P <= 64 (k_simulate mode 7): the jump tests both stages
+    of a lane; bit-exact against the oracle."""
+    ti = TOPOS.index(topo)
+    mi = MODELS.index("mlp_w4_1f1b")
+    cfgs = [(mi, ti, 1, 1, P, K, 1024) for P in (33, 48, 64) for K in (64, 128)]
+    _check_list(sim, cfgs)
+    fired = [_steps_alone(sim, (mi, ti, 1, 1, P, 128, 1024)) < 3 * (2 * P + 2 * 128 - 3) + 3 for P in (48, 64)]
+    assert any(fired), fired
