@@ -64,7 +64,7 @@ int ilog2(int64_t x) {
 
 // ------------------------------------------------------------ layout -------
 struct Layout {
-  size_t hdr, spec, ex, bk, cfg_bucket, pc, perm, items, ms, pk, rs, tp, part, part_n, gath, fin,
+  size_t hdr, spec, ex, bk, sub, cfg_bucket, pc, perm, items, ms, pk, rs, tp, part, part_n, gath, fin,
       fin_n, out, out_n, total;
 };
 
@@ -80,6 +80,7 @@ Layout layout(int64_t n_local, int64_t n_explicit) {
   L.spec = take(sizeof(SpecBlock));
   L.ex = take((size_t)(n_explicit > 0 ? n_explicit : 1) * sizeof(DExplicit));
   L.bk = take(kBucketSlots * sizeof(Bucket));
+  L.sub = take((size_t)2 * kBucketSlots * kSubSlots * 4);    // sub-order counts, cursors
   L.cfg_bucket = take(n * 4);
   L.pc = take(n * sizeof(PCfg));
   L.perm = take(n * sizeof(PCfg));
@@ -498,13 +499,14 @@ distir_status enqueue_all(distir_sim* sim, cudaStream_t st, const cudaEvent_t* e
   pb.launched = sp.f1b;
   // (one cooperative kernel with grid barriers instead of these four was
   // measured 10 us slower per launch on a B200 and dropped)
-  k_reset<<<(kBucketSlots + 255) / 256, 256, 0, st>>>(bk, hdr);
+  uint32_t* sub = at<uint32_t>(ws, L.sub);
+  k_reset<<<(kBucketSlots * kSubSlots / 4 + 255) / 256, 256, 0, st>>>(bk, hdr, sub);
   kernels++;
   if (n > 0) {
     const int eg = (int)std::min<int64_t>((n + 255) / 256, sim->enum_grid);
-    k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, pc, hdr);
-    k_plan<<<1, kPlanThreads, 0, st>>>(bk, hdr, pb);
-    k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, pc, perm, items);
+    k_enumerate<<<eg, 256, 0, st>>>(dsp, dex, bk, cb, ms, pk, rs, tpv, pc, hdr, sub);
+    k_plan<<<1, kPlanThreads, 0, st>>>(bk, hdr, pb, sub);
+    k_scatter<<<eg, 256, 0, st>>>(dsp, bk, cb, pc, perm, items, sub);
     kernels += 3;
   }
   CUDA_TRY(mark(1));

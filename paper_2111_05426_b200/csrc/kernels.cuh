@@ -181,6 +181,10 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
 // ZeRO with D > 1 runs its own kernel (mode 6) with D lanes per stage
 __device__ __forceinline__ bool is_zero(const Cfg& c) { return c.M.kind == 0 && c.M.zero && c.D > 1; }
 
+#ifndef DISTIR_SUBORDER
+#define DISTIR_SUBORDER 1               // GPT-2: order a bucket's configurations by microbatch size
+#endif
+constexpr int kSubSlots = 32;           // per-bucket sub-orders (log2 of the microbatch size)
 #ifndef DISTIR_GPT2_GROUP
 #define DISTIR_GPT2_GROUP 0             // GPT-2 buckets also keyed by the microbatch size (experiment, off)
 #endif
@@ -323,7 +327,8 @@ __device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp
                             Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
                             double* __restrict__ ms_out, int64_t* __restrict__ pk_out,
                             uint32_t* __restrict__ rs_out, double* __restrict__ tp_out,
-                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr, int bid, int nblk) {
+                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr,
+                            uint32_t* __restrict__ sub, int bid, int nblk) {
   const SpecBlock& sp = *spp;
   const int64_t nloc = sp.n_local;
   unsigned long long ev = 0, st = 0, nv = 0, tk = 0;
@@ -364,10 +369,20 @@ __device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp
       if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&bk[found].count, (unsigned)__popc(peers));
     }
     cfg_bucket[q] = found;
+    // sub-order within the bucket: GPT-2 configurations by log2 of the
+    // microbatch size (a warp of equal microbatches has equal op costs for
+    // equal T and topology, so its binade crossings coincide), others 0
+    uint32_t so = 0;
+    if (DISTIR_SUBORDER && c.M.kind == 1) {
+      const int64_t mb = c.B / (c.D * c.K);
+      so = mb > 0 ? (uint32_t)(63 - __clzll((unsigned long long)mb)) : 0u;
+      so = so < kSubSlots ? so : kSubSlots - 1;
+    }
+    atomicAdd(&sub[found * kSubSlots + so], 1u);
     pc_out[q] = PCfg{c.B, (uint32_t)q, (uint16_t)c.K, (uint8_t)c.P,
                      c.mi < 0 ? kSynthModel : (uint8_t)c.mi, (uint8_t)c.topo,
                      (uint8_t)(63 - __clzll((unsigned long long)c.D)),
-                     (uint8_t)(63 - __clzll((unsigned long long)c.T)), 0};
+                     (uint8_t)(63 - __clzll((unsigned long long)c.T)), (uint8_t)so};
   }
   // warp-aggregated statistics
   for (int o = 16; o > 0; o >>= 1) {
@@ -388,8 +403,9 @@ __global__ void k_enumerate(const SpecBlock* __restrict__ spp, const DExplicit* 
                             Bucket* __restrict__ bk, uint32_t* __restrict__ cfg_bucket,
                             double* __restrict__ ms_out, int64_t* __restrict__ pk_out,
                             uint32_t* __restrict__ rs_out, double* __restrict__ tp_out,
-                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr) {
-  enumerate_body(spp, ex, bk, cfg_bucket, ms_out, pk_out, rs_out, tp_out, pc_out, hdr, blockIdx.x, gridDim.x);
+                            PCfg* __restrict__ pc_out, WsHeader* __restrict__ hdr,
+                            uint32_t* __restrict__ sub) {
+  enumerate_body(spp, ex, bk, cfg_bucket, ms_out, pk_out, rs_out, tp_out, pc_out, hdr, sub, blockIdx.x, gridDim.x);
 }
 
 __device__ __forceinline__ uint32_t pow2ceil32(uint32_t x) {
@@ -439,7 +455,7 @@ __host__ __device__ __forceinline__ bool mlp_plain_shape(uint32_t L, uint32_t P,
           (K <= 32 && lanes <= 8));
 }
 __device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
-                                          const PlanBudget& budget) {
+                                          const PlanBudget& budget, uint32_t* __restrict__ sub) {
   __shared__ unsigned int s_items[kGroups][kNumClasses];
   __shared__ unsigned int s_alt[kGroups][kNumClasses][kMaxSplit + 1];   // items at split j
   __shared__ unsigned char s_shift[kGroups][kNumClasses];
@@ -517,6 +533,20 @@ __device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __r
     }
     B.cfg_base = atomicAdd(&s_cfg, cnt[u]);
     B.cursor = 0;
+    {   // the sub-orders' cursors start at their exclusive prefix (positions
+        // within the bucket); the counts were written by k_enumerate
+      uint32_t* sc = sub + (size_t)b * kSubSlots;
+      uint32_t* cu = sub + (size_t)kBucketSlots * kSubSlots + (size_t)b * kSubSlots;
+      uint32_t v[kSubSlots];
+#pragma unroll
+      for (int j = 0; j < kSubSlots; j++) v[j] = sc[j];      // independent loads first
+      uint32_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < kSubSlots; j++) {
+        cu[j] = acc;
+        acc += v[j];
+      }
+    }
     atomicAdd(&s_nb, 1u);
   }
   __syncthreads();
@@ -598,13 +628,14 @@ __device__ __forceinline__ void plan_body(Bucket* __restrict__ bk, WsHeader* __r
 }
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan(Bucket* __restrict__ bk, WsHeader* __restrict__ hdr,
-                                                       PlanBudget budget) {
-  plan_body(bk, hdr, budget);
+                                                       PlanBudget budget, uint32_t* __restrict__ sub) {
+  plan_body(bk, hdr, budget, sub);
 }
 
 __device__ __forceinline__ void scatter_body(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
                           const uint32_t* __restrict__ cfg_bucket, const PCfg* __restrict__ pc,
-                          PCfg* __restrict__ perm, Item* __restrict__ items, int bid, int nblk) {
+                          PCfg* __restrict__ perm, Item* __restrict__ items, uint32_t* __restrict__ sub,
+                          int bid, int nblk) {
   const int64_t nloc = spp->n_local;
   for (int64_t q = bid * (int64_t)blockDim.x + threadIdx.x; q < nloc;
        q += (int64_t)nblk * blockDim.x) {
@@ -617,16 +648,20 @@ __device__ __forceinline__ void scatter_body(const SpecBlock* __restrict__ spp, 
     // out positions groups configurations into warps differently, and on W3
     // that grouping is 5 % faster, r02ax -- W5's prepare is 28 % faster with
     // the aggregation)
+    // the position within the bucket comes from its sub-order's cursor
+    // (k_plan set it to the sub-order's first position)
+    const uint32_t si = b * kSubSlots + pc[q].pad;
+    uint32_t* cur = sub + (size_t)kBucketSlots * kSubSlots + si;
     uint32_t pos;
     if (DISTIR_SCATTER_AGG && nloc >= kScatterAggMin) {
-      const unsigned peers = __match_any_sync(__activemask(), b);
+      const unsigned peers = __match_any_sync(__activemask(), si);
       const int lead = __ffs(peers) - 1, me = threadIdx.x & 31;
       uint32_t base = 0;
-      if (me == lead) base = atomicAdd(&bk[b].cursor, (unsigned)__popc(peers));
+      if (me == lead) base = atomicAdd(cur, (unsigned)__popc(peers));
       base = __shfl_sync(peers, base, lead);
       pos = base + (uint32_t)__popc(peers & ((1u << me) - 1u));
     } else {
-      pos = atomicAdd(&bk[b].cursor, 1u);
+      pos = atomicAdd(cur, 1u);
     }
     const uint32_t cpw = bk[b].cpw;
     perm[bk[b].cfg_base + pos] = pc[q];
@@ -644,24 +679,28 @@ __device__ __forceinline__ void scatter_body(const SpecBlock* __restrict__ spp, 
 
 __global__ void k_scatter(const SpecBlock* __restrict__ spp, Bucket* __restrict__ bk,
                           const uint32_t* __restrict__ cfg_bucket, const PCfg* __restrict__ pc,
-                          PCfg* __restrict__ perm, Item* __restrict__ items) {
-  scatter_body(spp, bk, cfg_bucket, pc, perm, items, blockIdx.x, gridDim.x);
+                          PCfg* __restrict__ perm, Item* __restrict__ items, uint32_t* __restrict__ sub) {
+  scatter_body(spp, bk, cfg_bucket, pc, perm, items, sub, blockIdx.x, gridDim.x);
 }
 
 // Empty bucket table and zero header (every launch starts from them).
-__device__ __forceinline__ void reset_body(Bucket* bk, WsHeader* hdr, int bid, int nblk) {
+__device__ __forceinline__ void reset_body(Bucket* bk, WsHeader* hdr, uint32_t* sub, int bid, int nblk) {
   for (int i = bid * blockDim.x + threadIdx.x; i < kBucketSlots; i += nblk * blockDim.x) {
     Bucket b{};
     b.key = kEmptyKey;
     bk[i] = b;
   }
+  // the sub-order counts (the cursors are set by k_plan)
+  uint4* s4 = reinterpret_cast<uint4*>(sub);
+  for (int i = bid * blockDim.x + threadIdx.x; i < kBucketSlots * kSubSlots / 4; i += nblk * blockDim.x)
+    s4[i] = make_uint4(0u, 0u, 0u, 0u);
   if (bid == 0 && threadIdx.x == 0) {
     WsHeader h{};
     *hdr = h;
   }
 }
 
-__global__ void k_reset(Bucket* bk, WsHeader* hdr) { reset_body(bk, hdr, blockIdx.x, gridDim.x); }
+__global__ void k_reset(Bucket* bk, WsHeader* hdr, uint32_t* sub) { reset_body(bk, hdr, sub, blockIdx.x, gridDim.x); }
 
 
 #endif  // DISTIR_SIM_TU
