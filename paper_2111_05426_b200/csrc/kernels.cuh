@@ -182,9 +182,12 @@ __device__ __forceinline__ void op_counts(const Cfg& c, int64_t& events, int64_t
 __device__ __forceinline__ bool is_zero(const Cfg& c) { return c.M.kind == 0 && c.M.zero && c.D > 1; }
 
 #ifndef DISTIR_SUBORDER
-#define DISTIR_SUBORDER 1               // GPT-2: order a bucket's configurations by microbatch size
+#define DISTIR_SUBORDER 3               // GPT-2: order a bucket's configurations by microbatch size
+                                        // (1: log2 m; 3: (log2 m, log2 T) folded into 32 slots,
+                                        // r02bl: W3 k_simulate 0.0923 -> 0.0901 ms; 2: 128 slots,
+                                        // k_simulate 0.086 but prepare +14 us, r02bk)
 #endif
-constexpr int kSubSlots = 32;           // per-bucket sub-orders (log2 of the microbatch size)
+constexpr int kSubSlots = DISTIR_SUBORDER == 2 ? 128 : 32;   // per-bucket sub-orders
 #ifndef DISTIR_GPT2_GROUP
 #define DISTIR_GPT2_GROUP 0             // GPT-2 buckets also keyed by the microbatch size (experiment, off)
 #endif
@@ -376,6 +379,13 @@ __device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp
     if (DISTIR_SUBORDER && c.M.kind == 1) {
       const int64_t mb = c.B / (c.D * c.K);
       so = mb > 0 ? (uint32_t)(63 - __clzll((unsigned long long)mb)) : 0u;
+#if DISTIR_SUBORDER == 2
+      // ... and by tensor-parallel degree (equal m and T: equal op costs)
+      so = (so < 24 ? so : 24u) * 5u + (uint32_t)(63 - __clzll((unsigned long long)c.T)) % 5u;
+#elif DISTIR_SUBORDER == 3
+      // (m, T) folded into the 32 slots
+      so = (so * 5u + (uint32_t)(63 - __clzll((unsigned long long)c.T))) & 31u;
+#endif
       so = so < kSubSlots ? so : kSubSlots - 1;
     }
     atomicAdd(&sub[found * kSubSlots + so], 1u);
