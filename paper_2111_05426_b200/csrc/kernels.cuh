@@ -183,11 +183,14 @@ __device__ __forceinline__ bool is_zero(const Cfg& c) { return c.M.kind == 0 && 
 
 #ifndef DISTIR_SUBORDER
 #define DISTIR_SUBORDER 3               // GPT-2: order a bucket's configurations by microbatch size
-                                        // (1: log2 m; 3: (log2 m, log2 T) folded into 32 slots,
+                                        // (1: log2 m; 3: (log2 m, log2 T) folded into the slots,
                                         // r02bl: W3 k_simulate 0.0923 -> 0.0901 ms; 2: 128 slots,
                                         // k_simulate 0.086 but prepare +14 us, r02bk)
 #endif
-constexpr int kSubSlots = DISTIR_SUBORDER == 2 ? 128 : 32;   // per-bucket sub-orders
+#ifndef DISTIR_SUBSLOTS
+#define DISTIR_SUBSLOTS 16              // (32: W3 step 0.1235 ms; 16: 0.1226 -- prepare -2 us, simulate +1 us, r02bn)
+#endif
+constexpr int kSubSlots = DISTIR_SUBORDER == 2 ? 128 : DISTIR_SUBSLOTS;   // per-bucket sub-orders
 #ifndef DISTIR_GPT2_GROUP
 #define DISTIR_GPT2_GROUP 0             // GPT-2 buckets also keyed by the microbatch size (experiment, off)
 #endif
@@ -384,7 +387,7 @@ __device__ __forceinline__ void enumerate_body(const SpecBlock* __restrict__ spp
       so = (so < 24 ? so : 24u) * 5u + (uint32_t)(63 - __clzll((unsigned long long)c.T)) % 5u;
 #elif DISTIR_SUBORDER == 3
       // (m, T) folded into the 32 slots
-      so = (so * 5u + (uint32_t)(63 - __clzll((unsigned long long)c.T))) & 31u;
+      so = (so * 5u + (uint32_t)(63 - __clzll((unsigned long long)c.T))) & (uint32_t)(kSubSlots - 1);
 #endif
       so = so < kSubSlots ? so : kSubSlots - 1;
     }
